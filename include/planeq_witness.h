@@ -1,0 +1,181 @@
+/*
+ * planeq_witness.h -- C-ABI of the sm_100a stage-discharge engine.
+ *
+ * This boundary replaces the reference's per-stage discharge:
+ *   pkg/src/planeq/stages.py:267  run_stage(plan, stage, solver_argv, timeout_s)
+ * and the pieces it drives:
+ *   pkg/src/planeq/ops.py:923     sym_execute      (symbolic execution of both sub-DFGs)
+ *   pkg/src/planeq/smt.py:318     SolverSession.check  (SMT decision of residual pairs)
+ *   pkg/src/planeq/stages.py:221  _confirm          (replay of a candidate countermodel)
+ *
+ * Instead of symbolic expressions plus an SMT query, every stage is compiled
+ * (on the host, in C++) from a flat tensor-op program into straight-line
+ * scalar bytecode over the prime field F_p, p = 2^31 - 1, and evaluated on the
+ * GPU for a batch of random witness assignments; uninterpreted functions
+ * (EXP, RSQRT, SIGMOID) are keyed hash functions F_p -> F_p. A stage is
+ * refuted iff some valid witness makes an obligation's two sides differ; the
+ * failing witness is an exact integer counterexample.
+ *
+ * All entry points return 0 on success and a negative PQW_E* code on failure;
+ * pqw_last_error() describes the last failure on the calling thread.
+ * No torch types cross this boundary: plain pointers and sizes only.
+ */
+#ifndef PLANEQ_WITNESS_H
+#define PLANEQ_WITNESS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PQW_ABI_VERSION 1
+#define PQW_PRIME 2147483647u /* 2^31 - 1 */
+
+/* error codes */
+#define PQW_OK 0
+#define PQW_EINVAL (-1)   /* malformed program / argument */
+#define PQW_ENODEV (-2)   /* no CUDA device or driver */
+#define PQW_ECUDA (-3)    /* CUDA runtime failure */
+#define PQW_ESTATE (-4)   /* call out of order (e.g. run before compile) */
+
+/* per-stage compile status (pqw_stage_add out_status[0]) */
+#define PQW_STAGE_OK 0            /* residual obligations go to the GPU            */
+#define PQW_STAGE_PROVEN 1        /* every obligation closed by value numbering   */
+#define PQW_STAGE_REFUTED_CONST 2 /* constant/int obligation differs; info = obl   */
+#define PQW_STAGE_PAR_DIV0 3      /* parallel side divides by a constant zero      */
+#define PQW_STAGE_LOG_DIV0 4      /* logical side divides by a constant zero       */
+#define PQW_STAGE_BAD_INDEX 5     /* embedding id outside its table                 */
+
+/* tensor-op program opcodes (pqw_stage_add ir stream) */
+enum pqw_top {
+  PQW_T_VARS = 1,      /* out <- fresh variables; attr: var-table offset           */
+  PQW_T_INTS = 2,      /* out <- integer constants; attr: const-table offset        */
+  PQW_T_SLICE = 3,     /* out <- in[lo.. lo+out.shape]; attrs: lo per axis          */
+  PQW_T_RESID = 4,     /* out <- in0 - sum(in1..)  (last partial member)            */
+  PQW_T_CHECK = 5,     /* obligations in0[i] == in1[i]; attr: first obligation id   */
+  PQW_T_CHECKSUM = 6,  /* obligations in0[i] == sum_k ink[i]; attr: first obl id   */
+  PQW_T_SIDE = 7,      /* attr: 0 = logical ops follow, 1 = parallel ops follow     */
+  PQW_T_ADD = 16, PQW_T_SUB, PQW_T_MUL, PQW_T_DIV, PQW_T_DROPOUT, PQW_T_SILU_GRAD,
+  PQW_T_IDENTITY, PQW_T_SCALE, PQW_T_SHIFT, PQW_T_POW, PQW_T_RSQRT, PQW_T_SILU,
+  PQW_T_MOVE, PQW_T_SOFTMAX, PQW_T_CREATE_MASK, PQW_T_APPLY_MASK, PQW_T_VIEW,
+  PQW_T_TRANSPOSE, PQW_T_EXPAND, PQW_T_SUM, PQW_T_MEAN, PQW_T_MATMUL, PQW_T_EINSUM,
+  PQW_T_FULL, PQW_T_CHUNK, PQW_T_EMBEDDING, PQW_T_EMBEDDING_GRAD, PQW_T_GNORM_SQ,
+  PQW_T_ALL_REDUCE, PQW_T_ALL_GATHER, PQW_T_REDUCE_SCATTER, PQW_T_ALL_TO_ALL
+};
+
+/* scalar bytecode opcodes (what the GPU interprets; see pqw_stage_bytecode) */
+enum pqw_bop {
+  PQW_B_END = 0, PQW_B_CONST, PQW_B_VAR, PQW_B_ADD, PQW_B_SUB, PQW_B_MUL, PQW_B_NEG,
+  PQW_B_DIV, PQW_B_HASH, PQW_B_ACC_MUL, PQW_B_ACC_MAC, PQW_B_ACC_LD, PQW_B_ACC_ADD,
+  PQW_B_ACC_ST, PQW_B_CHK, PQW_B_DEN, PQW_B_ACC_MACF,
+  PQW_B_NUM_OPS
+};
+
+typedef struct pqw_ins {
+  uint32_t op;  /* pqw_bop */
+  uint32_t dst; /* slot, or obligation id for CHK */
+  uint32_t a;   /* slot / residue / var index */
+  uint32_t b;   /* slot / function index */
+} pqw_ins;
+
+typedef struct pqw_engine pqw_engine;
+
+/* ABI version (PQW_ABI_VERSION) -- lets the host refuse a stale library. */
+int pqw_abi_version(void);
+
+/* Human-readable description of the last error on this thread. */
+const char* pqw_last_error(void);
+
+/* Number of visible CUDA devices (0 when no driver/device), never fails. */
+int pqw_device_count(void);
+
+/*
+ * Create an engine bound to `device`. `seed` keys the witness stream;
+ * `fn_keys[3]` key the uninterpreted functions EXP, RSQRT, SIGMOID
+ * (host-derived from seed, see paper_2506_15961_b200/field.py).
+ * Compilation works without a device; run/probe need one.
+ */
+int pqw_engine_create(int device, uint64_t seed, const uint64_t fn_keys[3],
+                      pqw_engine** out);
+void pqw_engine_destroy(pqw_engine* e);
+
+/*
+ * Compile one stage's tensor-op program (stream layout documented in
+ * paper_2506_15961_b200/lower.py). consts: n_consts triples
+ * (residue, exact_num, exact_den) -- exact_den == 0 marks an inexact constant.
+ * var_keys: per-variable 64-bit keys. out_status[0] = PQW_STAGE_*,
+ * out_status[1] = info (obligation id for REFUTED_CONST / BAD_INDEX),
+ * out_status[2] = obligation count, out_status[3] = obligations closed by value
+ * numbering, out_status[4] = residual obligations, out_status[5] = bytecode
+ * length, out_status[6] = slots, out_status[7] = max numerator degree of a
+ * residual obligation (saturating), out_status[8..9] = lhs/rhs residues of the
+ * REFUTED_CONST obligation, out_status[10..11] = their exact integer values
+ * (INT64_MIN when not an exact integer), out_status[12] = field ops executed
+ * per witness, out_status[13] = variables, out_status[14..15] reserved.
+ * Returns the stage index (>= 0) or a negative error.
+ */
+int pqw_stage_add(pqw_engine* e, const int32_t* ir, size_t ir_len,
+                  const int64_t* consts, size_t n_consts,
+                  const uint64_t* var_keys, size_t n_vars, int64_t out_status[16]);
+
+/* Drop every compiled stage (device image included). */
+int pqw_reset(pqw_engine* e);
+
+/* Copy out the compiled bytecode of a stage (for inspection / CPU tests).
+ * Returns the instruction count; copies min(count, cap) instructions. */
+long pqw_stage_bytecode(pqw_engine* e, int stage, pqw_ins* out, size_t cap,
+                        uint32_t* n_slots);
+
+/* Variables in the cone of obligation `obl` of `stage` (sorted var ids);
+ * returns the count, copies at most cap. */
+long pqw_obligation_support(pqw_engine* e, int stage, uint32_t obl,
+                            uint32_t* out, size_t cap);
+
+/* Upload all compiled stages as one device image (plus result buffers). */
+int pqw_upload(pqw_engine* e);
+
+/*
+ * Evaluate every uploaded GPU stage on witnesses [0, n_witness) on `stream`
+ * (a cudaStream_t, NULL = legacy default). Asynchronous; results are read
+ * with pqw_results after a stream sync (pqw_results syncs).
+ */
+int pqw_launch(pqw_engine* e, uint32_t n_witness, void* stream);
+
+/*
+ * Per-stage results of the last launch (arrays of length n_stages).
+ * first_bad = (witness << 32) | obligation of the smallest failing witness
+ * (UINT64_MAX when none); n_valid = witnesses with every denominator nonzero;
+ * n_bad = valid witnesses with at least one failing obligation.
+ */
+int pqw_results(pqw_engine* e, uint64_t* first_bad, uint32_t* n_valid,
+                uint32_t* n_bad, size_t n_stages);
+
+/*
+ * Re-evaluate one stage at one witness and report both sides of obligation
+ * `obl` plus the values of the stage's variables (var_vals, length n_vars of
+ * that stage, may be NULL).
+ */
+int pqw_probe(pqw_engine* e, int stage, uint32_t witness, uint32_t obl,
+              uint32_t* lhs, uint32_t* rhs, uint32_t* var_vals, size_t n_vars);
+
+/* Device time of the last launch in milliseconds (CUDA events on the launch stream). */
+int pqw_last_launch_ms(pqw_engine* e, float* ms);
+
+/* Totals of the uploaded image: out[0] = stages on the GPU, out[1] = bytecode
+ * instructions, out[2] = max slots of a stage, out[3] = work items per witness
+ * tile, out[4 + op] = instructions of each pqw_bop (out has 4 + PQW_B_NUM_OPS
+ * entries). */
+int pqw_image_stats(pqw_engine* e, uint64_t* out, size_t cap);
+
+/* Measured integer-pipe ceiling of this device: field ops per second of
+ * register-resident, decode-free kernels: out[0] = F_p multiplies, out[1] =
+ * F_p adds, out[2] = keyed-hash evaluations. The roofline denominator of the
+ * interpreter (bench.py). */
+int pqw_peak_fieldops(int device, double out[3]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PLANEQ_WITNESS_H */

@@ -1,0 +1,38 @@
+// compiler.hpp -- host-side stage compiler: tensor-op program -> scalar F_p bytecode.
+#pragma once
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/planeq_witness.h"
+
+namespace pqw {
+
+struct CompiledStage {
+  int status = PQW_STAGE_OK;
+  int64_t info = -1;
+  uint32_t n_obligations = 0;
+  uint32_t n_fast = 0;
+  uint32_t n_residual = 0;
+  uint32_t n_slots = 0;
+  uint32_t n_vars = 0;
+  uint32_t var_base = 0;       // first global var index of this stage
+  uint64_t degree = 0;
+  uint64_t field_ops = 0;      // field operations per witness (roofline numerator)
+  int64_t const_lhs = 0, const_rhs = 0, exact_lhs = INT64_MIN, exact_rhs = INT64_MIN;
+  std::vector<pqw_ins> code;   // terminated by PQW_B_END when status == OK
+};
+
+// Compile one stage. `var_base` is the global index of the stage's first
+// variable (VAR instructions carry global indices). Throws std::runtime_error
+// on malformed input.
+CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* consts,
+                            size_t n_consts, uint32_t n_vars, uint32_t var_base,
+                            const uint64_t fn_keys[3]);
+
+// Variables (global indices) in the cone of obligation `obl`, by backward
+// slicing the bytecode.
+std::vector<uint32_t> obligation_support(const CompiledStage& st, uint32_t obl);
+
+}  // namespace pqw

@@ -1,0 +1,745 @@
+// witness_kernel.cu -- sm_100a bytecode interpreter for stage discharge, and
+// the extern "C" engine behind include/planeq_witness.h.
+//
+// Work decomposition: a work item is (stage, CTA tile). A CTA of WARPS warps
+// takes WARPS consecutive warp tiles of one stage; each warp evaluates the
+// stage program for WT = 32 * VW witnesses, lane l owning witnesses
+// [wtile*WT + VW*l, +VW) and moving them with one vector access per slot
+// read/write. The slot file is per warp, witness-innermost (slot s = 32
+// vec_t = 256 contiguous bytes): the first `smem_slots` slots live in shared
+// memory, the rest in per-warp global scratch (L1/L2-resident). The grid is
+// persistent (SMs x occupancy) and pulls items from an atomic counter; stages
+// are ordered by descending cost so the longest programs start first.
+//
+// The instruction stream is warp-uniform (every lane runs the same stage
+// program) and shared by the CTA's warps (L1 hits after the first warp), so
+// decode is a broadcast load, prefetched one instruction ahead, plus an
+// indirect branch that never diverges.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "compiler.hpp"
+#include "field.hpp"
+
+namespace pqw {
+namespace {
+
+// Each warp evaluates one stage program for WT = 32 * VW witnesses; a CTA of
+// WARPS warps runs WARPS consecutive witness tiles of the same stage, so the
+// instruction stream is fetched from L2 once and served to the other warps
+// from L1. VW witnesses per thread move with one vector access per slot.
+constexpr int VW = 2;
+constexpr int WARPS = 4;
+constexpr int BLOCK = 32 * WARPS;
+constexpr int WT = 32 * VW;          // witnesses per warp tile
+constexpr int TW = WT * WARPS;       // witnesses per CTA work item
+
+typedef uint2 vec_t;                 // VW u32 lanes
+static_assert(VW == 2, "vec_t is uint2");
+
+struct StageDesc {
+  uint32_t code_off;
+  uint32_t n_slots;
+  uint32_t var_base;
+  uint32_t result;  // index into result arrays
+};
+
+struct Params {
+  const uint4* code;
+  const StageDesc* stages;
+  const uint32_t* work;      // stage-desc index per work stage
+  const uint64_t* var_keys;
+  const uint64_t* fn_keys;   // 3 entries
+  uint32_t* counter;         // work-item counter
+  vec_t* scratch;            // per-warp overflow slot files
+  unsigned long long* first_bad;
+  uint32_t* n_valid;
+  uint32_t* n_bad;
+  uint32_t n_items;
+  uint32_t tiles;            // CTA work items per stage
+  uint32_t n_witness;
+  uint32_t smem_slots;       // slots per warp held in shared memory
+  uint32_t overflow_slots;   // per-warp scratch capacity in slots
+  // probe mode
+  uint32_t probe_w;
+  uint32_t probe_obl;
+  uint32_t* probe_out;       // [lhs, rhs]
+  uint32_t* probe_vars;
+};
+
+__device__ __forceinline__ vec_t vadd(vec_t a, vec_t b) { return make_uint2(fadd(a.x, b.x), fadd(a.y, b.y)); }
+__device__ __forceinline__ vec_t vsub(vec_t a, vec_t b) { return make_uint2(fsub(a.x, b.x), fsub(a.y, b.y)); }
+__device__ __forceinline__ vec_t vmul(vec_t a, vec_t b) { return make_uint2(fmul(a.x, b.x), fmul(a.y, b.y)); }
+
+template <bool PROBE>
+__device__ __forceinline__ void run_item(const Params& p, vec_t* wsm, vec_t* wgs, uint32_t sdesc,
+                                         uint32_t wtile) {
+  const StageDesc sd = p.stages[sdesc];
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t w0 = PROBE ? p.probe_w : wtile * WT + lane * VW;
+  const uint32_t nsm = p.smem_slots;
+
+  // slot s of this warp: 32 vec_t (256 B) in shared memory or global scratch
+  auto ptr = [&](uint32_t s) -> vec_t* {
+    return s < nsm ? wsm + (size_t)s * 32 + lane : wgs + (size_t)(s - nsm) * 32 + lane;
+  };
+
+  bool valid0 = PROBE ? lane == 0 : w0 < p.n_witness;
+  bool valid1 = PROBE ? false : (w0 + 1) < p.n_witness;
+  uint32_t bad0 = 0xFFFFFFFFu, bad1 = 0xFFFFFFFFu;
+  uint64_t acc0 = 0, acc1 = 0;
+
+  const uint4* code = p.code + sd.code_off;
+  uint4 nxt = __ldg(code);
+  for (uint32_t pc = 0;; ++pc) {
+    const uint4 in = nxt;
+    nxt = __ldg(code + pc + 1);  // prefetch: the image is padded with END, never past the end
+    switch (in.x) {
+      case PQW_B_END:
+        goto done;
+      case PQW_B_CONST:
+        *ptr(in.y) = make_uint2(in.z, in.z);
+        break;
+      case PQW_B_VAR: {
+        const uint64_t key = __ldg(p.var_keys + in.z);
+        vec_t v = make_uint2(witness_value(key, w0), witness_value(key, w0 + 1));
+        if (PROBE && lane == 0) p.probe_vars[in.z - sd.var_base] = v.x;
+        *ptr(in.y) = v;
+        break;
+      }
+      case PQW_B_ADD:
+        *ptr(in.y) = vadd(*ptr(in.z), *ptr(in.w));
+        break;
+      case PQW_B_SUB:
+        *ptr(in.y) = vsub(*ptr(in.z), *ptr(in.w));
+        break;
+      case PQW_B_MUL:
+        *ptr(in.y) = vmul(*ptr(in.z), *ptr(in.w));
+        break;
+      case PQW_B_NEG: {
+        vec_t a = *ptr(in.z);
+        *ptr(in.y) = make_uint2(fneg(a.x), fneg(a.y));
+        break;
+      }
+      case PQW_B_DIV: {
+        vec_t a = *ptr(in.z), b = *ptr(in.w);
+        *ptr(in.y) = make_uint2(fmul(a.x, finv(b.x)), fmul(a.y, finv(b.y)));
+        break;
+      }
+      case PQW_B_HASH: {
+        const uint64_t key = __ldg(p.fn_keys + in.w);
+        vec_t a = *ptr(in.z);
+        *ptr(in.y) = make_uint2(uf_apply(key, a.x), uf_apply(key, a.y));
+        break;
+      }
+      case PQW_B_ACC_LD: {
+        vec_t a = *ptr(in.z);
+        acc0 = a.x;
+        acc1 = a.y;
+        break;
+      }
+      case PQW_B_ACC_ADD: {
+        vec_t a = *ptr(in.z);
+        acc0 += a.x;
+        acc1 += a.y;
+        break;
+      }
+      case PQW_B_ACC_MUL: {
+        vec_t a = *ptr(in.z), b = *ptr(in.w);
+        acc0 = (uint64_t)a.x * b.x;
+        acc1 = (uint64_t)a.y * b.y;
+        break;
+      }
+      case PQW_B_ACC_MACF:
+        acc0 = ffold64(acc0);
+        acc1 = ffold64(acc1);
+        // fallthrough
+      case PQW_B_ACC_MAC: {
+        vec_t a = *ptr(in.z), b = *ptr(in.w);
+        acc0 += (uint64_t)a.x * b.x;
+        acc1 += (uint64_t)a.y * b.y;
+        break;
+      }
+      case PQW_B_ACC_ST:
+        *ptr(in.y) = make_uint2(fred64(acc0), fred64(acc1));
+        break;
+      case PQW_B_CHK: {
+        vec_t a = *ptr(in.z), b = *ptr(in.w);
+        if (PROBE && in.y == p.probe_obl && lane == 0) {
+          p.probe_out[0] = a.x;
+          p.probe_out[1] = b.x;
+        }
+        if (a.x != b.x) bad0 = min(bad0, in.y);
+        if (a.y != b.y) bad1 = min(bad1, in.y);
+        break;
+      }
+      case PQW_B_DEN: {
+        vec_t a = *ptr(in.z);
+        if (a.x == 0) valid0 = false;
+        if (a.y == 0) valid1 = false;
+        break;
+      }
+      default:
+        goto done;  // unreachable for a well-formed image
+    }
+  }
+done:
+  if (PROBE) return;
+  unsigned long long best = ~0ull;
+  uint32_t nv = 0, nb = 0;
+  if (valid0) {
+    nv++;
+    if (bad0 != 0xFFFFFFFFu) {
+      nb++;
+      best = ((unsigned long long)w0 << 32) | bad0;
+    }
+  }
+  if (valid1) {
+    nv++;
+    if (bad1 != 0xFFFFFFFFu) {
+      nb++;
+      unsigned long long k = ((unsigned long long)(w0 + 1) << 32) | bad1;
+      best = k < best ? k : best;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    nv += __shfl_down_sync(0xFFFFFFFFu, nv, off);
+    nb += __shfl_down_sync(0xFFFFFFFFu, nb, off);
+    unsigned long long o = __shfl_down_sync(0xFFFFFFFFu, best, off);
+    best = o < best ? o : best;
+  }
+  if (lane == 0) {
+    if (nv) atomicAdd(p.n_valid + sd.result, nv);
+    if (nb) atomicAdd(p.n_bad + sd.result, nb);
+    if (best != ~0ull) atomicMin(p.first_bad + sd.result, best);
+  }
+}
+
+template <bool PROBE>
+__global__ void __launch_bounds__(BLOCK) eval_kernel(Params p) {
+  extern __shared__ vec_t smem[];
+  __shared__ uint32_t s_item;
+  const uint32_t warp = threadIdx.x >> 5;
+  vec_t* wsm = smem + (size_t)warp * p.smem_slots * 32;
+  vec_t* wgs = p.scratch + ((size_t)blockIdx.x * WARPS + warp) * p.overflow_slots * 32;
+  if (PROBE) {
+    if (warp == 0) run_item<true>(p, wsm, wgs, p.work[0], 0);
+    return;
+  }
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(p.counter, 1u);
+    __syncthreads();
+    const uint32_t item = s_item;
+    __syncthreads();
+    if (item >= p.n_items) break;
+    const uint32_t tile = item % p.tiles;
+    const uint32_t wtile = tile * WARPS + warp;
+    // warps past the last witness skip the program entirely
+    if (wtile * WT < p.n_witness) run_item<false>(p, wsm, wgs, p.work[item / p.tiles], wtile);
+  }
+}
+
+// -- integer-pipe ceiling: register-resident field arithmetic, no decode, no memory.
+// KIND 0: fmul chains, 1: fadd chains, 2: keyed hash (mix64 + to_field).
+template <int KIND>
+__global__ void __launch_bounds__(256) peak_kernel(uint32_t* sink, int iters, uint32_t salt) {
+  uint32_t a[8], b[8];
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    a[j] = (t * 2654435761u + j * 40503u + salt) % P;
+    b[j] = (t * 2246822519u + j * 9973u + 7u) % P;
+  }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (KIND == 0) a[j] = fmul(a[j], b[j]);
+        else if (KIND == 1) a[j] = fadd(a[j], b[j]);
+        else a[j] = uf_apply(0x9E3779B97F4A7C15ull + b[j], a[j]);
+      }
+    }
+  }
+  uint32_t x = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) x ^= a[j];
+  if (x == salt * 2654435761u + 1u) sink[t] = x;  // opaque to the compiler: keeps chains live
+}
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CU(call)                                                              \
+  do {                                                                        \
+    cudaError_t e_ = (call);                                                  \
+    if (e_ != cudaSuccess)                                                    \
+      return fail(PQW_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+}  // namespace
+}  // namespace pqw
+
+struct pqw_engine {
+  int device = 0;
+  uint64_t seed = 0;
+  uint64_t fn_keys[3] = {0, 0, 0};
+  std::vector<pqw::CompiledStage> stages;
+  std::vector<uint64_t> var_keys;
+  // device image
+  bool uploaded = false;
+  std::vector<int> gpu_stage_of;   // result index -> stage index
+  uint4* d_code = nullptr;
+  pqw::StageDesc* d_stages = nullptr;
+  uint32_t* d_work = nullptr;
+  uint64_t* d_var_keys = nullptr;
+  uint64_t* d_fn_keys = nullptr;
+  uint32_t* d_counter = nullptr;
+  pqw::vec_t* d_scratch = nullptr;
+  unsigned long long* d_first_bad = nullptr;
+  uint32_t* d_n_valid = nullptr;
+  uint32_t* d_n_bad = nullptr;
+  uint32_t* d_probe = nullptr;
+  size_t scratch_bytes = 0;
+  uint32_t n_gpu_stages = 0;
+  uint32_t max_slots = 0;
+  uint32_t smem_slots = 0;
+  uint32_t overflow_slots = 0;
+  uint32_t grid = 0;
+  uint64_t n_code = 0;
+  uint64_t op_hist[PQW_B_NUM_OPS] = {};
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool timed = false;
+  std::vector<unsigned long long> h_first_bad;
+  std::vector<uint32_t> h_valid, h_bad;
+  bool results_ready = false;
+
+  void free_device() {
+    cudaFree(d_code);
+    cudaFree(d_stages);
+    cudaFree(d_work);
+    cudaFree(d_var_keys);
+    cudaFree(d_fn_keys);
+    cudaFree(d_counter);
+    cudaFree(d_scratch);
+    cudaFree(d_first_bad);
+    cudaFree(d_n_valid);
+    cudaFree(d_n_bad);
+    cudaFree(d_probe);
+    d_code = nullptr;
+    d_stages = nullptr;
+    d_work = nullptr;
+    d_var_keys = nullptr;
+    d_fn_keys = nullptr;
+    d_counter = nullptr;
+    d_scratch = nullptr;
+    d_first_bad = nullptr;
+    d_n_valid = nullptr;
+    d_n_bad = nullptr;
+    d_probe = nullptr;
+    uploaded = false;
+    results_ready = false;
+  }
+};
+
+using pqw::fail;
+
+extern "C" {
+
+int pqw_abi_version(void) { return PQW_ABI_VERSION; }
+
+const char* pqw_last_error(void) { return pqw::g_err.c_str(); }
+
+int pqw_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int pqw_engine_create(int device, uint64_t seed, const uint64_t fn_keys[3], pqw_engine** out) {
+  if (!out || !fn_keys) return fail(PQW_EINVAL, "null argument");
+  auto* e = new pqw_engine();
+  e->device = device;
+  e->seed = seed;
+  for (int i = 0; i < 3; ++i) e->fn_keys[i] = fn_keys[i];
+  *out = e;
+  return PQW_OK;
+}
+
+void pqw_engine_destroy(pqw_engine* e) {
+  if (!e) return;
+  if (e->uploaded || e->d_code) {
+    cudaSetDevice(e->device);
+    e->free_device();
+  }
+  if (e->ev0) cudaEventDestroy(e->ev0);
+  if (e->ev1) cudaEventDestroy(e->ev1);
+  delete e;
+}
+
+int pqw_stage_add(pqw_engine* e, const int32_t* ir, size_t ir_len, const int64_t* consts,
+                  size_t n_consts, const uint64_t* var_keys, size_t n_vars,
+                  int64_t out_status[16]) {
+  if (!e || !ir || !out_status) return fail(PQW_EINVAL, "null argument");
+  if (n_vars && !var_keys) return fail(PQW_EINVAL, "null var_keys");
+  if (n_consts && !consts) return fail(PQW_EINVAL, "null consts");
+  const uint32_t base = (uint32_t)e->var_keys.size();
+  pqw::CompiledStage st;
+  try {
+    st = pqw::compile_stage(ir, ir_len, consts, n_consts, (uint32_t)n_vars, base, e->fn_keys);
+  } catch (const std::exception& ex) {
+    return fail(PQW_EINVAL, std::string("stage compile: ") + ex.what());
+  }
+  e->var_keys.insert(e->var_keys.end(), var_keys, var_keys + n_vars);
+  for (int i = 0; i < 16; ++i) out_status[i] = 0;
+  out_status[0] = st.status;
+  out_status[1] = st.info;
+  out_status[2] = st.n_obligations;
+  out_status[3] = st.n_fast;
+  out_status[4] = st.n_residual;
+  out_status[5] = (int64_t)st.code.size();
+  out_status[6] = st.n_slots;
+  out_status[7] = (int64_t)std::min<uint64_t>(st.degree, (uint64_t)INT64_MAX);
+  out_status[8] = st.const_lhs;
+  out_status[9] = st.const_rhs;
+  out_status[10] = st.exact_lhs;
+  out_status[11] = st.exact_rhs;
+  out_status[12] = (int64_t)st.field_ops;
+  out_status[13] = st.n_vars;
+  e->stages.push_back(std::move(st));
+  e->uploaded = false;
+  return (int)(e->stages.size() - 1);
+}
+
+int pqw_reset(pqw_engine* e) {
+  if (!e) return fail(PQW_EINVAL, "null engine");
+  if (e->d_code) {
+    cudaSetDevice(e->device);
+    e->free_device();
+  }
+  e->stages.clear();
+  e->var_keys.clear();
+  e->gpu_stage_of.clear();
+  e->n_gpu_stages = 0;
+  return PQW_OK;
+}
+
+long pqw_stage_bytecode(pqw_engine* e, int stage, pqw_ins* out, size_t cap, uint32_t* n_slots) {
+  if (!e || stage < 0 || (size_t)stage >= e->stages.size()) return fail(PQW_EINVAL, "bad stage");
+  const auto& st = e->stages[stage];
+  if (n_slots) *n_slots = st.n_slots;
+  if (out) std::memcpy(out, st.code.data(), std::min(cap, st.code.size()) * sizeof(pqw_ins));
+  return (long)st.code.size();
+}
+
+long pqw_obligation_support(pqw_engine* e, int stage, uint32_t obl, uint32_t* out, size_t cap) {
+  if (!e || stage < 0 || (size_t)stage >= e->stages.size()) return fail(PQW_EINVAL, "bad stage");
+  const auto& st = e->stages[stage];
+  auto vars = pqw::obligation_support(st, obl);
+  if (out)
+    for (size_t i = 0; i < std::min(cap, vars.size()); ++i) out[i] = vars[i] - st.var_base;
+  return (long)vars.size();
+}
+
+int pqw_upload(pqw_engine* e) {
+  if (!e) return fail(PQW_EINVAL, "null engine");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= e->device) {
+    cudaGetLastError();
+    return fail(PQW_ENODEV, "no CUDA device for the witness engine");
+  }
+  CU(cudaSetDevice(e->device));
+  e->free_device();
+  // stages that need the GPU, longest first (LPT order for the work queue)
+  std::vector<int> ids;
+  for (size_t i = 0; i < e->stages.size(); ++i)
+    if (e->stages[i].status == PQW_STAGE_OK) ids.push_back((int)i);
+  std::stable_sort(ids.begin(), ids.end(), [&](int a, int b) {
+    return e->stages[a].code.size() > e->stages[b].code.size();
+  });
+  e->gpu_stage_of = ids;
+  e->n_gpu_stages = (uint32_t)ids.size();
+  std::vector<pqw_ins> code;
+  std::vector<pqw::StageDesc> descs;
+  std::vector<uint32_t> work;
+  e->max_slots = 0;
+  std::fill(std::begin(e->op_hist), std::end(e->op_hist), 0);
+  for (size_t r = 0; r < ids.size(); ++r) {
+    const auto& st = e->stages[ids[r]];
+    descs.push_back({(uint32_t)code.size(), st.n_slots, st.var_base, (uint32_t)r});
+    code.insert(code.end(), st.code.begin(), st.code.end());
+    work.push_back((uint32_t)r);
+    e->max_slots = std::max(e->max_slots, st.n_slots);
+    for (const auto& in : st.code)
+      if (in.op < PQW_B_NUM_OPS) e->op_hist[in.op]++;
+  }
+  e->n_code = code.size();
+  if (code.empty()) code.push_back(pqw_ins{PQW_B_END, 0, 0, 0});
+  code.push_back(pqw_ins{PQW_B_END, 0, 0, 0});  // the prefetching decoder reads one past END
+  if (descs.empty()) descs.push_back({0, 0, 0, 0});
+  if (work.empty()) work.push_back(0);
+
+  cudaDeviceProp prop;
+  CU(cudaGetDeviceProperties(&prop, e->device));
+  // shared-memory slot budget per warp: aim for >= 2 CTAs (8 warps) per SM,
+  // spill the rest of a stage's slot file to per-warp global scratch
+  const size_t slot_bytes = (size_t)pqw::TW * sizeof(uint32_t);  // one slot, all warps
+  size_t sm_cap = prop.sharedMemPerMultiprocessor;
+  size_t per_cta = std::min<size_t>(prop.sharedMemPerBlockOptin, sm_cap / 2) - 1024;
+  uint32_t fit = (uint32_t)(per_cta / slot_bytes);
+  const char* env_slots = getenv("PQW_SMEM_SLOTS");
+  if (env_slots) fit = std::min<uint32_t>(fit, (uint32_t)atoi(env_slots));
+  e->smem_slots = std::min<uint32_t>(std::max<uint32_t>(e->max_slots, 1), std::max<uint32_t>(fit, 1));
+  e->overflow_slots = e->max_slots > e->smem_slots ? e->max_slots - e->smem_slots : 0;
+  const size_t smem_bytes = (size_t)e->smem_slots * slot_bytes;
+  CU(cudaFuncSetAttribute(pqw::eval_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)smem_bytes));
+  CU(cudaFuncSetAttribute(pqw::eval_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)smem_bytes));
+  int per_sm = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pqw::eval_kernel<false>, pqw::BLOCK,
+                                                   smem_bytes));
+  if (per_sm < 1) per_sm = 1;
+  e->grid = (uint32_t)(prop.multiProcessorCount * per_sm);
+
+  CU(cudaMalloc(&e->d_code, code.size() * sizeof(pqw_ins)));
+  CU(cudaMemcpy(e->d_code, code.data(), code.size() * sizeof(pqw_ins), cudaMemcpyHostToDevice));
+  CU(cudaMalloc(&e->d_stages, descs.size() * sizeof(pqw::StageDesc)));
+  CU(cudaMemcpy(e->d_stages, descs.data(), descs.size() * sizeof(pqw::StageDesc),
+                cudaMemcpyHostToDevice));
+  CU(cudaMalloc(&e->d_work, work.size() * sizeof(uint32_t)));
+  CU(cudaMemcpy(e->d_work, work.data(), work.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  size_t nk = std::max<size_t>(e->var_keys.size(), 1);
+  CU(cudaMalloc(&e->d_var_keys, nk * sizeof(uint64_t)));
+  if (!e->var_keys.empty())
+    CU(cudaMemcpy(e->d_var_keys, e->var_keys.data(), e->var_keys.size() * sizeof(uint64_t),
+                  cudaMemcpyHostToDevice));
+  CU(cudaMalloc(&e->d_fn_keys, 3 * sizeof(uint64_t)));
+  CU(cudaMemcpy(e->d_fn_keys, e->fn_keys, 3 * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  CU(cudaMalloc(&e->d_counter, sizeof(uint32_t)));
+  e->scratch_bytes = (size_t)e->grid * std::max<uint32_t>(e->overflow_slots, 1) * slot_bytes;
+  CU(cudaMalloc(&e->d_scratch, e->scratch_bytes));
+  size_t nr = std::max<size_t>(ids.size(), 1);
+  CU(cudaMalloc(&e->d_first_bad, nr * sizeof(unsigned long long)));
+  CU(cudaMalloc(&e->d_n_valid, nr * sizeof(uint32_t)));
+  CU(cudaMalloc(&e->d_n_bad, nr * sizeof(uint32_t)));
+  CU(cudaMalloc(&e->d_probe, 2 * sizeof(uint32_t)));
+  if (!e->ev0) CU(cudaEventCreate(&e->ev0));
+  if (!e->ev1) CU(cudaEventCreate(&e->ev1));
+  e->uploaded = true;
+  e->results_ready = false;
+  return PQW_OK;
+}
+
+int pqw_launch(pqw_engine* e, uint32_t n_witness, void* stream) {
+  if (!e) return fail(PQW_EINVAL, "null engine");
+  if (!e->uploaded) return fail(PQW_ESTATE, "pqw_launch before pqw_upload");
+  if (n_witness == 0) return fail(PQW_EINVAL, "n_witness must be positive");
+  CU(cudaSetDevice(e->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t nr = std::max<size_t>(e->n_gpu_stages, 1);
+  CU(cudaMemsetAsync(e->d_first_bad, 0xFF, nr * sizeof(unsigned long long), s));
+  CU(cudaMemsetAsync(e->d_n_valid, 0, nr * sizeof(uint32_t), s));
+  CU(cudaMemsetAsync(e->d_n_bad, 0, nr * sizeof(uint32_t), s));
+  CU(cudaMemsetAsync(e->d_counter, 0, sizeof(uint32_t), s));
+  e->results_ready = false;
+  e->timed = false;
+  if (e->n_gpu_stages == 0) return PQW_OK;
+  pqw::Params p{};
+  p.code = reinterpret_cast<const uint4*>(e->d_code);
+  p.stages = e->d_stages;
+  p.work = e->d_work;
+  p.var_keys = e->d_var_keys;
+  p.fn_keys = e->d_fn_keys;
+  p.counter = e->d_counter;
+  p.scratch = e->d_scratch;
+  p.first_bad = e->d_first_bad;
+  p.n_valid = e->d_n_valid;
+  p.n_bad = e->d_n_bad;
+  p.tiles = (n_witness + pqw::TW - 1) / pqw::TW;
+  p.n_items = e->n_gpu_stages * p.tiles;
+  p.n_witness = n_witness;
+  p.smem_slots = e->smem_slots;
+  p.overflow_slots = std::max<uint32_t>(e->overflow_slots, 1);
+  const size_t smem_bytes = (size_t)e->smem_slots * pqw::TW * sizeof(uint32_t);
+  uint32_t grid = std::min<uint32_t>(e->grid, std::max<uint32_t>(p.n_items, 1));
+  CU(cudaEventRecord(e->ev0, s));
+  pqw::eval_kernel<false><<<grid, pqw::BLOCK, smem_bytes, s>>>(p);
+  CU(cudaGetLastError());
+  CU(cudaEventRecord(e->ev1, s));
+  e->timed = true;
+  return PQW_OK;
+}
+
+int pqw_results(pqw_engine* e, uint64_t* first_bad, uint32_t* n_valid, uint32_t* n_bad,
+                size_t n_stages) {
+  if (!e) return fail(PQW_EINVAL, "null engine");
+  if (n_stages != e->stages.size()) return fail(PQW_EINVAL, "n_stages must equal stage count");
+  if (!e->uploaded) return fail(PQW_ESTATE, "no uploaded image");
+  CU(cudaSetDevice(e->device));
+  const size_t nr = e->n_gpu_stages;
+  e->h_first_bad.resize(nr);
+  e->h_valid.resize(nr);
+  e->h_bad.resize(nr);
+  if (e->timed) CU(cudaEventSynchronize(e->ev1));
+  CU(cudaDeviceSynchronize());
+  if (nr) {
+    CU(cudaMemcpy(e->h_first_bad.data(), e->d_first_bad, nr * sizeof(unsigned long long),
+                  cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(e->h_valid.data(), e->d_n_valid, nr * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(e->h_bad.data(), e->d_n_bad, nr * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  }
+  for (size_t i = 0; i < n_stages; ++i) {
+    if (first_bad) first_bad[i] = ~0ull;
+    if (n_valid) n_valid[i] = 0;
+    if (n_bad) n_bad[i] = 0;
+  }
+  for (size_t r = 0; r < nr; ++r) {
+    int sidx = e->gpu_stage_of[r];
+    if (first_bad) first_bad[sidx] = e->h_first_bad[r];
+    if (n_valid) n_valid[sidx] = e->h_valid[r];
+    if (n_bad) n_bad[sidx] = e->h_bad[r];
+  }
+  return PQW_OK;
+}
+
+int pqw_probe(pqw_engine* e, int stage, uint32_t witness, uint32_t obl, uint32_t* lhs,
+              uint32_t* rhs, uint32_t* var_vals, size_t n_vars) {
+  if (!e || stage < 0 || (size_t)stage >= e->stages.size()) return fail(PQW_EINVAL, "bad stage");
+  if (!e->uploaded) return fail(PQW_ESTATE, "pqw_probe before pqw_upload");
+  const auto& st = e->stages[stage];
+  if (st.status != PQW_STAGE_OK) return fail(PQW_EINVAL, "stage has no GPU program");
+  if (var_vals && n_vars < st.n_vars) return fail(PQW_EINVAL, "var_vals too short");
+  CU(cudaSetDevice(e->device));
+  uint32_t r = 0;
+  for (; r < e->n_gpu_stages; ++r)
+    if (e->gpu_stage_of[r] == stage) break;
+  uint32_t* d_vars = nullptr;
+  CU(cudaMalloc(&d_vars, std::max<size_t>(st.n_vars, 1) * sizeof(uint32_t)));
+  uint32_t* d_work1 = nullptr;
+  CU(cudaMalloc(&d_work1, sizeof(uint32_t)));
+  CU(cudaMemcpy(d_work1, &r, sizeof(uint32_t), cudaMemcpyHostToDevice));
+  uint32_t init[2] = {0xFFFFFFFFu, 0xFFFFFFFFu};
+  CU(cudaMemcpy(e->d_probe, init, sizeof(init), cudaMemcpyHostToDevice));
+  pqw::Params p{};
+  p.code = reinterpret_cast<const uint4*>(e->d_code);
+  p.stages = e->d_stages;
+  p.work = d_work1;
+  p.var_keys = e->d_var_keys;
+  p.fn_keys = e->d_fn_keys;
+  p.counter = e->d_counter;
+  p.scratch = e->d_scratch;
+  p.n_items = 1;
+  p.tiles = 1;
+  p.n_witness = witness + 1;
+  p.smem_slots = e->smem_slots;
+  p.overflow_slots = std::max<uint32_t>(e->overflow_slots, 1);
+  p.probe_w = witness;
+  p.probe_obl = obl;
+  p.probe_out = e->d_probe;
+  p.probe_vars = d_vars;
+  const size_t smem_bytes = (size_t)e->smem_slots * pqw::TW * sizeof(uint32_t);
+  pqw::eval_kernel<true><<<1, pqw::BLOCK, smem_bytes>>>(p);
+  CU(cudaGetLastError());
+  CU(cudaDeviceSynchronize());
+  uint32_t got[2];
+  CU(cudaMemcpy(got, e->d_probe, sizeof(got), cudaMemcpyDeviceToHost));
+  if (lhs) *lhs = got[0];
+  if (rhs) *rhs = got[1];
+  if (var_vals && st.n_vars)
+    CU(cudaMemcpy(var_vals, d_vars, st.n_vars * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  cudaFree(d_vars);
+  cudaFree(d_work1);
+  return PQW_OK;
+}
+
+int pqw_last_launch_ms(pqw_engine* e, float* ms) {
+  if (!e || !ms) return fail(PQW_EINVAL, "null argument");
+  if (!e->timed) {
+    *ms = 0.f;
+    return PQW_OK;
+  }
+  CU(cudaSetDevice(e->device));
+  CU(cudaEventSynchronize(e->ev1));
+  CU(cudaEventElapsedTime(ms, e->ev0, e->ev1));
+  return PQW_OK;
+}
+
+int pqw_image_stats(pqw_engine* e, uint64_t* out, size_t cap) {
+  if (!e || !out) return fail(PQW_EINVAL, "null argument");
+  uint64_t buf[4 + PQW_B_NUM_OPS] = {};
+  uint64_t n_gpu = 0, n_code = 0, max_slots = 0;
+  uint64_t hist[PQW_B_NUM_OPS] = {};
+  for (const auto& st : e->stages) {
+    if (st.status != PQW_STAGE_OK) continue;
+    n_gpu++;
+    n_code += st.code.size();
+    max_slots = std::max<uint64_t>(max_slots, st.n_slots);
+    for (const auto& in : st.code)
+      if (in.op < PQW_B_NUM_OPS) hist[in.op]++;
+  }
+  buf[0] = n_gpu;
+  buf[1] = n_code;
+  buf[2] = max_slots;
+  buf[3] = e->smem_slots;
+  for (int i = 0; i < PQW_B_NUM_OPS; ++i) buf[4 + i] = hist[i];
+  std::memcpy(out, buf, std::min(cap, (size_t)(4 + PQW_B_NUM_OPS)) * sizeof(uint64_t));
+  return PQW_OK;
+}
+
+int pqw_peak_fieldops(int device, double out[3]) {
+  if (!out) return fail(PQW_EINVAL, "null argument");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device) {
+    cudaGetLastError();
+    return fail(PQW_ENODEV, "no CUDA device");
+  }
+  CU(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CU(cudaGetDeviceProperties(&prop, device));
+  const int blocks = prop.multiProcessorCount * 8, threads = 256, iters = 2048;
+  uint32_t* sink = nullptr;
+  CU(cudaMalloc(&sink, (size_t)blocks * threads * sizeof(uint32_t)));
+  cudaEvent_t e0, e1;
+  CU(cudaEventCreate(&e0));
+  CU(cudaEventCreate(&e1));
+  for (int kind = 0; kind < 3; ++kind) {
+    float best = 1e30f;
+    for (int rep = 0; rep < 4; ++rep) {
+      int it = kind == 2 ? iters / 8 : iters;
+      CU(cudaEventRecord(e0));
+      if (kind == 0) pqw::peak_kernel<0><<<blocks, threads>>>(sink, it, rep);
+      else if (kind == 1) pqw::peak_kernel<1><<<blocks, threads>>>(sink, it, rep);
+      else pqw::peak_kernel<2><<<blocks, threads>>>(sink, it, rep);
+      CU(cudaEventRecord(e1));
+      CU(cudaEventSynchronize(e1));
+      float ms = 0;
+      CU(cudaEventElapsedTime(&ms, e0, e1));
+      if (rep > 0 && ms < best) best = ms;  // rep 0 warms up
+    }
+    double n_ops = (double)blocks * threads * (kind == 2 ? iters / 8 : iters) * 16 * 8;
+    out[kind] = n_ops / (best * 1e-3);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  return PQW_OK;
+}
+
+}  // extern "C"

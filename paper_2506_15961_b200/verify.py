@@ -1,0 +1,237 @@
+"""Top-level verdict pipeline (drop-in for pkg/src/planeq/verify.py:62 verify_plan).
+
+Same order of business as the reference: concrete shape validation, lineage
+validation (tiling violations refute structurally), shape reduction, stage
+construction, stage discharge, one aggregated verdict. Discharge runs on the
+sm_100a witness engine: every stage of the plan is compiled into one device
+image and evaluated in one launch (no worker pool, no solver processes).
+
+Verdicts: "proven" -- every stage closed; "refuted" -- some stage has a
+confirmed counterexample (an integer witness assignment plus the keyed-hash
+interpretation of EXP/RSQRT/SIGMOID, replayable with exact rationals);
+"unknown" -- some stage had no valid witness (all denominators vanished).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import asdict, dataclass
+from typing import Any
+
+from . import field as F
+from .engine import (STAGE_BAD_INDEX, STAGE_LOG_DIV0, STAGE_OK, STAGE_PAR_DIV0, STAGE_PROVEN,
+                     STAGE_REFUTED_CONST, Engine)
+from .errors import GraphError, PlanEqError, UncoveredNode
+from .graph import validate_lineage
+from .opshape import validate_concrete
+from .plan import Plan
+from .stages import (LoweredStage, Stage, StageResult, bound_log2, build_stages, entry_order,
+                     lower_stage, shard_owner)
+
+DEFAULT_WITNESSES = 512
+
+
+@dataclass
+class VerifyOptions:
+    jobs: int = 1
+    no_reduce: bool = False
+    objective: str = "l1"
+    solver_argv: list[str] | None = None
+    timeout_s: float = 60.0
+    no_cancel: bool = False
+    strict: bool = False
+    # witness engine
+    witnesses: int = DEFAULT_WITNESSES
+    seed: int = 0
+    device: int = 0
+
+
+def _aggregate(results: list[StageResult], cancelled: int) -> str:
+    statuses = {r.status for r in results}
+    if "refuted" in statuses:
+        return "refuted"
+    if "unknown" in statuses or cancelled or not results:
+        return "unknown"
+    return "proven"
+
+
+class _Deferred:
+    """An exception raised while lowering a stage, re-raised in stage order."""
+
+    def __init__(self, exc: BaseException):
+        self.exc = exc
+
+
+def compile_stages(plan: Plan, stages: list[Stage], engine: Engine, seed: int):
+    """Lower and compile every stage into `engine`. Returns per-stage
+    (LoweredStage | _Deferred, StageCompile | None, compile seconds)."""
+    owner = shard_owner(plan, entry_order(plan))
+    out = []
+    for st in stages:
+        t0 = time.perf_counter()
+        try:
+            lw = lower_stage(plan, st, owner, seed)
+        except PlanEqError as e:
+            out.append((_Deferred(e), None, time.perf_counter() - t0))
+            continue
+        comp = engine.add_stage(lw.ir, lw.consts, lw.var_keys)
+        out.append((lw, comp, time.perf_counter() - t0))
+    return out
+
+
+def _const_detail(lw: LoweredStage, comp) -> dict[str, Any]:
+    label, idx = lw.locate(comp.info)
+    both_int = comp.exact_lhs is not None and comp.exact_rhs is not None
+    lv = comp.exact_lhs if comp.exact_lhs is not None else comp.const_lhs
+    rv = comp.exact_rhs if comp.exact_rhs is not None else comp.const_rhs
+    d = {"shard": label, "index": list(idx), "lhs_value": str(lv), "rhs_value": str(rv)}
+    if both_int:
+        d["reason"] = "token index mismatch"
+    else:
+        d["assignment"] = {}
+    return d
+
+
+def _witness_detail(engine: Engine, lw: LoweredStage, comp, first_bad: int,
+                    seed: int) -> dict[str, Any]:
+    w, obl = int(first_bad) >> 32, int(first_bad) & 0xFFFFFFFF
+    lhs, rhs, vals = engine.probe(comp.index, w, obl, comp.n_vars)
+    label, idx = lw.locate(obl)
+    support = engine.support(comp.index, obl)
+    names = sorted((lw.var_name(i), int(vals[i])) for i in support)
+    return {
+        "shard": label,
+        "index": list(idx),
+        "lhs_value": str(lhs),
+        "rhs_value": str(rhs),
+        "assignment": {n: str(v) for n, v in names[:16]},
+        "witness": w,
+        "obligation": obl,
+        "field": f"F_p, p={F.P}",
+        "seed": seed,
+        "uf": "keyed-hash (field.py uf_apply)",
+    }
+
+
+def discharge(plan: Plan, stages: list[Stage], opts: VerifyOptions,
+              engine: Engine | None = None) -> tuple[list[StageResult], int, dict]:
+    """Run every stage through the witness engine; returns (results, cancelled, stats)."""
+    own = engine is None
+    eng = engine or Engine(opts.device, opts.seed, F.fn_keys(opts.seed))
+    try:
+        t0 = time.perf_counter()
+        compiled = compile_stages(plan, stages, eng, opts.seed)
+        t_compile = time.perf_counter() - t0
+        needs_gpu = any(c is not None and c.status == STAGE_OK for _, c, _ in compiled)
+        gpu_ms = 0.0
+        fb = nv = nb = None
+        if needs_gpu:
+            eng.upload()
+            eng.launch(opts.witnesses)
+            fb, nv, nb = eng.results()
+            gpu_ms = eng.last_launch_ms()
+        n_gpu = sum(1 for _, c, _ in compiled if c is not None and c.status == STAGE_OK)
+        share = (gpu_ms / 1e3) / n_gpu if n_gpu else 0.0
+        results: list[StageResult] = []
+        cancelled = 0
+        for st, (lw, comp, t_c) in zip(stages, compiled):
+            if isinstance(lw, _Deferred):
+                raise lw.exc
+            r = StageResult(st.target, "proven", comp.obligations, comp.fast, comp.residual,
+                            t_c, degree_bound=comp.degree)
+            if comp.status == STAGE_PROVEN:
+                r.note = "closed by value numbering"
+            elif comp.status == STAGE_REFUTED_CONST:
+                r.status = "refuted"
+                r.detail = _const_detail(lw, comp)
+            elif comp.status == STAGE_PAR_DIV0:
+                r = StageResult(st.target, "refuted", 0, 0, 0, t_c,
+                                {"reason": "parallel side divides by zero: "
+                                           "constant denominator violates side condition"})
+            elif comp.status == STAGE_LOG_DIV0:
+                raise GraphError(f"stage {st.target}: logical side divides by zero: "
+                                 "constant denominator violates side condition")
+            elif comp.status == STAGE_BAD_INDEX:
+                raise GraphError(f"stage {st.target}: token id outside its embedding table")
+            else:
+                i = comp.index
+                r.witnesses = opts.witnesses
+                r.valid_witnesses = int(nv[i])
+                r.failing_witnesses = int(nb[i])
+                r.wall_s = t_c + share
+                r.false_equiv_log2 = bound_log2(comp.degree, int(nv[i]))
+                if int(fb[i]) != 0xFFFFFFFFFFFFFFFF:
+                    r.status = "refuted"
+                    r.detail = _witness_detail(eng, lw, comp, int(fb[i]), opts.seed)
+                elif int(nv[i]) == 0:
+                    r.status = "unknown"
+                    r.note = "no witness kept every denominator nonzero"
+            results.append(r)
+            if r.status == "refuted" and not opts.no_cancel:
+                cancelled = len(stages) - len(results)
+                break
+        stats = {"compile_s": round(t_compile, 6), "gpu_ms": round(gpu_ms, 4),
+                 "gpu_stages": n_gpu, "witnesses": opts.witnesses}
+        if needs_gpu:
+            stats.update(eng.image_stats())
+        return results, cancelled, stats
+    finally:
+        if own:
+            eng.close()
+
+
+def verify_plan(plan: Plan, opts: VerifyOptions | None = None) -> dict[str, Any]:
+    opts = opts or VerifyOptions()
+    t0 = time.perf_counter()
+    report: dict[str, Any] = {"verdict": "unknown", "stages": [], "jobs": opts.jobs}
+    if plan.parallel is None or plan.lineage is None:
+        raise GraphError("plan has no parallel graph or no lineage")
+    validate_concrete(plan.logical)
+    validate_concrete(plan.parallel)
+    problems = validate_lineage(plan.logical, plan.parallel, plan.lineage)
+    tiling = [p for p in problems if "do not tile" in p]
+    hard = [p for p in problems if "do not tile" not in p]
+    if hard:
+        raise GraphError("; ".join(hard))
+    if tiling:
+        report.update(verdict="refuted", refuted_by="structure", structure=tiling)
+        report["wall_s"] = round(time.perf_counter() - t0, 6)
+        return report
+
+    work = plan
+    if not opts.no_reduce:
+        from .shapes import reduce_plan
+        red = reduce_plan(plan, objective=opts.objective, solver_argv=opts.solver_argv,
+                          timeout_s=opts.timeout_s)
+        work = red.plan
+        report["reduction"] = red.report
+
+    stages, uncovered = build_stages(work)
+    report["uncovered"] = uncovered
+    loose = uncovered["parallel"] + uncovered["logical"]
+    if loose:
+        if opts.strict:
+            raise UncoveredNode(loose)
+        report["warning"] = (f"{len(loose)} node(s) feed no checkpoint and are "
+                             f"not checked: {loose[:8]}")
+
+    results, cancelled, stats = discharge(work, stages, opts)
+    verdict = _aggregate(results, cancelled)
+    total_ob = sum(r.obligations for r in results)
+    total_fast = sum(r.fastpath for r in results)
+    report.update(
+        verdict=verdict,
+        stages=[asdict(r) for r in results],
+        cancelled=cancelled,
+        obligations=total_ob,
+        fastpath_rate=round(total_fast / total_ob, 6) if total_ob else None,
+        engine=stats,
+        wall_s=round(time.perf_counter() - t0, 6),
+    )
+    if not stages:
+        report["note"] = "lineage has no produced checkpoints; nothing was proven"
+    for r in results:
+        if r.status == "refuted":
+            report["counterexample"] = {"target": r.target, **(r.detail or {})}
+            break
+    return report

@@ -1,0 +1,61 @@
+"""The C-ABI library loads on a CPU-only host and exports every declared symbol."""
+
+import ctypes
+import os
+import re
+
+from paper_2506_15961_b200 import engine
+
+HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include",
+                      "planeq_witness.h")
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\w[\w\s\*]*?\b(pqw_\w+)\s*\(", text, re.M)))
+
+
+def test_header_and_binding_agree(lib):
+    decl = declared_functions()
+    assert decl, "no functions parsed from the header"
+    assert sorted(engine.EXPORTS) == decl
+
+
+def test_every_symbol_exported(lib):
+    raw = ctypes.CDLL(engine.LIB_PATH)
+    for name in declared_functions():
+        assert hasattr(raw, name), name
+
+
+def test_abi_and_device_count_without_gpu(lib):
+    assert lib.pqw_abi_version() == engine.ABI_VERSION
+    assert engine.device_count() >= 0
+
+
+def test_compile_only_works_without_device(lib):
+    import numpy as np
+    from paper_2506_15961_b200.stages import IR_MAGIC, OPCODE, T_CHECK, T_VARS
+    # x (2 vars) ; y = x + x ; check y == scale(x, 2)
+    consts = np.array([[2, 2, 1]], dtype=np.int64)
+    ir = [IR_MAGIC, 3, 4, 2, 1, 2, 1, 2, 1, 2,
+          T_VARS, 0, 1, 1, 0, 0,
+          OPCODE["add"], 2, 1, 0, 0, 0, 1,
+          OPCODE["scale"], 1, 1, 1, 0, 2, 0]
+    ir += [T_CHECK, 2, 0, 1, 1, 2, 0]
+    e = engine.Engine(0, 1, (1, 2, 3))
+    c = e.add_stage(np.array(ir, dtype=np.int32), consts, np.array([5, 6], dtype=np.uint64))
+    assert c.obligations == 2 and c.status in (engine.STAGE_OK, engine.STAGE_PROVEN)
+    code, slots = e.bytecode(c.index)
+    assert code[-1, 0] == 0  # END
+    e.close()
+
+
+def test_malformed_program_is_rejected(lib):
+    import numpy as np
+    import pytest
+    from paper_2506_15961_b200.errors import EngineError
+    e = engine.Engine(0, 1, (1, 2, 3))
+    with pytest.raises(EngineError):
+        e.add_stage(np.array([1, 2, 3], dtype=np.int32), np.zeros((0, 3), np.int64),
+                    np.zeros(0, np.uint64))
+    e.close()
