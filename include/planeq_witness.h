@@ -69,7 +69,7 @@ enum pqw_top {
 enum pqw_bop {
   PQW_B_END = 0, PQW_B_CONST, PQW_B_VAR, PQW_B_ADD, PQW_B_SUB, PQW_B_MUL, PQW_B_NEG,
   PQW_B_DIV, PQW_B_HASH, PQW_B_ACC_MUL, PQW_B_ACC_MAC, PQW_B_ACC_LD, PQW_B_ACC_ADD,
-  PQW_B_ACC_ST, PQW_B_CHK, PQW_B_DEN, PQW_B_ACC_MACF,
+  PQW_B_ACC_ST, PQW_B_CHK, PQW_B_DEN, PQW_B_ACC_MACF, PQW_B_INV,
   PQW_B_NUM_OPS
 };
 

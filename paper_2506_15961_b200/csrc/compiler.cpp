@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <queue>
 #include <stdexcept>
 #include <unordered_map>
@@ -31,7 +32,7 @@ constexpr int32_t IR_MAGIC = 0x50515701;
 constexpr uint32_t NONE = 0xFFFFFFFFu;
 
 enum VKind : uint8_t { K_CONST = 0, K_VAR = 1, K_OP = 2 };
-enum VOp : uint8_t { O_NONE = 0, O_ADD, O_SUB, O_MUL, O_NEG, O_DIV, O_HASH, O_SUMN, O_DOT };
+enum VOp : uint8_t { O_NONE = 0, O_ADD, O_SUB, O_MUL, O_NEG, O_DIV, O_HASH, O_SUMN, O_DOT, O_INV };
 enum : uint8_t { F_DEN = 1, F_INT = 2 };
 enum Fn : uint32_t { FN_EXP = 0, FN_RSQRT = 1, FN_SIGMOID = 2 };
 
@@ -300,8 +301,10 @@ struct Builder {
       return mul(x, cst(inv, ex));
     }
     if (is_const(x) && res(x) == 0) return zero();
-    return intern(O_DIV, x, y, 0, nullptr, 0, sat_add(vals[x].dnum, vals[y].dden),
-                  sat_add(vals[x].dden, vals[y].dnum));
+    // x / y = x * y^-1 with the inverse value-numbered: rows that share a
+    // denominator (softmax normalizers, expanded sums) invert it once
+    uint32_t iv = intern(O_INV, y, 0, 0, nullptr, 0, vals[y].dden, vals[y].dnum);
+    return mul(x, iv);
   }
   uint32_t hash(uint32_t fn, uint32_t x) {
     if (is_const(x)) return cst(uf_apply(fn_keys[fn], res(x)), Exact{false, 0, 0});
@@ -1024,6 +1027,7 @@ struct Emitter {
         break;
       case O_NEG:
       case O_HASH:
+      case O_INV:
         out.push_back(v.a);
         break;
       default:
@@ -1067,7 +1071,7 @@ struct Emitter {
 
 CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* consts,
                             size_t n_consts, uint32_t n_vars, uint32_t var_base,
-                            const uint64_t fn_keys[3]) {
+                            const uint64_t fn_keys[3], uint32_t smem_slots) {
   CompiledStage st;
   st.n_vars = n_vars;
   st.var_base = var_base;
@@ -1188,25 +1192,70 @@ CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* con
     }
   }
 
-  // linear-scan slot allocation, lowest free slot first
-  std::vector<uint32_t> slot(B.vals.size(), NONE);
-  std::priority_queue<uint32_t, std::vector<uint32_t>, std::greater<uint32_t>> free_slots;
-  uint32_t n_slots = 0;
-  auto take = [&]() -> uint32_t {
-    if (!free_slots.empty()) {
-      uint32_t s = free_slots.top();
-      free_slots.pop();
-      return s;
+  // Two-level slot allocation. Slots [0, smem_slots) are the fast file (shared
+  // memory on the device), the rest spill to per-warp global scratch. A value
+  // occupies its slot over the group interval (def, last]: operands are read
+  // before a group writes its result, so a value may take the slot of one that
+  // dies in the same group. Fast slots go to the intervals with the most reads
+  // per group of lifetime (shortest, busiest first); the rest get spill slots
+  // by linear scan.
+  std::vector<int32_t> def(B.vals.size(), -1);
+  std::vector<uint32_t> uses(B.vals.size(), 0);
+  for (size_t g = 0; g < G; ++g) {
+    const auto& gr = E.groups[g];
+    if (gr.kind == 0) {
+      def[gr.v] = (int32_t)g;
+      E.operands(gr.v, ops);
+      for (uint32_t u : ops) uses[u]++;
+    } else if (gr.kind == 1) {
+      uses[gr.l]++;
+      uses[gr.r]++;
+    } else {
+      uses[gr.v]++;
     }
-    return n_slots++;
-  };
+  }
+  std::vector<uint32_t> slot(B.vals.size(), NONE);
+  std::vector<uint32_t> cand;
+  for (size_t g = 0; g < G; ++g)
+    if (E.groups[g].kind == 0 && last[E.groups[g].v] >= 0) cand.push_back(E.groups[g].v);
+  std::stable_sort(cand.begin(), cand.end(), [&](uint32_t a, uint32_t b) {
+    // uses / span, compared without division
+    uint64_t sa = (uint64_t)(last[a] - def[a]), sb = (uint64_t)(last[b] - def[b]);
+    return (uint64_t)uses[a] * sb > (uint64_t)uses[b] * sa;
+  });
+  std::vector<std::map<int32_t, int32_t>> occ(smem_slots);  // start -> end, per fast slot
+  uint32_t fast_used = 0;
+  for (uint32_t v : cand) {
+    const int32_t s0 = def[v], s1 = last[v];
+    for (uint32_t k = 0; k < smem_slots; ++k) {
+      auto& m = occ[k];
+      auto it = m.lower_bound(s0);
+      if (it != m.end() && it->first < s1) continue;       // next interval starts inside
+      if (it != m.begin() && std::prev(it)->second > s0) continue;  // previous reaches in
+      m.emplace(s0, s1);
+      slot[v] = k;
+      fast_used = std::max(fast_used, k + 1);
+      break;
+    }
+  }
+  std::priority_queue<uint32_t, std::vector<uint32_t>, std::greater<uint32_t>> free_spill;
+  uint32_t n_spill = 0;
   auto release_dead = [&](const std::vector<uint32_t>& used, int32_t g) {
     for (size_t i = 0; i < used.size(); ++i) {
       uint32_t u = used[i];
       bool dup = false;
       for (size_t j = 0; j < i; ++j) dup |= used[j] == u;
-      if (!dup && last[u] == g && slot[u] != NONE) free_slots.push(slot[u]);
+      if (!dup && last[u] == g && slot[u] != NONE && slot[u] >= smem_slots)
+        free_spill.push(slot[u] - smem_slots);
     }
+  };
+  auto take_spill = [&]() -> uint32_t {
+    if (!free_spill.empty()) {
+      uint32_t s = free_spill.top();
+      free_spill.pop();
+      return s;
+    }
+    return n_spill++;
   };
 
   std::vector<pqw_ins>& code = st.code;
@@ -1231,15 +1280,10 @@ CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* con
     const Val& v = B.vals[id];
     E.operands(id, ops);
     std::vector<uint32_t> used = ops;
-    // operands are read before the destination is written, so operand slots
-    // that die here may be reused for the result
     release_dead(used, (int32_t)g);
-    if (last[id] < 0) {
-      // emitted but never consumed (cannot happen for roots) -- skip
-      continue;
-    }
-    uint32_t d = take();
-    slot[id] = d;
+    if (last[id] < 0) continue;  // emitted but never consumed (cannot happen for roots)
+    if (slot[id] == NONE) slot[id] = smem_slots + take_spill();
+    uint32_t d = slot[id];
     if (v.kind == K_CONST) {
       put(PQW_B_CONST, d, (uint32_t)v.aux, 0);
     } else if (v.kind == K_VAR) {
@@ -1251,6 +1295,7 @@ CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* con
         case O_MUL: put(PQW_B_MUL, d, slot[v.a], slot[v.b]); break;
         case O_NEG: put(PQW_B_NEG, d, slot[v.a], 0); break;
         case O_DIV: put(PQW_B_DIV, d, slot[v.a], slot[v.b]); break;
+        case O_INV: put(PQW_B_INV, d, slot[v.a], 0); break;
         case O_HASH: put(PQW_B_HASH, d, slot[v.a], (uint32_t)v.aux); break;
         case O_SUMN: {
           // acc bound tracking: values < 2^31, acc is 64-bit
@@ -1285,7 +1330,8 @@ CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* con
     // same group) is released immediately
   }
   put(PQW_B_END, 0, 0, 0);
-  st.n_slots = n_slots;
+  st.n_slots = n_spill ? smem_slots + n_spill : fast_used;
+  st.n_fast_slots = fast_used;
   uint64_t ops_count = 0;
   for (const auto& ins : code)
     if (ins.op != PQW_B_END) ops_count++;
@@ -1341,6 +1387,7 @@ std::vector<uint32_t> obligation_support(const CompiledStage& st, uint32_t obl) 
         break;
       case PQW_B_NEG:
       case PQW_B_HASH:
+      case PQW_B_INV:
         if (need.erase(in.dst)) need.insert(in.a);
         break;
       default:  // binary

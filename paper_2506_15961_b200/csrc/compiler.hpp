@@ -15,7 +15,8 @@ struct CompiledStage {
   uint32_t n_obligations = 0;
   uint32_t n_fast = 0;
   uint32_t n_residual = 0;
-  uint32_t n_slots = 0;
+  uint32_t n_slots = 0;        // fast slots [0, smem_slots) + spill slots after them
+  uint32_t n_fast_slots = 0;   // fast slots actually used
   uint32_t n_vars = 0;
   uint32_t var_base = 0;       // first global var index of this stage
   uint64_t degree = 0;
@@ -25,11 +26,16 @@ struct CompiledStage {
 };
 
 // Compile one stage. `var_base` is the global index of the stage's first
-// variable (VAR instructions carry global indices). Throws std::runtime_error
-// on malformed input.
+// variable (VAR instructions carry global indices). Slots below `smem_slots`
+// are the fast (shared-memory) file; the allocator gives them to the busiest
+// short-lived values and spills the rest to slots >= smem_slots. Throws
+// std::runtime_error on malformed input.
 CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* consts,
                             size_t n_consts, uint32_t n_vars, uint32_t var_base,
-                            const uint64_t fn_keys[3]);
+                            const uint64_t fn_keys[3], uint32_t smem_slots);
+
+// Default fast-slot count (overridable per engine, PQW_FAST_SLOTS env var).
+constexpr uint32_t DEFAULT_FAST_SLOTS = 24;
 
 // Variables (global indices) in the cone of obligation `obl`, by backward
 // slicing the bytecode.

@@ -87,9 +87,18 @@ __device__ __forceinline__ void run_item(const Params& p, vec_t* wsm, vec_t* wgs
   const uint32_t w0 = PROBE ? p.probe_w : wtile * WT + lane * VW;
   const uint32_t nsm = p.smem_slots;
 
-  // slot s of this warp: 32 vec_t (256 B) in shared memory or global scratch
-  auto ptr = [&](uint32_t s) -> vec_t* {
-    return s < nsm ? wsm + (size_t)s * 32 + lane : wgs + (size_t)(s - nsm) * 32 + lane;
+  // slot s of this warp: 32 vec_t (256 B) in shared memory (s < nsm, 32-bit
+  // LDS/STS addressing) or in global scratch (spill slots); the branch is
+  // warp-uniform
+  auto ld = [&](uint32_t s) -> vec_t {
+    if (s < nsm) return wsm[s * 32u + lane];
+    return wgs[(size_t)(s - nsm) * 32u + lane];
+  };
+  auto st = [&](uint32_t s, vec_t v) {
+    if (s < nsm)
+      wsm[s * 32u + lane] = v;
+    else
+      wgs[(size_t)(s - nsm) * 32u + lane] = v;
   };
 
   bool valid0 = PROBE ? lane == 0 : w0 < p.n_witness;
@@ -106,54 +115,59 @@ __device__ __forceinline__ void run_item(const Params& p, vec_t* wsm, vec_t* wgs
       case PQW_B_END:
         goto done;
       case PQW_B_CONST:
-        *ptr(in.y) = make_uint2(in.z, in.z);
+        st(in.y, make_uint2(in.z, in.z));
         break;
       case PQW_B_VAR: {
         const uint64_t key = __ldg(p.var_keys + in.z);
         vec_t v = make_uint2(witness_value(key, w0), witness_value(key, w0 + 1));
         if (PROBE && lane == 0) p.probe_vars[in.z - sd.var_base] = v.x;
-        *ptr(in.y) = v;
+        st(in.y, v);
         break;
       }
       case PQW_B_ADD:
-        *ptr(in.y) = vadd(*ptr(in.z), *ptr(in.w));
+        st(in.y, vadd(ld(in.z), ld(in.w)));
         break;
       case PQW_B_SUB:
-        *ptr(in.y) = vsub(*ptr(in.z), *ptr(in.w));
+        st(in.y, vsub(ld(in.z), ld(in.w)));
         break;
       case PQW_B_MUL:
-        *ptr(in.y) = vmul(*ptr(in.z), *ptr(in.w));
+        st(in.y, vmul(ld(in.z), ld(in.w)));
         break;
       case PQW_B_NEG: {
-        vec_t a = *ptr(in.z);
-        *ptr(in.y) = make_uint2(fneg(a.x), fneg(a.y));
+        vec_t a = ld(in.z);
+        st(in.y, make_uint2(fneg(a.x), fneg(a.y)));
         break;
       }
       case PQW_B_DIV: {
-        vec_t a = *ptr(in.z), b = *ptr(in.w);
-        *ptr(in.y) = make_uint2(fmul(a.x, finv(b.x)), fmul(a.y, finv(b.y)));
+        vec_t a = ld(in.z), b = ld(in.w);
+        st(in.y, make_uint2(fmul(a.x, finv(b.x)), fmul(a.y, finv(b.y))));
+        break;
+      }
+      case PQW_B_INV: {
+        vec_t a = ld(in.z);
+        st(in.y, make_uint2(finv(a.x), finv(a.y)));
         break;
       }
       case PQW_B_HASH: {
         const uint64_t key = __ldg(p.fn_keys + in.w);
-        vec_t a = *ptr(in.z);
-        *ptr(in.y) = make_uint2(uf_apply(key, a.x), uf_apply(key, a.y));
+        vec_t a = ld(in.z);
+        st(in.y, make_uint2(uf_apply(key, a.x), uf_apply(key, a.y)));
         break;
       }
       case PQW_B_ACC_LD: {
-        vec_t a = *ptr(in.z);
+        vec_t a = ld(in.z);
         acc0 = a.x;
         acc1 = a.y;
         break;
       }
       case PQW_B_ACC_ADD: {
-        vec_t a = *ptr(in.z);
+        vec_t a = ld(in.z);
         acc0 += a.x;
         acc1 += a.y;
         break;
       }
       case PQW_B_ACC_MUL: {
-        vec_t a = *ptr(in.z), b = *ptr(in.w);
+        vec_t a = ld(in.z), b = ld(in.w);
         acc0 = (uint64_t)a.x * b.x;
         acc1 = (uint64_t)a.y * b.y;
         break;
@@ -163,16 +177,16 @@ __device__ __forceinline__ void run_item(const Params& p, vec_t* wsm, vec_t* wgs
         acc1 = ffold64(acc1);
         // fallthrough
       case PQW_B_ACC_MAC: {
-        vec_t a = *ptr(in.z), b = *ptr(in.w);
+        vec_t a = ld(in.z), b = ld(in.w);
         acc0 += (uint64_t)a.x * b.x;
         acc1 += (uint64_t)a.y * b.y;
         break;
       }
       case PQW_B_ACC_ST:
-        *ptr(in.y) = make_uint2(fred64(acc0), fred64(acc1));
+        st(in.y, make_uint2(fred64(acc0), fred64(acc1)));
         break;
       case PQW_B_CHK: {
-        vec_t a = *ptr(in.z), b = *ptr(in.w);
+        vec_t a = ld(in.z), b = ld(in.w);
         if (PROBE && in.y == p.probe_obl && lane == 0) {
           p.probe_out[0] = a.x;
           p.probe_out[1] = b.x;
@@ -182,7 +196,7 @@ __device__ __forceinline__ void run_item(const Params& p, vec_t* wsm, vec_t* wgs
         break;
       }
       case PQW_B_DEN: {
-        vec_t a = *ptr(in.z);
+        vec_t a = ld(in.z);
         if (a.x == 0) valid0 = false;
         if (a.y == 0) valid1 = false;
         break;
@@ -317,6 +331,7 @@ struct pqw_engine {
   uint32_t n_gpu_stages = 0;
   uint32_t max_slots = 0;
   uint32_t smem_slots = 0;
+  uint32_t fast_slots = pqw::DEFAULT_FAST_SLOTS;  // compile-time fast-file size
   uint32_t overflow_slots = 0;
   uint32_t grid = 0;
   uint64_t n_code = 0;
@@ -378,6 +393,10 @@ int pqw_engine_create(int device, uint64_t seed, const uint64_t fn_keys[3], pqw_
   e->device = device;
   e->seed = seed;
   for (int i = 0; i < 3; ++i) e->fn_keys[i] = fn_keys[i];
+  if (const char* fs = getenv("PQW_FAST_SLOTS")) {
+    int v = atoi(fs);
+    if (v >= 1 && v <= 200) e->fast_slots = (uint32_t)v;
+  }
   *out = e;
   return PQW_OK;
 }
@@ -402,7 +421,8 @@ int pqw_stage_add(pqw_engine* e, const int32_t* ir, size_t ir_len, const int64_t
   const uint32_t base = (uint32_t)e->var_keys.size();
   pqw::CompiledStage st;
   try {
-    st = pqw::compile_stage(ir, ir_len, consts, n_consts, (uint32_t)n_vars, base, e->fn_keys);
+    st = pqw::compile_stage(ir, ir_len, consts, n_consts, (uint32_t)n_vars, base, e->fn_keys,
+                            e->fast_slots);
   } catch (const std::exception& ex) {
     return fail(PQW_EINVAL, std::string("stage compile: ") + ex.what());
   }
@@ -497,15 +517,12 @@ int pqw_upload(pqw_engine* e) {
 
   cudaDeviceProp prop;
   CU(cudaGetDeviceProperties(&prop, e->device));
-  // shared-memory slot budget per warp: aim for >= 2 CTAs (8 warps) per SM,
-  // spill the rest of a stage's slot file to per-warp global scratch
+  // the fast (shared-memory) slot file has the size the stages were compiled
+  // for; spill slots live in per-warp global scratch
   const size_t slot_bytes = (size_t)pqw::TW * sizeof(uint32_t);  // one slot, all warps
-  size_t sm_cap = prop.sharedMemPerMultiprocessor;
-  size_t per_cta = std::min<size_t>(prop.sharedMemPerBlockOptin, sm_cap / 2) - 1024;
-  uint32_t fit = (uint32_t)(per_cta / slot_bytes);
-  const char* env_slots = getenv("PQW_SMEM_SLOTS");
-  if (env_slots) fit = std::min<uint32_t>(fit, (uint32_t)atoi(env_slots));
-  e->smem_slots = std::min<uint32_t>(std::max<uint32_t>(e->max_slots, 1), std::max<uint32_t>(fit, 1));
+  if ((size_t)e->fast_slots * slot_bytes > prop.sharedMemPerBlockOptin - 1024)
+    return fail(PQW_EINVAL, "fast slot file does not fit in shared memory");
+  e->smem_slots = std::max<uint32_t>(e->fast_slots, 1);
   e->overflow_slots = e->max_slots > e->smem_slots ? e->max_slots - e->smem_slots : 0;
   const size_t smem_bytes = (size_t)e->smem_slots * slot_bytes;
   CU(cudaFuncSetAttribute(pqw::eval_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -14,7 +14,7 @@ import numpy as np
 from oracle import m31
 
 OPS = ("END", "CONST", "VAR", "ADD", "SUB", "MUL", "NEG", "DIV", "HASH", "ACC_MUL", "ACC_MAC",
-       "ACC_LD", "ACC_ADD", "ACC_ST", "CHK", "DEN", "ACC_MACF")
+       "ACC_LD", "ACC_ADD", "ACC_ST", "CHK", "DEN", "ACC_MACF", "INV")
 FN = ("EXP", "RSQRT", "SIGMOID")
 
 
@@ -47,6 +47,8 @@ def run(code: np.ndarray, n_slots: int, var_keys: np.ndarray, var_base: int, see
             slots[dst] = (m31.P - slots[a]) % m31.P
         elif name == "DIV":
             slots[dst] = m31.mul(slots[a], m31.inv(slots[b]))
+        elif name == "INV":
+            slots[dst] = m31.inv(slots[a])
         elif name == "HASH":
             slots[dst] = m31.uf(seed, FN[b], slots[a])
         elif name == "ACC_LD":

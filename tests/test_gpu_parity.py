@@ -8,10 +8,13 @@ For every golden work plan (the reference's own reduced plan, tests/golden):
     assignment reproduces lhs != rhs.
 """
 
+import json
+import os
+
 import numpy as np
 import pytest
 
-from golden_io import load_plan, verdicts
+from golden_io import GOLDEN, load_plan, verdicts
 from oracle.stage_check import check_stage
 from paper_2506_15961_b200 import field as F
 from paper_2506_15961_b200.engine import STAGE_OK, Engine
@@ -20,6 +23,8 @@ from paper_2506_15961_b200.verify import VerifyOptions, discharge
 
 RECS = [r for r in verdicts() if "work_plan" in r]
 W = 512
+_BP = os.path.join(GOLDEN, "verdicts_bundled.json")
+BUNDLED = json.load(open(_BP)) if os.path.exists(_BP) else {}
 
 
 @pytest.mark.gpu
@@ -33,7 +38,21 @@ def test_stage_verdicts_match_reference(gpu, rec):
     results, cancelled, _ = discharge(plan, stages, VerifyOptions(no_cancel=True, witnesses=W))
     assert cancelled == 0
     got = [(r.target, r.status) for r in results]
-    assert got == [tuple(x) for x in ref["stage_status"]]
+    want = [tuple(x) for x in ref["stage_status"]]
+    assert [t for t, _ in got] == [t for t, _ in want]
+    for (t, g), (_, r) in zip(got, want):
+        if r in ("proven", "refuted"):
+            assert g == r, t
+        else:
+            # the reference's solver gave up (z3 timeout); the witness engine
+            # must decide -- refutations are replayed through the reference's
+            # evaluator in tests/test_replay_reference.py
+            assert g in ("proven", "refuted"), t
+    bundled = BUNDLED.get(rec["name"])
+    if bundled and "stage_status" in bundled:
+        for (t, g), (_, r) in zip(got, bundled["stage_status"]):
+            if r in ("proven", "refuted"):
+                assert g == r, (t, "bundled-solver verdict")
 
 
 @pytest.mark.gpu
@@ -82,7 +101,10 @@ def test_verify_plan_end_to_end_matches_reference(gpu):
             continue
         plan = load_plan(rec["work_plan"])
         rep = verify_plan(plan, VerifyOptions(no_reduce=True, no_cancel=True))
-        assert rep["verdict"] == ref["verdict"], rec["name"]
+        if ref["verdict"] in ("proven", "refuted"):
+            assert rep["verdict"] == ref["verdict"], rec["name"]
+        else:
+            assert rep["verdict"] in ("proven", "refuted"), rec["name"]
         if rep["verdict"] == "refuted" and rep.get("counterexample", {}).get("witness") is not None:
             cx = rep["counterexample"]
             assert cx["lhs_value"] != cx["rhs_value"]
