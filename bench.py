@@ -296,10 +296,11 @@ def main():
         peaks = peak_fieldops(local)
         hist = stats["op_hist"]
         # field-op classes per witness (one bytecode instruction on one witness)
-        mul_cls = hist["MUL"] + hist["ACC_MUL"] + hist["ACC_MAC"] + hist["ACC_MACF"] + hist["ACC_ST"]
+        mul_cls = hist["MUL"] + hist["ACC_MUL"] + hist["ACC_MAC"] + hist["ACC_MACF"] + \
+            hist["ACC_ST"] + 2 * (hist["ACC_MUL2"] + hist["ACC_MAC2"])
         add_cls = hist["ADD"] + hist["SUB"] + hist["NEG"] + hist["ACC_ADD"] + hist["ACC_LD"] + \
             hist["CONST"] + hist["CHK"] + hist["DEN"]
-        div_cls = hist["DIV"]
+        div_cls = hist["DIV"] + hist["INV"]
         hash_cls = hist["HASH"] + hist["VAR"]
         # per launch (rank 0's image), W witnesses each; a DIV is 37 multiplies
         ops_launch = (mul_cls + add_cls + hash_cls + 38 * div_cls) * W

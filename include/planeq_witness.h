@@ -70,6 +70,8 @@ enum pqw_bop {
   PQW_B_END = 0, PQW_B_CONST, PQW_B_VAR, PQW_B_ADD, PQW_B_SUB, PQW_B_MUL, PQW_B_NEG,
   PQW_B_DIV, PQW_B_HASH, PQW_B_ACC_MUL, PQW_B_ACC_MAC, PQW_B_ACC_LD, PQW_B_ACC_ADD,
   PQW_B_ACC_ST, PQW_B_CHK, PQW_B_DEN, PQW_B_ACC_MACF, PQW_B_INV,
+  PQW_B_ACC_MUL2, /* acc = a*b + c*d; c, d packed as 16-bit slots in dst */
+  PQW_B_ACC_MAC2, /* acc = fold(acc) + a*b + c*d */
   PQW_B_NUM_OPS
 };
 
@@ -164,9 +166,9 @@ int pqw_probe(pqw_engine* e, int stage, uint32_t witness, uint32_t obl,
 int pqw_last_launch_ms(pqw_engine* e, float* ms);
 
 /* Totals of the uploaded image: out[0] = stages on the GPU, out[1] = bytecode
- * instructions, out[2] = max slots of a stage, out[3] = work items per witness
- * tile, out[4 + op] = instructions of each pqw_bop (out has 4 + PQW_B_NUM_OPS
- * entries). */
+ * instructions, out[2] = max slots of a stage, out[3] = shared-memory slots, out[4 + op] = instructions of each pqw_bop (out has 4 + PQW_B_NUM_OPS
+ * entries), out[4 + PQW_B_NUM_OPS] = instructions of the uploaded image after
+ * sharing identical programs, out[5 + PQW_B_NUM_OPS] = compile-cache hits. */
 int pqw_image_stats(pqw_engine* e, uint64_t* out, size_t cap);
 
 /* Measured integer-pipe ceiling of this device: field ops per second of

@@ -30,6 +30,7 @@ namespace {
 
 constexpr int32_t IR_MAGIC = 0x50515701;
 constexpr uint32_t NONE = 0xFFFFFFFFu;
+constexpr size_t CHUNK = 16;  // max operands of one n-ary sum / dot before chunking
 
 enum VKind : uint8_t { K_CONST = 0, K_VAR = 1, K_OP = 2 };
 enum VOp : uint8_t { O_NONE = 0, O_ADD, O_SUB, O_MUL, O_NEG, O_DIV, O_HASH, O_SUMN, O_DOT, O_INV };
@@ -327,6 +328,15 @@ struct Builder {
     if (terms.size() == 1) return terms[0];
     if (terms.size() == 2) return add(terms[0], terms[1]);
     std::sort(terms.begin(), terms.end());
+    if (terms.size() > CHUNK) {
+      // long sums become sums of chunk partials, so the schedule never needs
+      // more than CHUNK operands (plus the partials) live at once
+      std::vector<uint32_t> parts;
+      for (size_t i = 0; i < terms.size(); i += CHUNK)
+        parts.push_back(sumn(std::vector<uint32_t>(
+            terms.begin() + i, terms.begin() + std::min(terms.size(), i + CHUNK))));
+      return sumn(parts);
+    }
     uint32_t n = 0, d = 0;
     bool any_den = false;
     for (uint32_t t : terms) any_den |= vals[t].dden != 0;
@@ -361,6 +371,18 @@ struct Builder {
       return sumn(extra);
     }
     std::sort(pr.begin(), pr.end());
+    if (pr.size() > CHUNK) {
+      std::vector<uint32_t> parts = extra;
+      for (size_t i = 0; i < pr.size(); i += CHUNK) {
+        std::vector<uint32_t> xs2, ys2;
+        for (size_t j = i; j < std::min(pr.size(), i + CHUNK); ++j) {
+          xs2.push_back(pr[j].first);
+          ys2.push_back(pr[j].second);
+        }
+        parts.push_back(dot(xs2, ys2));
+      }
+      return sumn(parts);
+    }
     std::vector<uint32_t> flat;
     flat.reserve(pr.size() * 2);
     uint32_t n = 0, d = 0;
@@ -1258,7 +1280,7 @@ CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* con
     return n_spill++;
   };
 
-  std::vector<pqw_ins>& code = st.code;
+  std::vector<pqw_ins>& code = *st.code;
   auto put = [&](uint32_t op, uint32_t dst, uint32_t a, uint32_t b) {
     code.push_back(pqw_ins{op, dst, a, b});
   };
@@ -1287,7 +1309,7 @@ CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* con
     if (v.kind == K_CONST) {
       put(PQW_B_CONST, d, (uint32_t)v.aux, 0);
     } else if (v.kind == K_VAR) {
-      put(PQW_B_VAR, d, var_base + v.a, 0);
+      put(PQW_B_VAR, d, v.a, 0);  // stage-relative: the device adds the stage's var_base
     } else {
       switch (v.op) {
         case O_ADD: put(PQW_B_ADD, d, slot[v.a], slot[v.b]); break;
@@ -1307,6 +1329,19 @@ CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* con
         case O_DOT: {
           const uint32_t* L = &B.pool[v.a];
           uint32_t npair = v.b / 2;
+          bool narrow = true;  // two-product forms pack two slots as 16-bit fields
+          for (uint32_t i = 0; i < v.b; ++i) narrow &= slot[L[i]] < 0x10000u;
+          if (narrow && npair >= 2) {
+            auto pack = [&](uint32_t i) { return slot[L[2 * i]] | (slot[L[2 * i + 1]] << 16); };
+            // acc = p0 + p1 (< 2^63); then fold + two products per step (< 2^34 + 2^63)
+            put(PQW_B_ACC_MUL2, pack(1), slot[L[0]], slot[L[1]]);
+            uint32_t i = 2;
+            for (; i + 1 < npair; i += 2)
+              put(PQW_B_ACC_MAC2, pack(i + 1), slot[L[2 * i]], slot[L[2 * i + 1]]);
+            if (i < npair) put(PQW_B_ACC_MACF, 0, slot[L[2 * i]], slot[L[2 * i + 1]]);
+            put(PQW_B_ACC_ST, d, 0, 0);
+            break;
+          }
           put(PQW_B_ACC_MUL, 0, slot[L[0]], slot[L[1]]);
           // products < 2^62: three fit below 2^64; fold (to < 2^34) before a 4th
           uint32_t since_fold = 1;
@@ -1341,7 +1376,7 @@ CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* con
 
 std::vector<uint32_t> obligation_support(const CompiledStage& st, uint32_t obl) {
   std::vector<uint32_t> vars;
-  const auto& code = st.code;
+  const auto& code = *st.code;
   long pc = -1;
   for (long i = 0; i < (long)code.size(); ++i)
     if (code[i].op == PQW_B_CHK && code[i].dst == obl) {
@@ -1372,6 +1407,16 @@ std::vector<uint32_t> obligation_support(const CompiledStage& st, uint32_t obl) 
         break;
       case PQW_B_ACC_ADD:
         if (acc_needed) need.insert(in.a);
+        break;
+      case PQW_B_ACC_MUL2:
+      case PQW_B_ACC_MAC2:
+        if (acc_needed) {
+          need.insert(in.a);
+          need.insert(in.b);
+          need.insert(in.dst & 0xFFFFu);
+          need.insert(in.dst >> 16);
+          if (in.op == PQW_B_ACC_MUL2) acc_needed = false;
+        }
         break;
       case PQW_B_ACC_LD:
         if (acc_needed) {

@@ -2,6 +2,7 @@
 #pragma once
 #include <stdint.h>
 
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -22,7 +23,9 @@ struct CompiledStage {
   uint64_t degree = 0;
   uint64_t field_ops = 0;      // field operations per witness (roofline numerator)
   int64_t const_lhs = 0, const_rhs = 0, exact_lhs = INT64_MIN, exact_rhs = INT64_MIN;
-  std::vector<pqw_ins> code;   // terminated by PQW_B_END when status == OK
+  // terminated by PQW_B_END when status == OK; shared between stages whose
+  // programs are identical (VAR operands are stage-relative)
+  std::shared_ptr<std::vector<pqw_ins>> code = std::make_shared<std::vector<pqw_ins>>();
 };
 
 // Compile one stage. `var_base` is the global index of the stage's first

@@ -1,0 +1,351 @@
+// interp.cuh -- the sm_100a bytecode interpreter (device code of witness_kernel.cu).
+//
+// Work decomposition: a work item is (stage, CTA tile). A CTA of WARPS warps
+// takes WARPS consecutive warp tiles of one stage; each warp evaluates the
+// stage program for WT = 32 * VW witnesses, lane l owning witnesses
+// [wtile*WT + VW*l, +VW) and moving them with one 128-bit access per slot
+// read/write. The slot file is per warp and witness-innermost (slot s = 32
+// Vec = 512 contiguous bytes): fast slots (s < smem_slots) live in shared
+// memory, spill slots in per-warp global scratch. The grid is persistent
+// (SMs x occupancy) and pulls items from an atomic counter; stages are ordered
+// by descending cost so the longest programs start first.
+//
+// The instruction stream is warp-uniform (every lane runs the same program)
+// and shared by the CTA's warps (L1 hits after the first warp): decode is one
+// broadcast 128-bit load, prefetched one instruction ahead, plus an indirect
+// branch that never diverges; its cost is amortized over VW witnesses per lane.
+#pragma once
+
+#include <stdint.h>
+
+#include "../../include/planeq_witness.h"
+#include "field.hpp"
+
+namespace pqw {
+namespace {
+
+constexpr int VW = 4;
+constexpr int WARPS = 4;
+constexpr int BLOCK = 32 * WARPS;
+constexpr int WT = 32 * VW;          // witnesses per warp tile
+constexpr int TW = WT * WARPS;       // witnesses per CTA work item
+
+struct alignas(16) Vec {
+  uint32_t v[VW];
+};
+
+struct StageDesc {
+  uint32_t code_off;
+  uint32_t n_slots;
+  uint32_t var_base;
+  uint32_t result;  // index into result arrays
+};
+
+struct Params {
+  const uint4* code;
+  const StageDesc* stages;
+  const uint32_t* work;      // stage-desc index per work stage
+  const uint64_t* var_keys;
+  const uint64_t* fn_keys;   // 3 entries
+  uint32_t* counter;         // work-item counter
+  Vec* scratch;              // per-warp spill slot files
+  unsigned long long* first_bad;
+  uint32_t* n_valid;
+  uint32_t* n_bad;
+  uint32_t n_items;
+  uint32_t tiles;            // CTA work items per stage
+  uint32_t n_witness;
+  uint32_t smem_slots;       // fast slots per warp (shared memory)
+  uint32_t overflow_slots;   // per-warp spill capacity in slots
+  // probe mode
+  uint32_t probe_w;
+  uint32_t probe_obl;
+  uint32_t* probe_out;       // [lhs, rhs]
+  uint32_t* probe_vars;
+};
+
+// opcode bitmasks: which instruction fields are slot operands / a written slot
+constexpr uint32_t bit(int op) { return 1u << op; }
+constexpr uint32_t USES_Z =
+    bit(PQW_B_ADD) | bit(PQW_B_SUB) | bit(PQW_B_MUL) | bit(PQW_B_NEG) | bit(PQW_B_DIV) |
+    bit(PQW_B_INV) | bit(PQW_B_HASH) | bit(PQW_B_ACC_LD) | bit(PQW_B_ACC_ADD) | bit(PQW_B_ACC_MUL) |
+    bit(PQW_B_ACC_MAC) | bit(PQW_B_ACC_MACF) | bit(PQW_B_ACC_MUL2) | bit(PQW_B_ACC_MAC2) |
+    bit(PQW_B_CHK) | bit(PQW_B_DEN);
+constexpr uint32_t USES_W = bit(PQW_B_ADD) | bit(PQW_B_SUB) | bit(PQW_B_MUL) | bit(PQW_B_DIV) |
+                            bit(PQW_B_ACC_MUL) | bit(PQW_B_ACC_MAC) | bit(PQW_B_ACC_MACF) |
+                            bit(PQW_B_ACC_MUL2) | bit(PQW_B_ACC_MAC2) | bit(PQW_B_CHK);
+constexpr uint32_t WRITES_Y = bit(PQW_B_CONST) | bit(PQW_B_VAR) | bit(PQW_B_ADD) | bit(PQW_B_SUB) |
+                              bit(PQW_B_MUL) | bit(PQW_B_NEG) | bit(PQW_B_DIV) | bit(PQW_B_INV) |
+                              bit(PQW_B_HASH) | bit(PQW_B_ACC_ST);
+static_assert(PQW_B_NUM_OPS <= 32, "opcode masks are 32-bit");
+
+template <bool PROBE>
+__device__ __forceinline__ void run_item(const Params& p, Vec* wsm, Vec* wgs, uint32_t sdesc,
+                                         uint32_t wtile) {
+  const StageDesc sd = p.stages[sdesc];
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t w0 = PROBE ? p.probe_w : wtile * WT + lane * VW;
+  const uint32_t nsm = p.smem_slots;
+
+  // warp-uniform branch between the shared-memory file and the spill file
+  auto ld = [&](uint32_t s) -> Vec {
+    if (s < nsm) return wsm[s * 32u + lane];
+    return wgs[(size_t)(s - nsm) * 32u + lane];
+  };
+  auto st = [&](uint32_t s, const Vec& v) {
+    if (s < nsm)
+      wsm[s * 32u + lane] = v;
+    else
+      wgs[(size_t)(s - nsm) * 32u + lane] = v;
+  };
+
+  bool valid[VW];
+  uint32_t bad[VW];
+  uint64_t acc[VW];
+#pragma unroll
+  for (int j = 0; j < VW; ++j) {
+    valid[j] = PROBE ? (lane == 0 && j == 0) : (w0 + j) < p.n_witness;
+    bad[j] = 0xFFFFFFFFu;
+    acc[j] = 0;
+  }
+
+  // Software pipelining: the operands (z, w) of instruction pc+1 are loaded
+  // before instruction pc executes, so their latency (shared memory, or L1/L2
+  // for spill slots) overlaps its arithmetic; a value that pc itself writes is
+  // forwarded from the result register instead.
+  const uint4* code = p.code + sd.code_off;
+  uint4 in = __ldg(code);
+  Vec A = {}, B = {};
+  if ((USES_Z >> in.x) & 1u) A = ld(in.z);
+  if ((USES_W >> in.x) & 1u) B = ld(in.w);
+  for (uint32_t pc = 0;; ++pc) {
+    const uint4 nxt = __ldg(code + pc + 1);  // the image is padded with END: never past the end
+    Vec An = A, Bn = B;
+    const bool nz = (USES_Z >> nxt.x) & 1u, nw = (USES_W >> nxt.x) & 1u;
+    if (nz) An = ld(nxt.z);
+    if (nw) Bn = ld(nxt.w);
+    Vec r;
+    switch (in.x) {
+      case PQW_B_END:
+        goto done;
+      case PQW_B_CONST:
+#pragma unroll
+        for (int j = 0; j < VW; ++j) r.v[j] = in.z;
+        st(in.y, r);
+        break;
+      case PQW_B_VAR: {
+        const uint64_t key = __ldg(p.var_keys + sd.var_base + in.z);
+#pragma unroll
+        for (int j = 0; j < VW; ++j) r.v[j] = witness_value(key, w0 + j);
+        if (PROBE && lane == 0) p.probe_vars[in.z] = r.v[0];
+        st(in.y, r);
+        break;
+      }
+      case PQW_B_ADD: {
+        const Vec a = A, b = B;
+#pragma unroll
+        for (int j = 0; j < VW; ++j) r.v[j] = fadd(a.v[j], b.v[j]);
+        st(in.y, r);
+        break;
+      }
+      case PQW_B_SUB: {
+        const Vec a = A, b = B;
+#pragma unroll
+        for (int j = 0; j < VW; ++j) r.v[j] = fsub(a.v[j], b.v[j]);
+        st(in.y, r);
+        break;
+      }
+      case PQW_B_MUL: {
+        const Vec a = A, b = B;
+#pragma unroll
+        for (int j = 0; j < VW; ++j) r.v[j] = fmul(a.v[j], b.v[j]);
+        st(in.y, r);
+        break;
+      }
+      case PQW_B_NEG: {
+        const Vec a = A;
+#pragma unroll
+        for (int j = 0; j < VW; ++j) r.v[j] = fneg(a.v[j]);
+        st(in.y, r);
+        break;
+      }
+      case PQW_B_DIV: {
+        const Vec a = A, b = B;
+#pragma unroll
+        for (int j = 0; j < VW; ++j) r.v[j] = fmul(a.v[j], finv(b.v[j]));
+        st(in.y, r);
+        break;
+      }
+      case PQW_B_INV: {
+        const Vec a = A;
+#pragma unroll
+        for (int j = 0; j < VW; ++j) r.v[j] = finv(a.v[j]);
+        st(in.y, r);
+        break;
+      }
+      case PQW_B_HASH: {
+        const uint64_t key = __ldg(p.fn_keys + in.w);
+        const Vec a = A;
+#pragma unroll
+        for (int j = 0; j < VW; ++j) r.v[j] = uf_apply(key, a.v[j]);
+        st(in.y, r);
+        break;
+      }
+      case PQW_B_ACC_LD: {
+        const Vec a = A;
+#pragma unroll
+        for (int j = 0; j < VW; ++j) acc[j] = a.v[j];
+        break;
+      }
+      case PQW_B_ACC_ADD: {
+        const Vec a = A;
+#pragma unroll
+        for (int j = 0; j < VW; ++j) acc[j] += a.v[j];
+        break;
+      }
+      case PQW_B_ACC_MUL: {
+        const Vec a = A, b = B;
+#pragma unroll
+        for (int j = 0; j < VW; ++j) acc[j] = (uint64_t)a.v[j] * b.v[j];
+        break;
+      }
+      case PQW_B_ACC_MACF:
+#pragma unroll
+        for (int j = 0; j < VW; ++j) acc[j] = ffold64(acc[j]);
+        // fallthrough
+      case PQW_B_ACC_MAC: {
+        const Vec a = A, b = B;
+#pragma unroll
+        for (int j = 0; j < VW; ++j) acc[j] += (uint64_t)a.v[j] * b.v[j];
+        break;
+      }
+      case PQW_B_ACC_MUL2: {  // acc = a*b + c*d  (two products < 2^63)
+        const Vec a = A, b = B, c = ld(in.y & 0xFFFFu), d = ld(in.y >> 16);
+#pragma unroll
+        for (int j = 0; j < VW; ++j)
+          acc[j] = (uint64_t)a.v[j] * b.v[j] + (uint64_t)c.v[j] * d.v[j];
+        break;
+      }
+      case PQW_B_ACC_MAC2: {  // acc = fold(acc) + a*b + c*d  (< 2^34 + 2^63)
+        const Vec a = A, b = B, c = ld(in.y & 0xFFFFu), d = ld(in.y >> 16);
+#pragma unroll
+        for (int j = 0; j < VW; ++j)
+          acc[j] = ffold64(acc[j]) + (uint64_t)a.v[j] * b.v[j] + (uint64_t)c.v[j] * d.v[j];
+        break;
+      }
+      case PQW_B_ACC_ST:
+#pragma unroll
+        for (int j = 0; j < VW; ++j) r.v[j] = fred64(acc[j]);
+        st(in.y, r);
+        break;
+      case PQW_B_CHK: {
+        const Vec a = A, b = B;
+        if (PROBE && in.y == p.probe_obl && lane == 0) {
+          p.probe_out[0] = a.v[0];
+          p.probe_out[1] = b.v[0];
+        }
+#pragma unroll
+        for (int j = 0; j < VW; ++j)
+          if (a.v[j] != b.v[j]) bad[j] = min(bad[j], in.y);
+        break;
+      }
+      case PQW_B_DEN: {
+        const Vec a = A;
+#pragma unroll
+        for (int j = 0; j < VW; ++j)
+          if (a.v[j] == 0) valid[j] = false;
+        break;
+      }
+      default:
+        goto done;  // unreachable for a well-formed image
+    }
+    if ((WRITES_Y >> in.x) & 1u) {  // read-after-write on the prefetched operands
+      if (nz && nxt.z == in.y) An = r;
+      if (nw && nxt.w == in.y) Bn = r;
+    }
+    A = An;
+    B = Bn;
+    in = nxt;
+  }
+done:
+  if (PROBE) return;
+  unsigned long long best = ~0ull;
+  uint32_t nv = 0, nb = 0;
+#pragma unroll
+  for (int j = 0; j < VW; ++j) {
+    if (!valid[j]) continue;
+    nv++;
+    if (bad[j] != 0xFFFFFFFFu) {
+      nb++;
+      const unsigned long long k = ((unsigned long long)(w0 + j) << 32) | bad[j];
+      best = k < best ? k : best;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    nv += __shfl_down_sync(0xFFFFFFFFu, nv, off);
+    nb += __shfl_down_sync(0xFFFFFFFFu, nb, off);
+    const unsigned long long o = __shfl_down_sync(0xFFFFFFFFu, best, off);
+    best = o < best ? o : best;
+  }
+  if (lane == 0) {
+    if (nv) atomicAdd(p.n_valid + sd.result, nv);
+    if (nb) atomicAdd(p.n_bad + sd.result, nb);
+    if (best != ~0ull) atomicMin(p.first_bad + sd.result, best);
+  }
+}
+
+template <bool PROBE>
+__global__ void __launch_bounds__(BLOCK) eval_kernel(Params p) {
+  extern __shared__ Vec smem[];
+  __shared__ uint32_t s_item;
+  const uint32_t warp = threadIdx.x >> 5;
+  Vec* wsm = smem + (size_t)warp * p.smem_slots * 32;
+  Vec* wgs = p.scratch + ((size_t)blockIdx.x * WARPS + warp) * p.overflow_slots * 32;
+  if (PROBE) {
+    if (warp == 0) run_item<true>(p, wsm, wgs, p.work[0], 0);
+    return;
+  }
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(p.counter, 1u);
+    __syncthreads();
+    const uint32_t item = s_item;
+    __syncthreads();
+    if (item >= p.n_items) break;
+    const uint32_t tile = item % p.tiles;
+    const uint32_t wtile = tile * WARPS + warp;
+    // warps past the last witness skip the program entirely
+    if (wtile * WT < p.n_witness) run_item<false>(p, wsm, wgs, p.work[item / p.tiles], wtile);
+  }
+}
+
+// -- integer-pipe ceiling: register-resident field arithmetic, no decode, no memory.
+// KIND 0: fmul chains, 1: fadd chains, 2: keyed hash (mix64 + to_field).
+template <int KIND>
+__global__ void __launch_bounds__(256) peak_kernel(uint32_t* sink, int iters, uint32_t salt) {
+  uint32_t a[8], b[8];
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    a[j] = (t * 2654435761u + j * 40503u + salt) % P;
+    b[j] = (t * 2246822519u + j * 9973u + 7u) % P;
+  }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (KIND == 0) a[j] = fmul(a[j], b[j]);
+        else if (KIND == 1) a[j] = fadd(a[j], b[j]);
+        else a[j] = uf_apply(0x9E3779B97F4A7C15ull + b[j], a[j]);
+      }
+    }
+  }
+  uint32_t x = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) x ^= a[j];
+  if (x == salt * 2654435761u + 1u) sink[t] = x;  // opaque to the compiler: keeps chains live
+}
+
+}  // namespace
+}  // namespace pqw

@@ -1,20 +1,6 @@
-// witness_kernel.cu -- sm_100a bytecode interpreter for stage discharge, and
-// the extern "C" engine behind include/planeq_witness.h.
-//
-// Work decomposition: a work item is (stage, CTA tile). A CTA of WARPS warps
-// takes WARPS consecutive warp tiles of one stage; each warp evaluates the
-// stage program for WT = 32 * VW witnesses, lane l owning witnesses
-// [wtile*WT + VW*l, +VW) and moving them with one vector access per slot
-// read/write. The slot file is per warp, witness-innermost (slot s = 32
-// vec_t = 256 contiguous bytes): the first `smem_slots` slots live in shared
-// memory, the rest in per-warp global scratch (L1/L2-resident). The grid is
-// persistent (SMs x occupancy) and pulls items from an atomic counter; stages
-// are ordered by descending cost so the longest programs start first.
-//
-// The instruction stream is warp-uniform (every lane runs the same stage
-// program) and shared by the CTA's warps (L1 hits after the first warp), so
-// decode is a broadcast load, prefetched one instruction ahead, plus an
-// indirect branch that never diverges.
+// witness_kernel.cu -- host side of the sm_100a stage-discharge engine: the
+// extern "C" API of include/planeq_witness.h (compile, upload, launch, results,
+// probe). The device interpreter lives in interp.cuh.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -24,271 +10,16 @@
 #include <mutex>
 #include <numeric>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "compiler.hpp"
 #include "field.hpp"
 
+#include "interp.cuh"
+
 namespace pqw {
 namespace {
-
-// Each warp evaluates one stage program for WT = 32 * VW witnesses; a CTA of
-// WARPS warps runs WARPS consecutive witness tiles of the same stage, so the
-// instruction stream is fetched from L2 once and served to the other warps
-// from L1. VW witnesses per thread move with one vector access per slot.
-constexpr int VW = 2;
-constexpr int WARPS = 4;
-constexpr int BLOCK = 32 * WARPS;
-constexpr int WT = 32 * VW;          // witnesses per warp tile
-constexpr int TW = WT * WARPS;       // witnesses per CTA work item
-
-typedef uint2 vec_t;                 // VW u32 lanes
-static_assert(VW == 2, "vec_t is uint2");
-
-struct StageDesc {
-  uint32_t code_off;
-  uint32_t n_slots;
-  uint32_t var_base;
-  uint32_t result;  // index into result arrays
-};
-
-struct Params {
-  const uint4* code;
-  const StageDesc* stages;
-  const uint32_t* work;      // stage-desc index per work stage
-  const uint64_t* var_keys;
-  const uint64_t* fn_keys;   // 3 entries
-  uint32_t* counter;         // work-item counter
-  vec_t* scratch;            // per-warp overflow slot files
-  unsigned long long* first_bad;
-  uint32_t* n_valid;
-  uint32_t* n_bad;
-  uint32_t n_items;
-  uint32_t tiles;            // CTA work items per stage
-  uint32_t n_witness;
-  uint32_t smem_slots;       // slots per warp held in shared memory
-  uint32_t overflow_slots;   // per-warp scratch capacity in slots
-  // probe mode
-  uint32_t probe_w;
-  uint32_t probe_obl;
-  uint32_t* probe_out;       // [lhs, rhs]
-  uint32_t* probe_vars;
-};
-
-__device__ __forceinline__ vec_t vadd(vec_t a, vec_t b) { return make_uint2(fadd(a.x, b.x), fadd(a.y, b.y)); }
-__device__ __forceinline__ vec_t vsub(vec_t a, vec_t b) { return make_uint2(fsub(a.x, b.x), fsub(a.y, b.y)); }
-__device__ __forceinline__ vec_t vmul(vec_t a, vec_t b) { return make_uint2(fmul(a.x, b.x), fmul(a.y, b.y)); }
-
-template <bool PROBE>
-__device__ __forceinline__ void run_item(const Params& p, vec_t* wsm, vec_t* wgs, uint32_t sdesc,
-                                         uint32_t wtile) {
-  const StageDesc sd = p.stages[sdesc];
-  const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t w0 = PROBE ? p.probe_w : wtile * WT + lane * VW;
-  const uint32_t nsm = p.smem_slots;
-
-  // slot s of this warp: 32 vec_t (256 B) in shared memory (s < nsm, 32-bit
-  // LDS/STS addressing) or in global scratch (spill slots); the branch is
-  // warp-uniform
-  auto ld = [&](uint32_t s) -> vec_t {
-    if (s < nsm) return wsm[s * 32u + lane];
-    return wgs[(size_t)(s - nsm) * 32u + lane];
-  };
-  auto st = [&](uint32_t s, vec_t v) {
-    if (s < nsm)
-      wsm[s * 32u + lane] = v;
-    else
-      wgs[(size_t)(s - nsm) * 32u + lane] = v;
-  };
-
-  bool valid0 = PROBE ? lane == 0 : w0 < p.n_witness;
-  bool valid1 = PROBE ? false : (w0 + 1) < p.n_witness;
-  uint32_t bad0 = 0xFFFFFFFFu, bad1 = 0xFFFFFFFFu;
-  uint64_t acc0 = 0, acc1 = 0;
-
-  const uint4* code = p.code + sd.code_off;
-  uint4 nxt = __ldg(code);
-  for (uint32_t pc = 0;; ++pc) {
-    const uint4 in = nxt;
-    nxt = __ldg(code + pc + 1);  // prefetch: the image is padded with END, never past the end
-    switch (in.x) {
-      case PQW_B_END:
-        goto done;
-      case PQW_B_CONST:
-        st(in.y, make_uint2(in.z, in.z));
-        break;
-      case PQW_B_VAR: {
-        const uint64_t key = __ldg(p.var_keys + in.z);
-        vec_t v = make_uint2(witness_value(key, w0), witness_value(key, w0 + 1));
-        if (PROBE && lane == 0) p.probe_vars[in.z - sd.var_base] = v.x;
-        st(in.y, v);
-        break;
-      }
-      case PQW_B_ADD:
-        st(in.y, vadd(ld(in.z), ld(in.w)));
-        break;
-      case PQW_B_SUB:
-        st(in.y, vsub(ld(in.z), ld(in.w)));
-        break;
-      case PQW_B_MUL:
-        st(in.y, vmul(ld(in.z), ld(in.w)));
-        break;
-      case PQW_B_NEG: {
-        vec_t a = ld(in.z);
-        st(in.y, make_uint2(fneg(a.x), fneg(a.y)));
-        break;
-      }
-      case PQW_B_DIV: {
-        vec_t a = ld(in.z), b = ld(in.w);
-        st(in.y, make_uint2(fmul(a.x, finv(b.x)), fmul(a.y, finv(b.y))));
-        break;
-      }
-      case PQW_B_INV: {
-        vec_t a = ld(in.z);
-        st(in.y, make_uint2(finv(a.x), finv(a.y)));
-        break;
-      }
-      case PQW_B_HASH: {
-        const uint64_t key = __ldg(p.fn_keys + in.w);
-        vec_t a = ld(in.z);
-        st(in.y, make_uint2(uf_apply(key, a.x), uf_apply(key, a.y)));
-        break;
-      }
-      case PQW_B_ACC_LD: {
-        vec_t a = ld(in.z);
-        acc0 = a.x;
-        acc1 = a.y;
-        break;
-      }
-      case PQW_B_ACC_ADD: {
-        vec_t a = ld(in.z);
-        acc0 += a.x;
-        acc1 += a.y;
-        break;
-      }
-      case PQW_B_ACC_MUL: {
-        vec_t a = ld(in.z), b = ld(in.w);
-        acc0 = (uint64_t)a.x * b.x;
-        acc1 = (uint64_t)a.y * b.y;
-        break;
-      }
-      case PQW_B_ACC_MACF:
-        acc0 = ffold64(acc0);
-        acc1 = ffold64(acc1);
-        // fallthrough
-      case PQW_B_ACC_MAC: {
-        vec_t a = ld(in.z), b = ld(in.w);
-        acc0 += (uint64_t)a.x * b.x;
-        acc1 += (uint64_t)a.y * b.y;
-        break;
-      }
-      case PQW_B_ACC_ST:
-        st(in.y, make_uint2(fred64(acc0), fred64(acc1)));
-        break;
-      case PQW_B_CHK: {
-        vec_t a = ld(in.z), b = ld(in.w);
-        if (PROBE && in.y == p.probe_obl && lane == 0) {
-          p.probe_out[0] = a.x;
-          p.probe_out[1] = b.x;
-        }
-        if (a.x != b.x) bad0 = min(bad0, in.y);
-        if (a.y != b.y) bad1 = min(bad1, in.y);
-        break;
-      }
-      case PQW_B_DEN: {
-        vec_t a = ld(in.z);
-        if (a.x == 0) valid0 = false;
-        if (a.y == 0) valid1 = false;
-        break;
-      }
-      default:
-        goto done;  // unreachable for a well-formed image
-    }
-  }
-done:
-  if (PROBE) return;
-  unsigned long long best = ~0ull;
-  uint32_t nv = 0, nb = 0;
-  if (valid0) {
-    nv++;
-    if (bad0 != 0xFFFFFFFFu) {
-      nb++;
-      best = ((unsigned long long)w0 << 32) | bad0;
-    }
-  }
-  if (valid1) {
-    nv++;
-    if (bad1 != 0xFFFFFFFFu) {
-      nb++;
-      unsigned long long k = ((unsigned long long)(w0 + 1) << 32) | bad1;
-      best = k < best ? k : best;
-    }
-  }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    nv += __shfl_down_sync(0xFFFFFFFFu, nv, off);
-    nb += __shfl_down_sync(0xFFFFFFFFu, nb, off);
-    unsigned long long o = __shfl_down_sync(0xFFFFFFFFu, best, off);
-    best = o < best ? o : best;
-  }
-  if (lane == 0) {
-    if (nv) atomicAdd(p.n_valid + sd.result, nv);
-    if (nb) atomicAdd(p.n_bad + sd.result, nb);
-    if (best != ~0ull) atomicMin(p.first_bad + sd.result, best);
-  }
-}
-
-template <bool PROBE>
-__global__ void __launch_bounds__(BLOCK) eval_kernel(Params p) {
-  extern __shared__ vec_t smem[];
-  __shared__ uint32_t s_item;
-  const uint32_t warp = threadIdx.x >> 5;
-  vec_t* wsm = smem + (size_t)warp * p.smem_slots * 32;
-  vec_t* wgs = p.scratch + ((size_t)blockIdx.x * WARPS + warp) * p.overflow_slots * 32;
-  if (PROBE) {
-    if (warp == 0) run_item<true>(p, wsm, wgs, p.work[0], 0);
-    return;
-  }
-  for (;;) {
-    if (threadIdx.x == 0) s_item = atomicAdd(p.counter, 1u);
-    __syncthreads();
-    const uint32_t item = s_item;
-    __syncthreads();
-    if (item >= p.n_items) break;
-    const uint32_t tile = item % p.tiles;
-    const uint32_t wtile = tile * WARPS + warp;
-    // warps past the last witness skip the program entirely
-    if (wtile * WT < p.n_witness) run_item<false>(p, wsm, wgs, p.work[item / p.tiles], wtile);
-  }
-}
-
-// -- integer-pipe ceiling: register-resident field arithmetic, no decode, no memory.
-// KIND 0: fmul chains, 1: fadd chains, 2: keyed hash (mix64 + to_field).
-template <int KIND>
-__global__ void __launch_bounds__(256) peak_kernel(uint32_t* sink, int iters, uint32_t salt) {
-  uint32_t a[8], b[8];
-  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    a[j] = (t * 2654435761u + j * 40503u + salt) % P;
-    b[j] = (t * 2246822519u + j * 9973u + 7u) % P;
-  }
-  for (int it = 0; it < iters; ++it) {
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        if (KIND == 0) a[j] = fmul(a[j], b[j]);
-        else if (KIND == 1) a[j] = fadd(a[j], b[j]);
-        else a[j] = uf_apply(0x9E3779B97F4A7C15ull + b[j], a[j]);
-      }
-    }
-  }
-  uint32_t x = 0;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) x ^= a[j];
-  if (x == salt * 2654435761u + 1u) sink[t] = x;  // opaque to the compiler: keeps chains live
-}
 
 thread_local std::string g_err;
 
@@ -313,6 +44,11 @@ struct pqw_engine {
   uint64_t fn_keys[3] = {0, 0, 0};
   std::vector<pqw::CompiledStage> stages;
   std::vector<uint64_t> var_keys;
+  // program cache: text hash -> first stage compiled from it (+ its source for exact compare)
+  std::unordered_map<uint64_t, size_t> cache;
+  std::unordered_map<size_t, std::pair<std::vector<int32_t>, std::vector<int64_t>>> cache_src;
+  uint64_t cache_hits = 0;
+  uint64_t n_code_unique = 0;
   // device image
   bool uploaded = false;
   std::vector<int> gpu_stage_of;   // result index -> stage index
@@ -322,7 +58,7 @@ struct pqw_engine {
   uint64_t* d_var_keys = nullptr;
   uint64_t* d_fn_keys = nullptr;
   uint32_t* d_counter = nullptr;
-  pqw::vec_t* d_scratch = nullptr;
+  pqw::Vec* d_scratch = nullptr;
   unsigned long long* d_first_bad = nullptr;
   uint32_t* d_n_valid = nullptr;
   uint32_t* d_n_bad = nullptr;
@@ -419,12 +155,37 @@ int pqw_stage_add(pqw_engine* e, const int32_t* ir, size_t ir_len, const int64_t
   if (n_vars && !var_keys) return fail(PQW_EINVAL, "null var_keys");
   if (n_consts && !consts) return fail(PQW_EINVAL, "null consts");
   const uint32_t base = (uint32_t)e->var_keys.size();
+  // identical programs (e.g. the same layer repeated) compile once: the cache
+  // key is the program text; a hit shares the bytecode and only rebases vars
+  uint64_t h = pqw::mix64(0x5157ull ^ ir_len ^ ((uint64_t)n_consts << 32) ^ ((uint64_t)n_vars << 48));
+  for (size_t i = 0; i < ir_len; ++i) h = pqw::mix64(h + (uint32_t)ir[i]);
+  for (size_t i = 0; i < 3 * n_consts; ++i) h = pqw::mix64(h + (uint64_t)consts[i]);
   pqw::CompiledStage st;
-  try {
-    st = pqw::compile_stage(ir, ir_len, consts, n_consts, (uint32_t)n_vars, base, e->fn_keys,
-                            e->fast_slots);
-  } catch (const std::exception& ex) {
-    return fail(PQW_EINVAL, std::string("stage compile: ") + ex.what());
+  bool hit = false;
+  auto it = e->cache.find(h);
+  if (it != e->cache.end()) {
+    const auto& ent = e->cache_src[it->second];
+    if (ent.first.size() == ir_len && std::equal(ent.first.begin(), ent.first.end(), ir) &&
+        ent.second.size() == 3 * n_consts &&
+        std::equal(ent.second.begin(), ent.second.end(), consts)) {
+      st = e->stages[it->second];
+      st.var_base = base;
+      hit = true;
+      e->cache_hits++;
+    }
+  }
+  if (!hit) {
+    try {
+      st = pqw::compile_stage(ir, ir_len, consts, n_consts, (uint32_t)n_vars, base, e->fn_keys,
+                              e->fast_slots);
+    } catch (const std::exception& ex) {
+      return fail(PQW_EINVAL, std::string("stage compile: ") + ex.what());
+    }
+    if (it == e->cache.end()) {
+      e->cache.emplace(h, e->stages.size());
+      e->cache_src[e->stages.size()] = {std::vector<int32_t>(ir, ir + ir_len),
+                                        std::vector<int64_t>(consts, consts + 3 * n_consts)};
+    }
   }
   e->var_keys.insert(e->var_keys.end(), var_keys, var_keys + n_vars);
   for (int i = 0; i < 16; ++i) out_status[i] = 0;
@@ -433,7 +194,7 @@ int pqw_stage_add(pqw_engine* e, const int32_t* ir, size_t ir_len, const int64_t
   out_status[2] = st.n_obligations;
   out_status[3] = st.n_fast;
   out_status[4] = st.n_residual;
-  out_status[5] = (int64_t)st.code.size();
+  out_status[5] = (int64_t)st.code->size();
   out_status[6] = st.n_slots;
   out_status[7] = (int64_t)std::min<uint64_t>(st.degree, (uint64_t)INT64_MAX);
   out_status[8] = st.const_lhs;
@@ -455,6 +216,9 @@ int pqw_reset(pqw_engine* e) {
   }
   e->stages.clear();
   e->var_keys.clear();
+  e->cache.clear();
+  e->cache_src.clear();
+  e->cache_hits = 0;
   e->gpu_stage_of.clear();
   e->n_gpu_stages = 0;
   return PQW_OK;
@@ -464,8 +228,8 @@ long pqw_stage_bytecode(pqw_engine* e, int stage, pqw_ins* out, size_t cap, uint
   if (!e || stage < 0 || (size_t)stage >= e->stages.size()) return fail(PQW_EINVAL, "bad stage");
   const auto& st = e->stages[stage];
   if (n_slots) *n_slots = st.n_slots;
-  if (out) std::memcpy(out, st.code.data(), std::min(cap, st.code.size()) * sizeof(pqw_ins));
-  return (long)st.code.size();
+  if (out) std::memcpy(out, st.code->data(), std::min(cap, st.code->size()) * sizeof(pqw_ins));
+  return (long)st.code->size();
 }
 
 long pqw_obligation_support(pqw_engine* e, int stage, uint32_t obl, uint32_t* out, size_t cap) {
@@ -473,7 +237,7 @@ long pqw_obligation_support(pqw_engine* e, int stage, uint32_t obl, uint32_t* ou
   const auto& st = e->stages[stage];
   auto vars = pqw::obligation_support(st, obl);
   if (out)
-    for (size_t i = 0; i < std::min(cap, vars.size()); ++i) out[i] = vars[i] - st.var_base;
+    for (size_t i = 0; i < std::min(cap, vars.size()); ++i) out[i] = vars[i];
   return (long)vars.size();
 }
 
@@ -491,25 +255,36 @@ int pqw_upload(pqw_engine* e) {
   for (size_t i = 0; i < e->stages.size(); ++i)
     if (e->stages[i].status == PQW_STAGE_OK) ids.push_back((int)i);
   std::stable_sort(ids.begin(), ids.end(), [&](int a, int b) {
-    return e->stages[a].code.size() > e->stages[b].code.size();
+    return e->stages[a].code->size() > e->stages[b].code->size();
   });
   e->gpu_stage_of = ids;
   e->n_gpu_stages = (uint32_t)ids.size();
   std::vector<pqw_ins> code;
   std::vector<pqw::StageDesc> descs;
   std::vector<uint32_t> work;
+  std::unordered_map<const std::vector<pqw_ins>*, uint32_t> placed;  // shared programs: one copy
   e->max_slots = 0;
+  e->n_code = 0;
   std::fill(std::begin(e->op_hist), std::end(e->op_hist), 0);
   for (size_t r = 0; r < ids.size(); ++r) {
     const auto& st = e->stages[ids[r]];
-    descs.push_back({(uint32_t)code.size(), st.n_slots, st.var_base, (uint32_t)r});
-    code.insert(code.end(), st.code.begin(), st.code.end());
+    auto pit = placed.find(st.code.get());
+    uint32_t off;
+    if (pit == placed.end()) {
+      off = (uint32_t)code.size();
+      placed.emplace(st.code.get(), off);
+      code.insert(code.end(), st.code->begin(), st.code->end());
+    } else {
+      off = pit->second;
+    }
+    descs.push_back({off, st.n_slots, st.var_base, (uint32_t)r});
     work.push_back((uint32_t)r);
     e->max_slots = std::max(e->max_slots, st.n_slots);
-    for (const auto& in : st.code)
+    e->n_code += st.code->size();
+    for (const auto& in : *st.code)
       if (in.op < PQW_B_NUM_OPS) e->op_hist[in.op]++;
   }
-  e->n_code = code.size();
+  e->n_code_unique = code.size();
   if (code.empty()) code.push_back(pqw_ins{PQW_B_END, 0, 0, 0});
   code.push_back(pqw_ins{PQW_B_END, 0, 0, 0});  // the prefetching decoder reads one past END
   if (descs.empty()) descs.push_back({0, 0, 0, 0});
@@ -700,15 +475,15 @@ int pqw_last_launch_ms(pqw_engine* e, float* ms) {
 
 int pqw_image_stats(pqw_engine* e, uint64_t* out, size_t cap) {
   if (!e || !out) return fail(PQW_EINVAL, "null argument");
-  uint64_t buf[4 + PQW_B_NUM_OPS] = {};
+  uint64_t buf[6 + PQW_B_NUM_OPS] = {};
   uint64_t n_gpu = 0, n_code = 0, max_slots = 0;
   uint64_t hist[PQW_B_NUM_OPS] = {};
   for (const auto& st : e->stages) {
     if (st.status != PQW_STAGE_OK) continue;
     n_gpu++;
-    n_code += st.code.size();
+    n_code += st.code->size();
     max_slots = std::max<uint64_t>(max_slots, st.n_slots);
-    for (const auto& in : st.code)
+    for (const auto& in : *st.code)
       if (in.op < PQW_B_NUM_OPS) hist[in.op]++;
   }
   buf[0] = n_gpu;
@@ -716,7 +491,9 @@ int pqw_image_stats(pqw_engine* e, uint64_t* out, size_t cap) {
   buf[2] = max_slots;
   buf[3] = e->smem_slots;
   for (int i = 0; i < PQW_B_NUM_OPS; ++i) buf[4 + i] = hist[i];
-  std::memcpy(out, buf, std::min(cap, (size_t)(4 + PQW_B_NUM_OPS)) * sizeof(uint64_t));
+  buf[4 + PQW_B_NUM_OPS] = e->n_code_unique;
+  buf[5 + PQW_B_NUM_OPS] = e->cache_hits;
+  std::memcpy(out, buf, std::min(cap, (size_t)(6 + PQW_B_NUM_OPS)) * sizeof(uint64_t));
   return PQW_OK;
 }
 

@@ -30,7 +30,7 @@ STAGE_BAD_INDEX = 5
 
 # bytecode opcodes (pqw_bop)
 BOP_NAMES = ("END", "CONST", "VAR", "ADD", "SUB", "MUL", "NEG", "DIV", "HASH", "ACC_MUL",
-             "ACC_MAC", "ACC_LD", "ACC_ADD", "ACC_ST", "CHK", "DEN", "ACC_MACF", "INV")
+             "ACC_MAC", "ACC_LD", "ACC_ADD", "ACC_ST", "CHK", "DEN", "ACC_MACF", "INV", "ACC_MUL2", "ACC_MAC2")
 N_BOPS = len(BOP_NAMES)
 
 EXPORTS = ("pqw_abi_version", "pqw_last_error", "pqw_device_count", "pqw_engine_create",
@@ -245,8 +245,9 @@ class Engine:
         return float(ms.value)
 
     def image_stats(self) -> dict:
-        out = np.zeros(4 + N_BOPS, dtype=np.uint64)
+        out = np.zeros(6 + N_BOPS, dtype=np.uint64)
         self._check(self.lib.pqw_image_stats(self._h, _ptr(out, C.c_uint64), out.size))
         return {"gpu_stages": int(out[0]), "instructions": int(out[1]),
                 "max_slots": int(out[2]), "smem_slots": int(out[3]),
-                "op_hist": {BOP_NAMES[i]: int(out[4 + i]) for i in range(N_BOPS)}}
+                "op_hist": {BOP_NAMES[i]: int(out[4 + i]) for i in range(N_BOPS)},
+                "unique_instructions": int(out[4 + N_BOPS]), "cache_hits": int(out[5 + N_BOPS])}

@@ -161,6 +161,17 @@ def list_sites(plan: Plan, category: str) -> list[FaultSpec]:
         cons = g.consumers_map()
         sites = [FaultSpec(category, tid, {}) for tid, t in g.tensors.items()
                  if cons.get(tid) and t.dtype == "real" and not t.meta.get("mask")]
+    # -- extensions for the Llama/DeepSeek bug-injected configs (not in the reference)
+    elif category == "wrong_allreduce_scaling":
+        sites = [FaultSpec(category, n.id, {"factor": "1/tp"}) for n in g.nodes
+                 if n.kind in ("all_reduce", "reduce_scatter") and
+                 (n.id.startswith("ar.") or n.id.startswith("rs.") or n.id.startswith("tpar."))]
+    elif category == "misordered_concat":
+        sites = [FaultSpec(category, n.id, {"swap": [0, 1]}) for n in g.nodes
+                 if n.kind in ("all_gather", "all_to_all") and len(n.inputs) >= 2]
+    elif category == "dropped_partial_sum":
+        sites = [FaultSpec(category, n.id, {"slot": len(n.inputs) - 1}) for n in g.nodes
+                 if n.kind in ("all_reduce", "reduce_scatter") and len(n.inputs) >= 2]
     else:
         raise PlanEqError(f"unknown fault category {category!r}")
     return sites
@@ -248,6 +259,21 @@ def inject(plan: Plan, spec: FaultSpec) -> Plan:
             entry.shards[i + 1:]
     elif c == "extra_op":
         _insert_scale(g, spec.site, Fraction(2), "xop")
+    elif c == "wrong_allreduce_scaling":
+        # average instead of sum over the tensor group: every output scaled by 1/k
+        n = g.nodes[_find(g, spec.site)]
+        for out in n.outputs:
+            _insert_scale(g, out, Fraction(1, len(n.inputs)), "avg")
+    elif c == "misordered_concat":
+        n = g.nodes[_find(g, spec.site)]
+        i, j = spec.detail.get("swap", [0, 1])
+        ins = list(n.inputs)
+        ins[i], ins[j] = ins[j], ins[i]
+        _replace(g, n.id, inputs=ins)
+    elif c == "dropped_partial_sum":
+        # one partial never reaches the collective: it contributes zero
+        n = g.nodes[_find(g, spec.site)]
+        _insert_scale(g, n.inputs[int(spec.detail["slot"])], Fraction(0), "drop")
     else:
         raise PlanEqError(f"unknown fault category {c!r}")
     mutant.provenance = dict(mutant.provenance)

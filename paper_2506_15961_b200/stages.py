@@ -108,16 +108,19 @@ def build_stages(plan: Plan) -> tuple[list[Stage], dict[str, list[str]]]:
     claimed_p: set[str] = set()
     all_ckpt = set(lineage)
     earlier_shards: set[str] = set()
+    lmade, pmade = set(lprod), set(pprod)
+    lpos = {n.id: i for i, n in enumerate(logical.nodes)}
+    ppos = {n.id: i for i, n in enumerate(parallel.nodes)}
     for tid in order:
         if tid in lprod:
-            lnodes, lbound = backward_slice(logical, [tid], all_ckpt - {tid}, lprod)
-            lnodes = topo_sort(logical, lnodes)
+            lnodes, lbound = backward_slice(logical, [tid], all_ckpt - {tid}, lprod, lpos)
+            lnodes = topo_sort(logical, lnodes, lmade)
             for b in sorted(lbound):
                 if b not in lineage:
                     raise GraphError(f"stage {tid}: logical input {b!r} has no checkpoint entry")
             roots = [s.tensor for s in lineage[tid].shards]
-            pnodes, pbound = backward_slice(parallel, roots, earlier_shards, pprod)
-            pnodes = topo_sort(parallel, pnodes)
+            pnodes, pbound = backward_slice(parallel, roots, earlier_shards, pprod, ppos)
+            pnodes = topo_sort(parallel, pnodes, pmade)
             for b in sorted(pbound):
                 if b not in earlier_shards:
                     raise GraphError(f"stage {tid}: parallel input {b!r} is not a checkpoint shard")

@@ -1,16 +1,27 @@
-"""Named verification workloads for bench.py and the tests.
+"""Named verification workloads (the BASELINE.json configs) for bench.py and tests.
 
-A workload is a work plan (the plan the discharge step runs on). Round 1
-ships the reference's own reduced toy-decoder plans (committed fixtures under
-tests/golden/plans, produced by the reference's parallelizer and shape
-reducer); generated Llama-style plans are added by plangen.
+Every workload is a *work plan*: the plan the discharge step runs on.
+
+* reference toy plans: committed fixtures under tests/golden/plans (produced by
+  the reference's own parallelizer and shape reducer);
+* Llama-3 / DeepSeek-V3 family plans: generated here (builder -> completion ->
+  parallelize) at the minimal dimensions that keep every split non-degenerate
+  -- the same pattern the reference's reducer produces on the toy decoder
+  (batch = max(2, dp*nm), seq = 2 (a multiple of tp under sequence
+  parallelism), hidden = 2, head_dim = 2, heads = 2*tp, kv_heads = tp, ffn =
+  2*tp, vocab >= batch*seq and a multiple of tp). They are "shape-reduced by
+  construction": the z3-based minimizer (shapes.py, exact on the toy) stalls
+  on the grouped-query view products of these graphs, as the reference's does.
 """
 
 from __future__ import annotations
 
 import gzip
 import os
+from dataclasses import dataclass
 
+from . import builder, completion
+from .parallelize import ParallelConfig, parallelize
 from .plan import Plan, loads
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -21,7 +32,54 @@ FIXTURES = {
                          "reference toy decoder (2 layers), dp2 tp2 pp2 nm2, reduced by the reference"),
     "toy-tp2": ("tp2.work.json.gz", "reference toy decoder (2 layers), tp2, reduced by the reference"),
 }
-DEFAULT = "toy-dp2tp2pp2nm2"
+
+
+@dataclass(frozen=True)
+class LlamaPlanSpec:
+    layers: int
+    tp: int
+    pp: int
+    dp: int
+    nm: int
+    sp: bool
+    desc: str
+    family: str = "llama3"
+
+
+def reduced_llama_config(layers: int, tp: int, dp: int, nm: int, sp: bool,
+                         name: str = "llama") -> builder.LlamaConfig:
+    batch = max(2, dp * nm)
+    seq = max(2, tp) if sp else 2
+    vocab = batch * seq
+    vocab += (-vocab) % tp
+    return builder.LlamaConfig(layers=layers, hidden=2, heads=2 * tp, kv_heads=tp, seq=seq,
+                               vocab=vocab, batch=batch, ffn=2 * tp, head_dim=2, name=name)
+
+
+GENERATED = {
+    # BASELINE configs[0]
+    "llama-2l-tp2dp2": LlamaPlanSpec(2, tp=2, pp=1, dp=2, nm=1, sp=False,
+                                     desc="2-layer Llama-style decoder, TP=2 x DP=2, shape-reduced"),
+    # BASELINE configs[1] -- the N=1 bench workload
+    "llama3-8b-tp4pp2dp2-sp": LlamaPlanSpec(32, tp=4, pp=2, dp=2, nm=2, sp=True,
+                                            desc="Llama3-8B (32 layers, GQA) TP=4 PP=2 DP=2 nm=2 "
+                                                 "with sequence parallelism, shape-reduced"),
+    # BASELINE configs[3]
+    "llama3-405b-tp8pp16dp2": LlamaPlanSpec(126, tp=8, pp=16, dp=2, nm=2, sp=False,
+                                            desc="Llama3-405B (126 layers, GQA) TP=8 PP=16 DP=2 nm=2, "
+                                                 "shape-reduced full stage sweep"),
+    # small members of the same families (tests)
+    "llama-4l-tp2pp2dp2-sp": LlamaPlanSpec(4, tp=2, pp=2, dp=2, nm=2, sp=True,
+                                           desc="4-layer Llama-style decoder, TP=2 PP=2 DP=2 nm=2 SP"),
+}
+DEFAULT = "llama3-8b-tp4pp2dp2-sp"
+
+
+def llama_plan(spec: LlamaPlanSpec) -> Plan:
+    lc = reduced_llama_config(spec.layers, spec.tp, spec.dp, spec.nm, spec.sp)
+    g = completion.complete(builder.llama_forward(lc), completion.LossSpec("mean"))
+    cfg = ParallelConfig(dp=spec.dp, tp=spec.tp, pp=spec.pp, nm=spec.nm, sp=spec.sp)
+    return parallelize(g, cfg, lineage_interiors=builder.toy_interiors(g))
 
 
 def _fixture(fname: str) -> Plan:
@@ -35,4 +93,7 @@ def get_workload(name: str = "default") -> tuple[str, Plan]:
     if name in FIXTURES:
         fname, desc = FIXTURES[name]
         return f"{name}: {desc}", _fixture(fname)
-    raise KeyError(f"unknown workload {name!r}; known: {sorted(FIXTURES)}")
+    if name in GENERATED:
+        spec = GENERATED[name]
+        return f"{name}: {spec.desc}", llama_plan(spec)
+    raise KeyError(f"unknown workload {name!r}; known: {sorted(FIXTURES) + sorted(GENERATED)}")

@@ -14,7 +14,7 @@ import numpy as np
 from oracle import m31
 
 OPS = ("END", "CONST", "VAR", "ADD", "SUB", "MUL", "NEG", "DIV", "HASH", "ACC_MUL", "ACC_MAC",
-       "ACC_LD", "ACC_ADD", "ACC_ST", "CHK", "DEN", "ACC_MACF", "INV")
+       "ACC_LD", "ACC_ADD", "ACC_ST", "CHK", "DEN", "ACC_MACF", "INV", "ACC_MUL2", "ACC_MAC2")
 FN = ("EXP", "RSQRT", "SIGMOID")
 
 
@@ -34,7 +34,7 @@ def run(code: np.ndarray, n_slots: int, var_keys: np.ndarray, var_base: int, see
         if name == "CONST":
             slots[dst] = a
         elif name == "VAR":
-            key = np.uint64(var_keys[a - var_base])
+            key = np.uint64(var_keys[a])  # VAR operands are stage-relative
             with np.errstate(over="ignore"):
                 slots[dst] = m31.to_field(m31.mix64(key + w1 * m31.GOLDEN))
         elif name == "ADD":
@@ -61,6 +61,17 @@ def run(code: np.ndarray, n_slots: int, var_keys: np.ndarray, var_base: int, see
             if name == "ACC_MACF":
                 acc = np.array([(int(v) & m31.PI) + (int(v) >> 31) for v in acc], dtype=object)
             acc = acc + slots[a].astype(object) * slots[b].astype(object)
+            assert all(int(v) < (1 << 64) for v in acc), "accumulator overflow"
+        elif name == "ACC_MUL2":
+            c, d = dst & 0xFFFF, dst >> 16
+            acc = slots[a].astype(object) * slots[b].astype(object) + \
+                slots[c].astype(object) * slots[d].astype(object)
+            assert all(int(v) < (1 << 64) for v in acc), "accumulator overflow"
+        elif name == "ACC_MAC2":
+            c, d = dst & 0xFFFF, dst >> 16
+            acc = np.array([(int(v) & m31.PI) + (int(v) >> 31) for v in acc], dtype=object)
+            acc = acc + slots[a].astype(object) * slots[b].astype(object) + \
+                slots[c].astype(object) * slots[d].astype(object)
             assert all(int(v) < (1 << 64) for v in acc), "accumulator overflow"
         elif name == "ACC_ST":
             slots[dst] = np.array([int(v) % m31.PI for v in acc], dtype=np.uint64)

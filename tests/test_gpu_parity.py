@@ -35,6 +35,8 @@ def test_stage_verdicts_match_reference(gpu, rec):
     ref = rec["default"]
     if "stage_status" not in ref:
         pytest.skip(f"reference raised {ref.get('error')} before discharge")
+    if ref.get("refuted_by") == "structure":
+        pytest.skip("reference refuted the plan structurally (lineage tiling) before discharge")
     results, cancelled, _ = discharge(plan, stages, VerifyOptions(no_cancel=True, witnesses=W))
     assert cancelled == 0
     got = [(r.target, r.status) for r in results]
