@@ -64,21 +64,6 @@ struct Params {
   uint32_t* probe_vars;
 };
 
-// opcode bitmasks: which instruction fields are slot operands / a written slot
-constexpr uint32_t bit(int op) { return 1u << op; }
-constexpr uint32_t USES_Z =
-    bit(PQW_B_ADD) | bit(PQW_B_SUB) | bit(PQW_B_MUL) | bit(PQW_B_NEG) | bit(PQW_B_DIV) |
-    bit(PQW_B_INV) | bit(PQW_B_HASH) | bit(PQW_B_ACC_LD) | bit(PQW_B_ACC_ADD) | bit(PQW_B_ACC_MUL) |
-    bit(PQW_B_ACC_MAC) | bit(PQW_B_ACC_MACF) | bit(PQW_B_ACC_MUL2) | bit(PQW_B_ACC_MAC2) |
-    bit(PQW_B_CHK) | bit(PQW_B_DEN);
-constexpr uint32_t USES_W = bit(PQW_B_ADD) | bit(PQW_B_SUB) | bit(PQW_B_MUL) | bit(PQW_B_DIV) |
-                            bit(PQW_B_ACC_MUL) | bit(PQW_B_ACC_MAC) | bit(PQW_B_ACC_MACF) |
-                            bit(PQW_B_ACC_MUL2) | bit(PQW_B_ACC_MAC2) | bit(PQW_B_CHK);
-constexpr uint32_t WRITES_Y = bit(PQW_B_CONST) | bit(PQW_B_VAR) | bit(PQW_B_ADD) | bit(PQW_B_SUB) |
-                              bit(PQW_B_MUL) | bit(PQW_B_NEG) | bit(PQW_B_DIV) | bit(PQW_B_INV) |
-                              bit(PQW_B_HASH) | bit(PQW_B_ACC_ST);
-static_assert(PQW_B_NUM_OPS <= 32, "opcode masks are 32-bit");
-
 template <bool PROBE>
 __device__ __forceinline__ void run_item(const Params& p, Vec* wsm, Vec* wgs, uint32_t sdesc,
                                          uint32_t wtile) {
@@ -109,21 +94,11 @@ __device__ __forceinline__ void run_item(const Params& p, Vec* wsm, Vec* wgs, ui
     acc[j] = 0;
   }
 
-  // Software pipelining: the operands (z, w) of instruction pc+1 are loaded
-  // before instruction pc executes, so their latency (shared memory, or L1/L2
-  // for spill slots) overlaps its arithmetic; a value that pc itself writes is
-  // forwarded from the result register instead.
   const uint4* code = p.code + sd.code_off;
-  uint4 in = __ldg(code);
-  Vec A = {}, B = {};
-  if ((USES_Z >> in.x) & 1u) A = ld(in.z);
-  if ((USES_W >> in.x) & 1u) B = ld(in.w);
+  uint4 nxt = __ldg(code);
   for (uint32_t pc = 0;; ++pc) {
-    const uint4 nxt = __ldg(code + pc + 1);  // the image is padded with END: never past the end
-    Vec An = A, Bn = B;
-    const bool nz = (USES_Z >> nxt.x) & 1u, nw = (USES_W >> nxt.x) & 1u;
-    if (nz) An = ld(nxt.z);
-    if (nw) Bn = ld(nxt.w);
+    const uint4 in = nxt;
+    nxt = __ldg(code + pc + 1);  // the image is padded with END: never past the end
     Vec r;
     switch (in.x) {
       case PQW_B_END:
@@ -142,42 +117,42 @@ __device__ __forceinline__ void run_item(const Params& p, Vec* wsm, Vec* wgs, ui
         break;
       }
       case PQW_B_ADD: {
-        const Vec a = A, b = B;
+        const Vec a = ld(in.z), b = ld(in.w);
 #pragma unroll
         for (int j = 0; j < VW; ++j) r.v[j] = fadd(a.v[j], b.v[j]);
         st(in.y, r);
         break;
       }
       case PQW_B_SUB: {
-        const Vec a = A, b = B;
+        const Vec a = ld(in.z), b = ld(in.w);
 #pragma unroll
         for (int j = 0; j < VW; ++j) r.v[j] = fsub(a.v[j], b.v[j]);
         st(in.y, r);
         break;
       }
       case PQW_B_MUL: {
-        const Vec a = A, b = B;
+        const Vec a = ld(in.z), b = ld(in.w);
 #pragma unroll
         for (int j = 0; j < VW; ++j) r.v[j] = fmul(a.v[j], b.v[j]);
         st(in.y, r);
         break;
       }
       case PQW_B_NEG: {
-        const Vec a = A;
+        const Vec a = ld(in.z);
 #pragma unroll
         for (int j = 0; j < VW; ++j) r.v[j] = fneg(a.v[j]);
         st(in.y, r);
         break;
       }
       case PQW_B_DIV: {
-        const Vec a = A, b = B;
+        const Vec a = ld(in.z), b = ld(in.w);
 #pragma unroll
         for (int j = 0; j < VW; ++j) r.v[j] = fmul(a.v[j], finv(b.v[j]));
         st(in.y, r);
         break;
       }
       case PQW_B_INV: {
-        const Vec a = A;
+        const Vec a = ld(in.z);
 #pragma unroll
         for (int j = 0; j < VW; ++j) r.v[j] = finv(a.v[j]);
         st(in.y, r);
@@ -185,26 +160,26 @@ __device__ __forceinline__ void run_item(const Params& p, Vec* wsm, Vec* wgs, ui
       }
       case PQW_B_HASH: {
         const uint64_t key = __ldg(p.fn_keys + in.w);
-        const Vec a = A;
+        const Vec a = ld(in.z);
 #pragma unroll
         for (int j = 0; j < VW; ++j) r.v[j] = uf_apply(key, a.v[j]);
         st(in.y, r);
         break;
       }
       case PQW_B_ACC_LD: {
-        const Vec a = A;
+        const Vec a = ld(in.z);
 #pragma unroll
         for (int j = 0; j < VW; ++j) acc[j] = a.v[j];
         break;
       }
       case PQW_B_ACC_ADD: {
-        const Vec a = A;
+        const Vec a = ld(in.z);
 #pragma unroll
         for (int j = 0; j < VW; ++j) acc[j] += a.v[j];
         break;
       }
       case PQW_B_ACC_MUL: {
-        const Vec a = A, b = B;
+        const Vec a = ld(in.z), b = ld(in.w);
 #pragma unroll
         for (int j = 0; j < VW; ++j) acc[j] = (uint64_t)a.v[j] * b.v[j];
         break;
@@ -214,20 +189,20 @@ __device__ __forceinline__ void run_item(const Params& p, Vec* wsm, Vec* wgs, ui
         for (int j = 0; j < VW; ++j) acc[j] = ffold64(acc[j]);
         // fallthrough
       case PQW_B_ACC_MAC: {
-        const Vec a = A, b = B;
+        const Vec a = ld(in.z), b = ld(in.w);
 #pragma unroll
         for (int j = 0; j < VW; ++j) acc[j] += (uint64_t)a.v[j] * b.v[j];
         break;
       }
       case PQW_B_ACC_MUL2: {  // acc = a*b + c*d  (two products < 2^63)
-        const Vec a = A, b = B, c = ld(in.y & 0xFFFFu), d = ld(in.y >> 16);
+        const Vec a = ld(in.z), b = ld(in.w), c = ld(in.y & 0xFFFFu), d = ld(in.y >> 16);
 #pragma unroll
         for (int j = 0; j < VW; ++j)
           acc[j] = (uint64_t)a.v[j] * b.v[j] + (uint64_t)c.v[j] * d.v[j];
         break;
       }
       case PQW_B_ACC_MAC2: {  // acc = fold(acc) + a*b + c*d  (< 2^34 + 2^63)
-        const Vec a = A, b = B, c = ld(in.y & 0xFFFFu), d = ld(in.y >> 16);
+        const Vec a = ld(in.z), b = ld(in.w), c = ld(in.y & 0xFFFFu), d = ld(in.y >> 16);
 #pragma unroll
         for (int j = 0; j < VW; ++j)
           acc[j] = ffold64(acc[j]) + (uint64_t)a.v[j] * b.v[j] + (uint64_t)c.v[j] * d.v[j];
@@ -239,7 +214,7 @@ __device__ __forceinline__ void run_item(const Params& p, Vec* wsm, Vec* wgs, ui
         st(in.y, r);
         break;
       case PQW_B_CHK: {
-        const Vec a = A, b = B;
+        const Vec a = ld(in.z), b = ld(in.w);
         if (PROBE && in.y == p.probe_obl && lane == 0) {
           p.probe_out[0] = a.v[0];
           p.probe_out[1] = b.v[0];
@@ -250,7 +225,7 @@ __device__ __forceinline__ void run_item(const Params& p, Vec* wsm, Vec* wgs, ui
         break;
       }
       case PQW_B_DEN: {
-        const Vec a = A;
+        const Vec a = ld(in.z);
 #pragma unroll
         for (int j = 0; j < VW; ++j)
           if (a.v[j] == 0) valid[j] = false;
@@ -259,13 +234,6 @@ __device__ __forceinline__ void run_item(const Params& p, Vec* wsm, Vec* wgs, ui
       default:
         goto done;  // unreachable for a well-formed image
     }
-    if ((WRITES_Y >> in.x) & 1u) {  // read-after-write on the prefetched operands
-      if (nz && nxt.z == in.y) An = r;
-      if (nw && nxt.w == in.y) Bn = r;
-    }
-    A = An;
-    B = Bn;
-    in = nxt;
   }
 done:
   if (PROBE) return;
