@@ -72,6 +72,7 @@ enum pqw_bop {
   PQW_B_ACC_ST, PQW_B_CHK, PQW_B_DEN, PQW_B_ACC_MACF, PQW_B_INV,
   PQW_B_ACC_MUL2, /* acc = a*b + c*d; c, d packed as 16-bit slots in dst */
   PQW_B_ACC_MAC2, /* acc = fold(acc) + a*b + c*d */
+  PQW_B_BAR,      /* phase boundary: CTA barrier (cooperative programs) */
   PQW_B_NUM_OPS
 };
 

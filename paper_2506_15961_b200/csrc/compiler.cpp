@@ -31,6 +31,7 @@ namespace {
 constexpr int32_t IR_MAGIC = 0x50515701;
 constexpr uint32_t NONE = 0xFFFFFFFFu;
 constexpr size_t CHUNK = 16;  // max operands of one n-ary sum / dot before chunking
+constexpr size_t UNITS_PER_WARP = 4;  // scheduling units per warp per phase
 
 enum VKind : uint8_t { K_CONST = 0, K_VAR = 1, K_OP = 2 };
 enum VOp : uint8_t { O_NONE = 0, O_ADD, O_SUB, O_MUL, O_NEG, O_DIV, O_HASH, O_SUMN, O_DOT, O_INV };
@@ -1093,9 +1094,12 @@ struct Emitter {
 
 CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* consts,
                             size_t n_consts, uint32_t n_vars, uint32_t var_base,
-                            const uint64_t fn_keys[3], uint32_t smem_slots) {
+                            const uint64_t fn_keys[3], uint32_t smem_slots,
+                            uint32_t n_warps) {
   CompiledStage st;
   st.n_vars = n_vars;
+  st.n_warps = n_warps;
+  if (n_warps < 1 || n_warps > 32) bad("n_warps must be in [1, 32]");
   st.var_base = var_base;
   Compiler C;
   C.B.fn_keys = fn_keys;
@@ -1197,115 +1201,175 @@ CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* con
   }
   for (uint32_t d : B.dens) E.emit_value(d);
 
-  // last use per value (group index)
+  // ---- cooperative schedule --------------------------------------------------
+  // Units are emitter groups (a value, a check, a definedness test). A CTA of
+  // n_warps warps evaluates the stage for 32 witnesses (one per lane) out of a
+  // shared value file; the program is list-scheduled into phases separated by
+  // CTA barriers: a unit is ready once every unit it reads from ran in an
+  // earlier phase, ready units are taken in depth-first (obligation) order --
+  // the order that keeps the live set small -- up to UNITS_PER_WARP per warp,
+  // and spread over the warps by instruction count.
   const size_t G = E.groups.size();
-  std::vector<int32_t> last(B.vals.size(), -1);
   std::vector<uint32_t> ops;
-  for (size_t g = 0; g < G; ++g) {
+  std::vector<int32_t> unit_of(B.vals.size(), -1);  // value -> defining group
+  for (size_t g = 0; g < G; ++g)
+    if (E.groups[g].kind == 0) unit_of[E.groups[g].v] = (int32_t)g;
+  auto reads_of = [&](size_t g, std::vector<uint32_t>& out) {
     const auto& gr = E.groups[g];
+    out.clear();
     if (gr.kind == 0) {
-      E.operands(gr.v, ops);
-      for (uint32_t u : ops) last[u] = (int32_t)g;
+      E.operands(gr.v, out);
     } else if (gr.kind == 1) {
-      last[gr.l] = (int32_t)g;
-      last[gr.r] = (int32_t)g;
+      out.push_back(gr.l);
+      out.push_back(gr.r);
     } else {
-      last[gr.v] = std::max(last[gr.v], (int32_t)g);
+      out.push_back(gr.v);
+    }
+  };
+  auto cost_of = [&](size_t g) -> uint32_t {
+    const auto& gr = E.groups[g];
+    if (gr.kind != 0) return 1;
+    const Val& v = B.vals[gr.v];
+    if (v.kind == K_OP && v.op == O_SUMN) return v.b + 1;
+    if (v.kind == K_OP && v.op == O_DOT) return v.b / 4 + 2;
+    return 1;
+  };
+  std::vector<std::vector<uint32_t>> users(G);
+  std::vector<uint32_t> indeg(G, 0);
+  for (size_t g = 0; g < G; ++g) {
+    reads_of(g, ops);
+    std::sort(ops.begin(), ops.end());
+    ops.erase(std::unique(ops.begin(), ops.end()), ops.end());
+    for (uint32_t u : ops) {
+      int32_t d = unit_of[u];
+      if (d < 0) bad("internal: operand without a defining unit");
+      users[d].push_back((uint32_t)g);
+      indeg[g]++;
     }
   }
+  const uint32_t NW = n_warps;
+  const size_t CAP = (size_t)NW * UNITS_PER_WARP;
+  std::vector<int32_t> phase_of(G, -1), warp_of(G, -1);
+  std::vector<std::vector<uint32_t>> phases;
+  {
+    std::priority_queue<uint32_t, std::vector<uint32_t>, std::greater<uint32_t>> ready;
+    for (size_t g = 0; g < G; ++g)
+      if (indeg[g] == 0) ready.push((uint32_t)g);
+    std::vector<uint32_t> load(NW);
+    while (!ready.empty()) {
+      std::vector<uint32_t> batch;
+      while (!ready.empty() && batch.size() < CAP) {
+        batch.push_back(ready.top());
+        ready.pop();
+      }
+      const int32_t p = (int32_t)phases.size();
+      std::fill(load.begin(), load.end(), 0);
+      for (uint32_t g : batch) {
+        uint32_t w = (uint32_t)(std::min_element(load.begin(), load.end()) - load.begin());
+        load[w] += cost_of(g);
+        phase_of[g] = p;
+        warp_of[g] = (int32_t)w;
+      }
+      for (uint32_t g : batch)
+        for (uint32_t u : users[g])
+          if (--indeg[u] == 0) ready.push(u);
+      phases.push_back(std::move(batch));
+    }
+  }
+  for (size_t g = 0; g < G; ++g)
+    if (phase_of[g] < 0) bad("internal: unscheduled unit (cycle)");
 
-  // Two-level slot allocation. Slots [0, smem_slots) are the fast file (shared
-  // memory on the device), the rest spill to per-warp global scratch. A value
-  // occupies its slot over the group interval (def, last]: operands are read
-  // before a group writes its result, so a value may take the slot of one that
-  // dies in the same group. Fast slots go to the intervals with the most reads
-  // per group of lifetime (shortest, busiest first); the rest get spill slots
-  // by linear scan.
-  std::vector<int32_t> def(B.vals.size(), -1);
+  // liveness on phases: a value written in phase d is readable from d+1 on and
+  // holds its slot through its last reading phase l; another value may take the
+  // slot only from a phase strictly after l (warps of one phase run unordered)
+  std::vector<int32_t> defp(B.vals.size(), -1), lastp(B.vals.size(), -1);
   std::vector<uint32_t> uses(B.vals.size(), 0);
   for (size_t g = 0; g < G; ++g) {
-    const auto& gr = E.groups[g];
-    if (gr.kind == 0) {
-      def[gr.v] = (int32_t)g;
-      E.operands(gr.v, ops);
-      for (uint32_t u : ops) uses[u]++;
-    } else if (gr.kind == 1) {
-      uses[gr.l]++;
-      uses[gr.r]++;
-    } else {
-      uses[gr.v]++;
+    if (E.groups[g].kind == 0) defp[E.groups[g].v] = phase_of[g];
+    reads_of(g, ops);
+    for (uint32_t u : ops) {
+      lastp[u] = std::max(lastp[u], phase_of[g]);
+      uses[u]++;
     }
   }
   std::vector<uint32_t> slot(B.vals.size(), NONE);
   std::vector<uint32_t> cand;
   for (size_t g = 0; g < G; ++g)
-    if (E.groups[g].kind == 0 && last[E.groups[g].v] >= 0) cand.push_back(E.groups[g].v);
+    if (E.groups[g].kind == 0 && lastp[E.groups[g].v] >= 0) cand.push_back(E.groups[g].v);
+  // fast file: busiest values per phase of lifetime first, packed into slots
   std::stable_sort(cand.begin(), cand.end(), [&](uint32_t a, uint32_t b) {
-    // uses / span, compared without division
-    uint64_t sa = (uint64_t)(last[a] - def[a]), sb = (uint64_t)(last[b] - def[b]);
+    uint64_t sa = (uint64_t)(lastp[a] - defp[a] + 1), sb = (uint64_t)(lastp[b] - defp[b] + 1);
     return (uint64_t)uses[a] * sb > (uint64_t)uses[b] * sa;
   });
-  std::vector<std::map<int32_t, int32_t>> occ(smem_slots);  // start -> end, per fast slot
+  std::vector<std::map<int32_t, int32_t>> occ(smem_slots);  // closed intervals start -> end
   uint32_t fast_used = 0;
+  // next-fit start hint: most slots are full early, scanning from a rotating
+  // origin keeps the packing near-linear
   for (uint32_t v : cand) {
-    const int32_t s0 = def[v], s1 = last[v];
+    const int32_t s0 = defp[v], s1 = lastp[v];
     for (uint32_t k = 0; k < smem_slots; ++k) {
       auto& m = occ[k];
       auto it = m.lower_bound(s0);
-      if (it != m.end() && it->first < s1) continue;       // next interval starts inside
-      if (it != m.begin() && std::prev(it)->second > s0) continue;  // previous reaches in
+      if (it != m.end() && it->first <= s1) continue;
+      if (it != m.begin() && std::prev(it)->second >= s0) continue;
       m.emplace(s0, s1);
       slot[v] = k;
       fast_used = std::max(fast_used, k + 1);
       break;
     }
   }
-  std::priority_queue<uint32_t, std::vector<uint32_t>, std::greater<uint32_t>> free_spill;
+  // spill file: linear scan over phases
+  std::vector<uint32_t> spill_vals;
+  for (uint32_t v : cand)
+    if (slot[v] == NONE) spill_vals.push_back(v);
+  std::sort(spill_vals.begin(), spill_vals.end(),
+            [&](uint32_t a, uint32_t b) { return defp[a] < defp[b]; });
   uint32_t n_spill = 0;
-  auto release_dead = [&](const std::vector<uint32_t>& used, int32_t g) {
-    for (size_t i = 0; i < used.size(); ++i) {
-      uint32_t u = used[i];
-      bool dup = false;
-      for (size_t j = 0; j < i; ++j) dup |= used[j] == u;
-      if (!dup && last[u] == g && slot[u] != NONE && slot[u] >= smem_slots)
-        free_spill.push(slot[u] - smem_slots);
+  {
+    // (release phase, slot) min-heap; a slot released after phase l serves defs > l
+    std::priority_queue<std::pair<int32_t, uint32_t>, std::vector<std::pair<int32_t, uint32_t>>,
+                        std::greater<std::pair<int32_t, uint32_t>>> busy;
+    std::priority_queue<uint32_t, std::vector<uint32_t>, std::greater<uint32_t>> free_s;
+    for (uint32_t v : spill_vals) {
+      while (!busy.empty() && busy.top().first < defp[v]) {
+        free_s.push(busy.top().second);
+        busy.pop();
+      }
+      uint32_t s;
+      if (!free_s.empty()) {
+        s = free_s.top();
+        free_s.pop();
+      } else {
+        s = n_spill++;
+      }
+      slot[v] = smem_slots + s;
+      busy.push({lastp[v], s});
     }
-  };
-  auto take_spill = [&]() -> uint32_t {
-    if (!free_spill.empty()) {
-      uint32_t s = free_spill.top();
-      free_spill.pop();
-      return s;
-    }
-    return n_spill++;
-  };
+  }
 
+  // emission: a table of per-warp stream offsets, then one stream per warp;
+  // every stream has one BAR per phase boundary and ends with END
   std::vector<pqw_ins>& code = *st.code;
+  const uint32_t table = (NW + 3) / 4;
+  code.assign(table, pqw_ins{PQW_B_END, 0, 0, 0});
+  std::vector<std::vector<uint32_t>> per_warp_phase(NW);
   auto put = [&](uint32_t op, uint32_t dst, uint32_t a, uint32_t b) {
     code.push_back(pqw_ins{op, dst, a, b});
   };
-  for (size_t g = 0; g < G; ++g) {
+  auto emit_unit = [&](uint32_t g) {
     const auto& gr = E.groups[g];
     if (gr.kind == 1) {
       put(PQW_B_CHK, gr.obl, slot[gr.l], slot[gr.r]);
-      std::vector<uint32_t> used{gr.l, gr.r};
-      release_dead(used, (int32_t)g);
-      continue;
+      return;
     }
     if (gr.kind == 2) {
       put(PQW_B_DEN, 0, slot[gr.v], 0);
-      std::vector<uint32_t> used{gr.v};
-      release_dead(used, (int32_t)g);
-      continue;
+      return;
     }
-    uint32_t id = gr.v;
+    const uint32_t id = gr.v;
     const Val& v = B.vals[id];
-    E.operands(id, ops);
-    std::vector<uint32_t> used = ops;
-    release_dead(used, (int32_t)g);
-    if (last[id] < 0) continue;  // emitted but never consumed (cannot happen for roots)
-    if (slot[id] == NONE) slot[id] = smem_slots + take_spill();
-    uint32_t d = slot[id];
+    const uint32_t d = slot[id];
+    if (d == NONE) return;  // never read (cannot happen for scheduled values)
     if (v.kind == K_CONST) {
       put(PQW_B_CONST, d, (uint32_t)v.aux, 0);
     } else if (v.kind == K_VAR) {
@@ -1320,7 +1384,6 @@ CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* con
         case O_INV: put(PQW_B_INV, d, slot[v.a], 0); break;
         case O_HASH: put(PQW_B_HASH, d, slot[v.a], (uint32_t)v.aux); break;
         case O_SUMN: {
-          // acc bound tracking: values < 2^31, acc is 64-bit
           put(PQW_B_ACC_LD, 0, slot[B.pool[v.a]], 0);
           for (uint32_t i = 1; i < v.b; ++i) put(PQW_B_ACC_ADD, 0, slot[B.pool[v.a + i]], 0);
           put(PQW_B_ACC_ST, d, 0, 0);
@@ -1328,7 +1391,7 @@ CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* con
         }
         case O_DOT: {
           const uint32_t* L = &B.pool[v.a];
-          uint32_t npair = v.b / 2;
+          const uint32_t npair = v.b / 2;
           bool narrow = true;  // two-product forms pack two slots as 16-bit fields
           for (uint32_t i = 0; i < v.b; ++i) narrow &= slot[L[i]] < 0x10000u;
           if (narrow && npair >= 2) {
@@ -1361,22 +1424,65 @@ CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* con
           bad("internal: bad value op");
       }
     }
-    // a value nobody reads again (only possible for roots consumed in this
-    // same group) is released immediately
+  };
+  std::vector<std::vector<std::vector<uint32_t>>> plan_units(
+      NW, std::vector<std::vector<uint32_t>>(phases.size()));
+  for (size_t p = 0; p < phases.size(); ++p)
+    for (uint32_t g : phases[p]) plan_units[warp_of[g]][p].push_back(g);
+  for (uint32_t w = 0; w < NW; ++w) {
+    const uint32_t off = (uint32_t)code.size();
+    uint32_t* tab = reinterpret_cast<uint32_t*>(code.data());
+    tab[w] = off;  // pqw_ins is four u32: the table is NW u32 offsets
+    for (size_t p = 0; p < phases.size(); ++p) {
+      for (uint32_t g : plan_units[w][p]) emit_unit(g);
+      put(p + 1 < phases.size() ? PQW_B_BAR : PQW_B_END, 0, 0, 0);
+    }
+    if (phases.empty()) put(PQW_B_END, 0, 0, 0);
   }
-  put(PQW_B_END, 0, 0, 0);
   st.n_slots = n_spill ? smem_slots + n_spill : fast_used;
   st.n_fast_slots = fast_used;
+  st.n_phases = (uint32_t)phases.size();
   uint64_t ops_count = 0;
-  for (const auto& ins : code)
-    if (ins.op != PQW_B_END) ops_count++;
+  for (size_t i = table; i < code.size(); ++i)
+    if (code[i].op != PQW_B_END && code[i].op != PQW_B_BAR) ops_count++;
   st.field_ops = ops_count;
   return st;
 }
 
+// The streams of a cooperative program interleaved phase by phase (warp 0's
+// part of phase 0, warp 1's, ..., then phase 1): a sequential order with the
+// program's dataflow, used for backward slicing.
+static std::vector<pqw_ins> linearize(const CompiledStage& st) {
+  const auto& code = *st.code;
+  const uint32_t NW = st.n_warps;
+  const uint32_t* tab = reinterpret_cast<const uint32_t*>(code.data());
+  std::vector<size_t> pc(NW);
+  for (uint32_t w = 0; w < NW; ++w) pc[w] = tab[w];
+  std::vector<pqw_ins> out;
+  std::vector<bool> done(NW, false);
+  size_t live = NW;
+  while (live) {
+    for (uint32_t w = 0; w < NW; ++w) {
+      if (done[w]) continue;
+      for (;;) {
+        const pqw_ins& in = code[pc[w]++];
+        if (in.op == PQW_B_BAR) break;
+        if (in.op == PQW_B_END) {
+          done[w] = true;
+          live--;
+          break;
+        }
+        out.push_back(in);
+      }
+    }
+  }
+  out.push_back(pqw_ins{PQW_B_END, 0, 0, 0});
+  return out;
+}
+
 std::vector<uint32_t> obligation_support(const CompiledStage& st, uint32_t obl) {
   std::vector<uint32_t> vars;
-  const auto& code = *st.code;
+  const std::vector<pqw_ins> code = linearize(st);
   long pc = -1;
   for (long i = 0; i < (long)code.size(); ++i)
     if (code[i].op == PQW_B_CHK && code[i].dst == obl) {

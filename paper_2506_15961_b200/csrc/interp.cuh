@@ -1,19 +1,22 @@
 // interp.cuh -- the sm_100a bytecode interpreter (device code of witness_kernel.cu).
 //
-// Work decomposition: a work item is (stage, CTA tile). A CTA of WARPS warps
-// takes WARPS consecutive warp tiles of one stage; each warp evaluates the
-// stage program for WT = 32 * VW witnesses, lane l owning witnesses
-// [wtile*WT + VW*l, +VW) and moving them with one 128-bit access per slot
-// read/write. The slot file is per warp and witness-innermost (slot s = 32
-// Vec = 512 contiguous bytes): fast slots (s < smem_slots) live in shared
-// memory, spill slots in per-warp global scratch. The grid is persistent
-// (SMs x occupancy) and pulls items from an atomic counter; stages are ordered
-// by descending cost so the longest programs start first.
+// Cooperative execution. A work item is (stage, tile of 32 witnesses). The CTA
+// (NW warps) evaluates the stage for the tile's 32 witnesses -- one witness per
+// lane -- out of ONE value file shared by all its warps: slot s of the file is
+// 32 consecutive u32 (128 B, one conflict-free LDS/STS per warp access) in
+// shared memory for s < smem_slots, or in the CTA's global spill region. The
+// compiler split the stage program into NW instruction streams and into phases
+// (list scheduling in depth-first order, so the live set stays that of a
+// sequential evaluation): within a phase the warps' instructions are mutually
+// independent, a BAR ends the phase (named CTA barrier), so the warps of the
+// CTA supply the instruction-level parallelism that one witness lacks while
+// the whole live set of a stage -- up to ~1600 values -- stays on chip.
 //
-// The instruction stream is warp-uniform (every lane runs the same program)
-// and shared by the CTA's warps (L1 hits after the first warp): decode is one
-// broadcast 128-bit load, prefetched one instruction ahead, plus an indirect
-// branch that never diverges; its cost is amortized over VW witnesses per lane.
+// The grid is persistent (SMs x occupancy) and pulls items from an atomic
+// counter; stages are ordered by descending cost. Decode is a warp-uniform
+// broadcast 128-bit load (instruction streams are shared by all CTAs working
+// on the same program, so they live in L1/L2), prefetched one ahead, plus an
+// indirect branch that never diverges.
 #pragma once
 
 #include <stdint.h>
@@ -24,15 +27,9 @@
 namespace pqw {
 namespace {
 
-constexpr int VW = 4;
-constexpr int WARPS = 4;
-constexpr int BLOCK = 32 * WARPS;
-constexpr int WT = 32 * VW;          // witnesses per warp tile
-constexpr int TW = WT * WARPS;       // witnesses per CTA work item
-
-struct alignas(16) Vec {
-  uint32_t v[VW];
-};
+constexpr int NW = 8;               // warps per CTA (must equal the compile-time n_warps)
+constexpr int BLOCK = 32 * NW;
+constexpr int TW = 32;              // witnesses per work item (one per lane)
 
 struct StageDesc {
   uint32_t code_off;
@@ -48,15 +45,15 @@ struct Params {
   const uint64_t* var_keys;
   const uint64_t* fn_keys;   // 3 entries
   uint32_t* counter;         // work-item counter
-  Vec* scratch;              // per-warp spill slot files
+  uint32_t* scratch;         // per-CTA spill value files
   unsigned long long* first_bad;
   uint32_t* n_valid;
   uint32_t* n_bad;
   uint32_t n_items;
-  uint32_t tiles;            // CTA work items per stage
+  uint32_t tiles;            // work items per stage
   uint32_t n_witness;
-  uint32_t smem_slots;       // fast slots per warp (shared memory)
-  uint32_t overflow_slots;   // per-warp spill capacity in slots
+  uint32_t smem_slots;       // fast slots (shared memory)
+  uint32_t overflow_slots;   // per-CTA spill capacity in slots
   // probe mode
   uint32_t probe_w;
   uint32_t probe_obl;
@@ -64,226 +61,162 @@ struct Params {
   uint32_t* probe_vars;
 };
 
+__device__ __forceinline__ void cta_bar() { asm volatile("bar.sync 1, %0;" ::"r"(BLOCK) : "memory"); }
+
+// Runs this warp's stream of the stage program for witness w = tile*32 + lane,
+// folding the lane's definedness and first failing obligation into valid/bad.
 template <bool PROBE>
-__device__ __forceinline__ void run_item(const Params& p, Vec* wsm, Vec* wgs, uint32_t sdesc,
-                                         uint32_t wtile) {
-  const StageDesc sd = p.stages[sdesc];
+__device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd, uint32_t* sfile,
+                                           uint32_t* gfile, uint32_t w, bool& valid,
+                                           uint32_t& bad) {
   const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t w0 = PROBE ? p.probe_w : wtile * WT + lane * VW;
+  const uint32_t warp = threadIdx.x >> 5;
   const uint32_t nsm = p.smem_slots;
-
-  // warp-uniform branch between the shared-memory file and the spill file
-  auto ld = [&](uint32_t s) -> Vec {
-    if (s < nsm) return wsm[s * 32u + lane];
-    return wgs[(size_t)(s - nsm) * 32u + lane];
+  auto ld = [&](uint32_t s) -> uint32_t {
+    if (s < nsm) return sfile[s * 32u + lane];
+    return gfile[(size_t)(s - nsm) * 32u + lane];
   };
-  auto st = [&](uint32_t s, const Vec& v) {
+  auto st = [&](uint32_t s, uint32_t v) {
     if (s < nsm)
-      wsm[s * 32u + lane] = v;
+      sfile[s * 32u + lane] = v;
     else
-      wgs[(size_t)(s - nsm) * 32u + lane] = v;
+      gfile[(size_t)(s - nsm) * 32u + lane] = v;
   };
-
-  bool valid[VW];
-  uint32_t bad[VW];
-  uint64_t acc[VW];
-#pragma unroll
-  for (int j = 0; j < VW; ++j) {
-    valid[j] = PROBE ? (lane == 0 && j == 0) : (w0 + j) < p.n_witness;
-    bad[j] = 0xFFFFFFFFu;
-    acc[j] = 0;
-  }
-
-  const uint4* code = p.code + sd.code_off;
+  const uint4* base = p.code + sd.code_off;
+  const uint32_t off = __ldg(reinterpret_cast<const uint32_t*>(base) + warp);
+  const uint4* code = base + off;
+  uint64_t acc = 0;
   uint4 nxt = __ldg(code);
   for (uint32_t pc = 0;; ++pc) {
     const uint4 in = nxt;
-    nxt = __ldg(code + pc + 1);  // the image is padded with END: never past the end
-    Vec r;
+    nxt = __ldg(code + pc + 1);  // every stream ends with END and the image is padded
     switch (in.x) {
       case PQW_B_END:
-        goto done;
+        return;
+      case PQW_B_BAR:
+        cta_bar();
+        break;
       case PQW_B_CONST:
-#pragma unroll
-        for (int j = 0; j < VW; ++j) r.v[j] = in.z;
-        st(in.y, r);
+        st(in.y, in.z);
         break;
       case PQW_B_VAR: {
-        const uint64_t key = __ldg(p.var_keys + sd.var_base + in.z);
-#pragma unroll
-        for (int j = 0; j < VW; ++j) r.v[j] = witness_value(key, w0 + j);
-        if (PROBE && lane == 0) p.probe_vars[in.z] = r.v[0];
-        st(in.y, r);
+        const uint32_t v = witness_value(__ldg(p.var_keys + sd.var_base + in.z), w);
+        if (PROBE && w == p.probe_w) p.probe_vars[in.z] = v;
+        st(in.y, v);
         break;
       }
-      case PQW_B_ADD: {
-        const Vec a = ld(in.z), b = ld(in.w);
-#pragma unroll
-        for (int j = 0; j < VW; ++j) r.v[j] = fadd(a.v[j], b.v[j]);
-        st(in.y, r);
+      case PQW_B_ADD:
+        st(in.y, fadd(ld(in.z), ld(in.w)));
         break;
-      }
-      case PQW_B_SUB: {
-        const Vec a = ld(in.z), b = ld(in.w);
-#pragma unroll
-        for (int j = 0; j < VW; ++j) r.v[j] = fsub(a.v[j], b.v[j]);
-        st(in.y, r);
+      case PQW_B_SUB:
+        st(in.y, fsub(ld(in.z), ld(in.w)));
         break;
-      }
-      case PQW_B_MUL: {
-        const Vec a = ld(in.z), b = ld(in.w);
-#pragma unroll
-        for (int j = 0; j < VW; ++j) r.v[j] = fmul(a.v[j], b.v[j]);
-        st(in.y, r);
+      case PQW_B_MUL:
+        st(in.y, fmul(ld(in.z), ld(in.w)));
         break;
-      }
-      case PQW_B_NEG: {
-        const Vec a = ld(in.z);
-#pragma unroll
-        for (int j = 0; j < VW; ++j) r.v[j] = fneg(a.v[j]);
-        st(in.y, r);
+      case PQW_B_NEG:
+        st(in.y, fneg(ld(in.z)));
         break;
-      }
-      case PQW_B_DIV: {
-        const Vec a = ld(in.z), b = ld(in.w);
-#pragma unroll
-        for (int j = 0; j < VW; ++j) r.v[j] = fmul(a.v[j], finv(b.v[j]));
-        st(in.y, r);
+      case PQW_B_DIV:
+        st(in.y, fmul(ld(in.z), finv(ld(in.w))));
         break;
-      }
-      case PQW_B_INV: {
-        const Vec a = ld(in.z);
-#pragma unroll
-        for (int j = 0; j < VW; ++j) r.v[j] = finv(a.v[j]);
-        st(in.y, r);
+      case PQW_B_INV:
+        st(in.y, finv(ld(in.z)));
         break;
-      }
-      case PQW_B_HASH: {
-        const uint64_t key = __ldg(p.fn_keys + in.w);
-        const Vec a = ld(in.z);
-#pragma unroll
-        for (int j = 0; j < VW; ++j) r.v[j] = uf_apply(key, a.v[j]);
-        st(in.y, r);
+      case PQW_B_HASH:
+        st(in.y, uf_apply(__ldg(p.fn_keys + in.w), ld(in.z)));
         break;
-      }
-      case PQW_B_ACC_LD: {
-        const Vec a = ld(in.z);
-#pragma unroll
-        for (int j = 0; j < VW; ++j) acc[j] = a.v[j];
+      case PQW_B_ACC_LD:
+        acc = ld(in.z);
         break;
-      }
-      case PQW_B_ACC_ADD: {
-        const Vec a = ld(in.z);
-#pragma unroll
-        for (int j = 0; j < VW; ++j) acc[j] += a.v[j];
+      case PQW_B_ACC_ADD:
+        acc += ld(in.z);
         break;
-      }
-      case PQW_B_ACC_MUL: {
-        const Vec a = ld(in.z), b = ld(in.w);
-#pragma unroll
-        for (int j = 0; j < VW; ++j) acc[j] = (uint64_t)a.v[j] * b.v[j];
+      case PQW_B_ACC_MUL:
+        acc = (uint64_t)ld(in.z) * ld(in.w);
         break;
-      }
       case PQW_B_ACC_MACF:
-#pragma unroll
-        for (int j = 0; j < VW; ++j) acc[j] = ffold64(acc[j]);
+        acc = ffold64(acc);
         // fallthrough
-      case PQW_B_ACC_MAC: {
-        const Vec a = ld(in.z), b = ld(in.w);
-#pragma unroll
-        for (int j = 0; j < VW; ++j) acc[j] += (uint64_t)a.v[j] * b.v[j];
+      case PQW_B_ACC_MAC:
+        acc += (uint64_t)ld(in.z) * ld(in.w);
         break;
-      }
-      case PQW_B_ACC_MUL2: {  // acc = a*b + c*d  (two products < 2^63)
-        const Vec a = ld(in.z), b = ld(in.w), c = ld(in.y & 0xFFFFu), d = ld(in.y >> 16);
-#pragma unroll
-        for (int j = 0; j < VW; ++j)
-          acc[j] = (uint64_t)a.v[j] * b.v[j] + (uint64_t)c.v[j] * d.v[j];
+      case PQW_B_ACC_MUL2:  // acc = a*b + c*d  (< 2^63)
+        acc = (uint64_t)ld(in.z) * ld(in.w) + (uint64_t)ld(in.y & 0xFFFFu) * ld(in.y >> 16);
         break;
-      }
-      case PQW_B_ACC_MAC2: {  // acc = fold(acc) + a*b + c*d  (< 2^34 + 2^63)
-        const Vec a = ld(in.z), b = ld(in.w), c = ld(in.y & 0xFFFFu), d = ld(in.y >> 16);
-#pragma unroll
-        for (int j = 0; j < VW; ++j)
-          acc[j] = ffold64(acc[j]) + (uint64_t)a.v[j] * b.v[j] + (uint64_t)c.v[j] * d.v[j];
+      case PQW_B_ACC_MAC2:  // acc = fold(acc) + a*b + c*d  (< 2^34 + 2^63)
+        acc = ffold64(acc) + (uint64_t)ld(in.z) * ld(in.w) +
+              (uint64_t)ld(in.y & 0xFFFFu) * ld(in.y >> 16);
         break;
-      }
       case PQW_B_ACC_ST:
-#pragma unroll
-        for (int j = 0; j < VW; ++j) r.v[j] = fred64(acc[j]);
-        st(in.y, r);
+        st(in.y, fred64(acc));
         break;
       case PQW_B_CHK: {
-        const Vec a = ld(in.z), b = ld(in.w);
-        if (PROBE && in.y == p.probe_obl && lane == 0) {
-          p.probe_out[0] = a.v[0];
-          p.probe_out[1] = b.v[0];
+        const uint32_t a = ld(in.z), b = ld(in.w);
+        if (PROBE && in.y == p.probe_obl && w == p.probe_w) {
+          p.probe_out[0] = a;
+          p.probe_out[1] = b;
         }
-#pragma unroll
-        for (int j = 0; j < VW; ++j)
-          if (a.v[j] != b.v[j]) bad[j] = min(bad[j], in.y);
+        if (a != b) bad = min(bad, in.y);
         break;
       }
-      case PQW_B_DEN: {
-        const Vec a = ld(in.z);
-#pragma unroll
-        for (int j = 0; j < VW; ++j)
-          if (a.v[j] == 0) valid[j] = false;
+      case PQW_B_DEN:
+        if (ld(in.z) == 0) valid = false;
         break;
-      }
       default:
-        goto done;  // unreachable for a well-formed image
+        return;  // unreachable for a well-formed image
     }
-  }
-done:
-  if (PROBE) return;
-  unsigned long long best = ~0ull;
-  uint32_t nv = 0, nb = 0;
-#pragma unroll
-  for (int j = 0; j < VW; ++j) {
-    if (!valid[j]) continue;
-    nv++;
-    if (bad[j] != 0xFFFFFFFFu) {
-      nb++;
-      const unsigned long long k = ((unsigned long long)(w0 + j) << 32) | bad[j];
-      best = k < best ? k : best;
-    }
-  }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    nv += __shfl_down_sync(0xFFFFFFFFu, nv, off);
-    nb += __shfl_down_sync(0xFFFFFFFFu, nb, off);
-    const unsigned long long o = __shfl_down_sync(0xFFFFFFFFu, best, off);
-    best = o < best ? o : best;
-  }
-  if (lane == 0) {
-    if (nv) atomicAdd(p.n_valid + sd.result, nv);
-    if (nb) atomicAdd(p.n_bad + sd.result, nb);
-    if (best != ~0ull) atomicMin(p.first_bad + sd.result, best);
   }
 }
 
 template <bool PROBE>
 __global__ void __launch_bounds__(BLOCK) eval_kernel(Params p) {
-  extern __shared__ Vec smem[];
+  extern __shared__ uint32_t sfile[];
   __shared__ uint32_t s_item;
+  __shared__ uint32_t s_invalid;     // lanes with a vanished denominator (bitmask)
+  __shared__ uint32_t s_bad[32];     // first failing obligation per lane
+  const uint32_t lane = threadIdx.x & 31u;
   const uint32_t warp = threadIdx.x >> 5;
-  Vec* wsm = smem + (size_t)warp * p.smem_slots * 32;
-  Vec* wgs = p.scratch + ((size_t)blockIdx.x * WARPS + warp) * p.overflow_slots * 32;
-  if (PROBE) {
-    if (warp == 0) run_item<true>(p, wsm, wgs, p.work[0], 0);
-    return;
-  }
+  uint32_t* gfile = p.scratch + (size_t)blockIdx.x * p.overflow_slots * 32u;
   for (;;) {
-    if (threadIdx.x == 0) s_item = atomicAdd(p.counter, 1u);
+    if (threadIdx.x == 0) s_item = PROBE ? 0u : atomicAdd(p.counter, 1u);
+    if (threadIdx.x < 32) s_bad[threadIdx.x] = 0xFFFFFFFFu;
+    if (threadIdx.x == 0) s_invalid = 0;
     __syncthreads();
     const uint32_t item = s_item;
-    __syncthreads();
     if (item >= p.n_items) break;
-    const uint32_t tile = item % p.tiles;
-    const uint32_t wtile = tile * WARPS + warp;
-    // warps past the last witness skip the program entirely
-    if (wtile * WT < p.n_witness) run_item<false>(p, wsm, wgs, p.work[item / p.tiles], wtile);
+    const uint32_t stage = PROBE ? p.work[0] : p.work[item / p.tiles];
+    const uint32_t tile = PROBE ? p.probe_w / 32u : item % p.tiles;
+    const StageDesc sd = p.stages[stage];
+    const uint32_t w = tile * 32u + lane;
+    bool valid = PROBE ? (w == p.probe_w) : (w < p.n_witness);
+    uint32_t bad = 0xFFFFFFFFu;
+    run_stream<PROBE>(p, sd, sfile, gfile, w, valid, bad);
+    // merge the warps' verdicts for each lane
+    const uint32_t inval = __ballot_sync(0xFFFFFFFFu, !valid);
+    if (lane == 0 && inval) atomicOr(&s_invalid, inval);
+    if (bad != 0xFFFFFFFFu) atomicMin(&s_bad[lane], bad);
+    __syncthreads();
+    if (!PROBE && warp == 0) {
+      const bool ok = !((s_invalid >> lane) & 1u) && w < p.n_witness;
+      const uint32_t b = s_bad[lane];
+      uint32_t nv = ok, nb = ok && b != 0xFFFFFFFFu;
+      unsigned long long best = nb ? (((unsigned long long)w << 32) | b) : ~0ull;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        nv += __shfl_down_sync(0xFFFFFFFFu, nv, o);
+        nb += __shfl_down_sync(0xFFFFFFFFu, nb, o);
+        const unsigned long long t = __shfl_down_sync(0xFFFFFFFFu, best, o);
+        best = t < best ? t : best;
+      }
+      if (lane == 0) {
+        if (nv) atomicAdd(p.n_valid + sd.result, nv);
+        if (nb) atomicAdd(p.n_bad + sd.result, nb);
+        if (best != ~0ull) atomicMin(p.first_bad + sd.result, best);
+      }
+    }
+    __syncthreads();  // the value file and s_* are reused by the next item
+    if (PROBE) break;
   }
 }
 

@@ -58,7 +58,7 @@ struct pqw_engine {
   uint64_t* d_var_keys = nullptr;
   uint64_t* d_fn_keys = nullptr;
   uint32_t* d_counter = nullptr;
-  pqw::Vec* d_scratch = nullptr;
+  uint32_t* d_scratch = nullptr;
   unsigned long long* d_first_bad = nullptr;
   uint32_t* d_n_valid = nullptr;
   uint32_t* d_n_bad = nullptr;
@@ -131,7 +131,7 @@ int pqw_engine_create(int device, uint64_t seed, const uint64_t fn_keys[3], pqw_
   for (int i = 0; i < 3; ++i) e->fn_keys[i] = fn_keys[i];
   if (const char* fs = getenv("PQW_FAST_SLOTS")) {
     int v = atoi(fs);
-    if (v >= 1 && v <= 200) e->fast_slots = (uint32_t)v;
+    if (v >= 1 && v <= 1700) e->fast_slots = (uint32_t)v;
   }
   *out = e;
   return PQW_OK;
@@ -177,7 +177,7 @@ int pqw_stage_add(pqw_engine* e, const int32_t* ir, size_t ir_len, const int64_t
   if (!hit) {
     try {
       st = pqw::compile_stage(ir, ir_len, consts, n_consts, (uint32_t)n_vars, base, e->fn_keys,
-                              e->fast_slots);
+                              e->fast_slots, pqw::NW);
     } catch (const std::exception& ex) {
       return fail(PQW_EINVAL, std::string("stage compile: ") + ex.what());
     }
@@ -295,7 +295,7 @@ int pqw_upload(pqw_engine* e) {
   // the fast (shared-memory) slot file has the size the stages were compiled
   // for; spill slots live in per-warp global scratch
   const size_t slot_bytes = (size_t)pqw::TW * sizeof(uint32_t);  // one slot, all warps
-  if ((size_t)e->fast_slots * slot_bytes > prop.sharedMemPerBlockOptin - 1024)
+  if ((size_t)e->fast_slots * slot_bytes > prop.sharedMemPerBlockOptin - 2048)
     return fail(PQW_EINVAL, "fast slot file does not fit in shared memory");
   e->smem_slots = std::max<uint32_t>(e->fast_slots, 1);
   e->overflow_slots = e->max_slots > e->smem_slots ? e->max_slots - e->smem_slots : 0;

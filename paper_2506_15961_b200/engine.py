@@ -30,7 +30,7 @@ STAGE_BAD_INDEX = 5
 
 # bytecode opcodes (pqw_bop)
 BOP_NAMES = ("END", "CONST", "VAR", "ADD", "SUB", "MUL", "NEG", "DIV", "HASH", "ACC_MUL",
-             "ACC_MAC", "ACC_LD", "ACC_ADD", "ACC_ST", "CHK", "DEN", "ACC_MACF", "INV", "ACC_MUL2", "ACC_MAC2")
+             "ACC_MAC", "ACC_LD", "ACC_ADD", "ACC_ST", "CHK", "DEN", "ACC_MACF", "INV", "ACC_MUL2", "ACC_MAC2", "BAR")
 N_BOPS = len(BOP_NAMES)
 
 EXPORTS = ("pqw_abi_version", "pqw_last_error", "pqw_device_count", "pqw_engine_create",
