@@ -272,7 +272,7 @@ def main():
         r = e2.results()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
         st2 = e2.image_stats()
-        h2d = 16 * st2["instructions"] + 8 * sum(lw.var_keys.size for lw in lowered) + \
+        h2d = 16 * st2["unique_instructions"] + 8 * sum(lw.var_keys.size for lw in lowered) + \
             16 * st2["gpu_stages"]
         d2h = sum(a.nbytes for a in r)
         e2.close()
@@ -294,18 +294,10 @@ def main():
 
     if rank == 0:
         peaks = peak_fieldops(local)
-        hist = stats["op_hist"]
-        # field-op classes per witness (one bytecode instruction on one witness)
-        mul_cls = hist["MUL"] + hist["ACC_MUL"] + hist["ACC_MAC"] + hist["ACC_MACF"] + \
-            hist["ACC_ST"] + 2 * (hist["ACC_MUL2"] + hist["ACC_MAC2"])
-        add_cls = hist["ADD"] + hist["SUB"] + hist["NEG"] + hist["ACC_ADD"] + hist["ACC_LD"] + \
-            hist["CONST"] + hist["CHK"] + hist["DEN"]
-        div_cls = hist["DIV"] + hist["INV"]
-        hash_cls = hist["HASH"] + hist["VAR"]
-        # per launch (rank 0's image), W witnesses each; a DIV is 37 multiplies
-        ops_launch = (mul_cls + add_cls + hash_cls + 38 * div_cls) * W
-        t_peak = ((mul_cls + 38 * div_cls) / peaks["mul"] + add_cls / peaks["add"] +
-                  hash_cls / peaks["hash"]) * W
+        fo = stats["field_ops"]  # per witness, by class, over rank 0's GPU stages
+        ops_launch = sum(fo.values()) * W
+        t_peak = (fo["mul"] / peaks["mul"] + (fo["add"] + fo["cmp"]) / peaks["add"] +
+                  fo["hash"] / peaks["hash"] + fo["inv"] / peaks["inv"]) * W
         kern_s = eng_ms / 1e3 if eng_ms > 0 else total_ms / args.steps / 1e3
         achieved = ops_launch / kern_s
         peak = ops_launch / t_peak

@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define PQW_ABI_VERSION 1
+#define PQW_ABI_VERSION 2
 #define PQW_PRIME 2147483647u /* 2^31 - 1 */
 
 /* error codes */
@@ -65,23 +65,40 @@ enum pqw_top {
   PQW_T_ALL_REDUCE, PQW_T_ALL_GATHER, PQW_T_REDUCE_SCATTER, PQW_T_ALL_TO_ALL
 };
 
-/* scalar bytecode opcodes (what the GPU interprets; see pqw_stage_bytecode) */
+/*
+ * Stage-program opcodes (what the GPU interprets; see pqw_stage_bytecode and
+ * paper_2506_15961_b200/csrc/isa.hpp). A program is a table of per-warp stream
+ * offsets followed by one instruction stream per warp; an instruction is a
+ * header record {op | fn << 8 | k << 16, n, aux, 0} and payload records that
+ * list, 8 ops at a time, the u32 fields of n independent ops of one kind.
+ */
 enum pqw_bop {
-  PQW_B_END = 0, PQW_B_CONST, PQW_B_VAR, PQW_B_ADD, PQW_B_SUB, PQW_B_MUL, PQW_B_NEG,
-  PQW_B_DIV, PQW_B_HASH, PQW_B_ACC_MUL, PQW_B_ACC_MAC, PQW_B_ACC_LD, PQW_B_ACC_ADD,
-  PQW_B_ACC_ST, PQW_B_CHK, PQW_B_DEN, PQW_B_ACC_MACF, PQW_B_INV,
-  PQW_B_ACC_MUL2, /* acc = a*b + c*d; c, d packed as 16-bit slots in dst */
-  PQW_B_ACC_MAC2, /* acc = fold(acc) + a*b + c*d */
-  PQW_B_BAR,      /* phase boundary: CTA barrier (cooperative programs) */
+  PQW_B_END = 0,
+  PQW_B_DOT,    /* d = sum_j a_j * b_j over k pairs (k = 1: multiply)        */
+  PQW_B_SUM,    /* d = sum_j a_j over k terms (k = 2: add)                    */
+  PQW_B_SUB, PQW_B_NEG,
+  PQW_B_HASH,   /* d = f_fn(a): keyed hash standing in for EXP/RSQRT/SIGMOID */
+  PQW_B_INV,    /* d_i = a_i^-1, batched (one inversion per instruction)      */
+  PQW_B_VAR,    /* d = witness value of a stage variable                      */
+  PQW_B_CONST,
+  PQW_B_CHK,    /* obligation: lhs == rhs                                     */
+  PQW_B_DEN,    /* definedness: a != 0                                        */
+  PQW_B_FILL, PQW_B_SPILL, /* global spill slot <-> shared value file         */
+  PQW_B_WAIT,   /* wait for other warps' progress                             */
+  PQW_B_SIGNAL, /* publish this warp's progress                               */
   PQW_B_NUM_OPS
 };
 
+/* One 16-byte record of a stage program (header or payload). */
 typedef struct pqw_ins {
-  uint32_t op;  /* pqw_bop */
-  uint32_t dst; /* slot, or obligation id for CHK */
-  uint32_t a;   /* slot / residue / var index */
-  uint32_t b;   /* slot / function index */
+  uint32_t op;  /* header: op | fn << 8 | k << 16; payload: field word 0 */
+  uint32_t dst; /* header: n (ops in the bundle);   payload: field word 1 */
+  uint32_t a;   /* header: aux (SIGNAL value);      payload: field word 2 */
+  uint32_t b;   /* header: 0;                       payload: field word 3 */
 } pqw_ins;
+
+/* entries of pqw_image_stats */
+#define PQW_IMAGE_STATS_LEN (14 + PQW_B_NUM_OPS)
 
 typedef struct pqw_engine pqw_engine;
 
@@ -112,11 +129,12 @@ void pqw_engine_destroy(pqw_engine* e);
  * out_status[1] = info (obligation id for REFUTED_CONST / BAD_INDEX),
  * out_status[2] = obligation count, out_status[3] = obligations closed by value
  * numbering, out_status[4] = residual obligations, out_status[5] = bytecode
- * length, out_status[6] = slots, out_status[7] = max numerator degree of a
+ * length in records, out_status[6] = shared-memory slots, out_status[7] = max numerator degree of a
  * residual obligation (saturating), out_status[8..9] = lhs/rhs residues of the
  * REFUTED_CONST obligation, out_status[10..11] = their exact integer values
  * (INT64_MIN when not an exact integer), out_status[12] = field ops executed
- * per witness, out_status[13] = variables, out_status[14..15] reserved.
+ * per witness, out_status[13] = variables, out_status[14] = global spill
+ * slots, out_status[15] = instruction bundles.
  * Returns the stage index (>= 0) or a negative error.
  */
 int pqw_stage_add(pqw_engine* e, const int32_t* ir, size_t ir_len,
@@ -166,17 +184,22 @@ int pqw_probe(pqw_engine* e, int stage, uint32_t witness, uint32_t obl,
 /* Device time of the last launch in milliseconds (CUDA events on the launch stream). */
 int pqw_last_launch_ms(pqw_engine* e, float* ms);
 
-/* Totals of the uploaded image: out[0] = stages on the GPU, out[1] = bytecode
- * instructions, out[2] = max slots of a stage, out[3] = shared-memory slots, out[4 + op] = instructions of each pqw_bop (out has 4 + PQW_B_NUM_OPS
- * entries), out[4 + PQW_B_NUM_OPS] = instructions of the uploaded image after
- * sharing identical programs, out[5 + PQW_B_NUM_OPS] = compile-cache hits. */
+/* Totals over the compiled GPU stages (PQW_IMAGE_STATS_LEN entries):
+ * out[0] = stages on the GPU, out[1] = program records, out[2] = max shared
+ * slots of a stage, out[3] = shared slots of the uploaded value file,
+ * out[4 + op] = ops of each pqw_bop, out[4 + N] = records of the uploaded
+ * image after sharing identical programs, out[5 + N] = compile-cache hits,
+ * out[6 + N .. 10 + N] = field ops per witness by class (multiplies, adds,
+ * keyed hashes, inversions, compares), out[11 + N] = max global spill slots
+ * of a stage, out[12 + N] = bundles, out[13 + N] = cross-warp waits
+ * (N = PQW_B_NUM_OPS). */
 int pqw_image_stats(pqw_engine* e, uint64_t* out, size_t cap);
 
 /* Measured integer-pipe ceiling of this device: field ops per second of
  * register-resident, decode-free kernels: out[0] = F_p multiplies, out[1] =
- * F_p adds, out[2] = keyed-hash evaluations. The roofline denominator of the
- * interpreter (bench.py). */
-int pqw_peak_fieldops(int device, double out[3]);
+ * F_p adds, out[2] = keyed-hash evaluations, out[3] = inversions. The
+ * roofline denominator of the interpreter (bench.py). */
+int pqw_peak_fieldops(int device, double out[4]);
 
 #ifdef __cplusplus
 }

@@ -31,7 +31,6 @@ namespace {
 constexpr int32_t IR_MAGIC = 0x50515701;
 constexpr uint32_t NONE = 0xFFFFFFFFu;
 constexpr size_t CHUNK = 16;  // max operands of one n-ary sum / dot before chunking
-constexpr size_t UNITS_PER_WARP = 4;  // scheduling units per warp per phase
 
 enum VKind : uint8_t { K_CONST = 0, K_VAR = 1, K_OP = 2 };
 enum VOp : uint8_t { O_NONE = 0, O_ADD, O_SUB, O_MUL, O_NEG, O_DIV, O_HASH, O_SUMN, O_DOT, O_INV };
@@ -1095,7 +1094,7 @@ struct Emitter {
 CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* consts,
                             size_t n_consts, uint32_t n_vars, uint32_t var_base,
                             const uint64_t fn_keys[3], uint32_t smem_slots,
-                            uint32_t n_warps) {
+                            uint32_t n_warps, const SchedOptions& sched) {
   CompiledStage st;
   st.n_vars = n_vars;
   st.n_warps = n_warps;
@@ -1201,351 +1200,103 @@ CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* con
   }
   for (uint32_t d : B.dens) E.emit_value(d);
 
-  // ---- cooperative schedule --------------------------------------------------
-  // Units are emitter groups (a value, a check, a definedness test). A CTA of
-  // n_warps warps evaluates the stage for 32 witnesses (one per lane) out of a
-  // shared value file; the program is list-scheduled into phases separated by
-  // CTA barriers: a unit is ready once every unit it reads from ran in an
-  // earlier phase, ready units are taken in depth-first (obligation) order --
-  // the order that keeps the live set small -- up to UNITS_PER_WARP per warp,
-  // and spread over the warps by instruction count.
-  const size_t G = E.groups.size();
-  std::vector<uint32_t> ops;
-  std::vector<int32_t> unit_of(B.vals.size(), -1);  // value -> defining group
-  for (size_t g = 0; g < G; ++g)
-    if (E.groups[g].kind == 0) unit_of[E.groups[g].v] = (int32_t)g;
-  auto reads_of = [&](size_t g, std::vector<uint32_t>& out) {
-    const auto& gr = E.groups[g];
-    out.clear();
-    if (gr.kind == 0) {
-      E.operands(gr.v, out);
-    } else if (gr.kind == 1) {
-      out.push_back(gr.l);
-      out.push_back(gr.r);
-    } else {
-      out.push_back(gr.v);
-    }
-  };
-  auto cost_of = [&](size_t g) -> uint32_t {
-    const auto& gr = E.groups[g];
-    if (gr.kind != 0) return 1;
-    const Val& v = B.vals[gr.v];
-    if (v.kind == K_OP && v.op == O_SUMN) return v.b + 1;
-    if (v.kind == K_OP && v.op == O_DOT) return v.b / 4 + 2;
-    return 1;
-  };
-  std::vector<std::vector<uint32_t>> users(G);
-  std::vector<uint32_t> indeg(G, 0);
-  for (size_t g = 0; g < G; ++g) {
-    reads_of(g, ops);
-    std::sort(ops.begin(), ops.end());
-    ops.erase(std::unique(ops.begin(), ops.end()), ops.end());
-    for (uint32_t u : ops) {
-      int32_t d = unit_of[u];
-      if (d < 0) bad("internal: operand without a defining unit");
-      users[d].push_back((uint32_t)g);
-      indeg[g]++;
-    }
-  }
-  const uint32_t NW = n_warps;
-  const size_t CAP = (size_t)NW * UNITS_PER_WARP;
-  std::vector<int32_t> phase_of(G, -1), warp_of(G, -1);
-  std::vector<std::vector<uint32_t>> phases;
+  // ---- back end: DAG of scheduling units in depth-first priority order -------
+  auto dag = std::make_shared<Dag>();
   {
-    std::priority_queue<uint32_t, std::vector<uint32_t>, std::greater<uint32_t>> ready;
+    const size_t G = E.groups.size();
+    std::vector<int32_t> unit_of(B.vals.size(), -1);
     for (size_t g = 0; g < G; ++g)
-      if (indeg[g] == 0) ready.push((uint32_t)g);
-    std::vector<uint32_t> load(NW);
-    while (!ready.empty()) {
-      std::vector<uint32_t> batch;
-      while (!ready.empty() && batch.size() < CAP) {
-        batch.push_back(ready.top());
-        ready.pop();
-      }
-      const int32_t p = (int32_t)phases.size();
-      std::fill(load.begin(), load.end(), 0);
-      for (uint32_t g : batch) {
-        uint32_t w = (uint32_t)(std::min_element(load.begin(), load.end()) - load.begin());
-        load[w] += cost_of(g);
-        phase_of[g] = p;
-        warp_of[g] = (int32_t)w;
-      }
-      for (uint32_t g : batch)
-        for (uint32_t u : users[g])
-          if (--indeg[u] == 0) ready.push(u);
-      phases.push_back(std::move(batch));
-    }
-  }
-  for (size_t g = 0; g < G; ++g)
-    if (phase_of[g] < 0) bad("internal: unscheduled unit (cycle)");
-
-  // liveness on phases: a value written in phase d is readable from d+1 on and
-  // holds its slot through its last reading phase l; another value may take the
-  // slot only from a phase strictly after l (warps of one phase run unordered)
-  std::vector<int32_t> defp(B.vals.size(), -1), lastp(B.vals.size(), -1);
-  std::vector<uint32_t> uses(B.vals.size(), 0);
-  for (size_t g = 0; g < G; ++g) {
-    if (E.groups[g].kind == 0) defp[E.groups[g].v] = phase_of[g];
-    reads_of(g, ops);
-    for (uint32_t u : ops) {
-      lastp[u] = std::max(lastp[u], phase_of[g]);
-      uses[u]++;
-    }
-  }
-  std::vector<uint32_t> slot(B.vals.size(), NONE);
-  std::vector<uint32_t> cand;
-  for (size_t g = 0; g < G; ++g)
-    if (E.groups[g].kind == 0 && lastp[E.groups[g].v] >= 0) cand.push_back(E.groups[g].v);
-  // fast file: busiest values per phase of lifetime first, packed into slots
-  std::stable_sort(cand.begin(), cand.end(), [&](uint32_t a, uint32_t b) {
-    uint64_t sa = (uint64_t)(lastp[a] - defp[a] + 1), sb = (uint64_t)(lastp[b] - defp[b] + 1);
-    return (uint64_t)uses[a] * sb > (uint64_t)uses[b] * sa;
-  });
-  std::vector<std::map<int32_t, int32_t>> occ(smem_slots);  // closed intervals start -> end
-  uint32_t fast_used = 0;
-  // next-fit start hint: most slots are full early, scanning from a rotating
-  // origin keeps the packing near-linear
-  for (uint32_t v : cand) {
-    const int32_t s0 = defp[v], s1 = lastp[v];
-    for (uint32_t k = 0; k < smem_slots; ++k) {
-      auto& m = occ[k];
-      auto it = m.lower_bound(s0);
-      if (it != m.end() && it->first <= s1) continue;
-      if (it != m.begin() && std::prev(it)->second >= s0) continue;
-      m.emplace(s0, s1);
-      slot[v] = k;
-      fast_used = std::max(fast_used, k + 1);
-      break;
-    }
-  }
-  // spill file: linear scan over phases
-  std::vector<uint32_t> spill_vals;
-  for (uint32_t v : cand)
-    if (slot[v] == NONE) spill_vals.push_back(v);
-  std::sort(spill_vals.begin(), spill_vals.end(),
-            [&](uint32_t a, uint32_t b) { return defp[a] < defp[b]; });
-  uint32_t n_spill = 0;
-  {
-    // (release phase, slot) min-heap; a slot released after phase l serves defs > l
-    std::priority_queue<std::pair<int32_t, uint32_t>, std::vector<std::pair<int32_t, uint32_t>>,
-                        std::greater<std::pair<int32_t, uint32_t>>> busy;
-    std::priority_queue<uint32_t, std::vector<uint32_t>, std::greater<uint32_t>> free_s;
-    for (uint32_t v : spill_vals) {
-      while (!busy.empty() && busy.top().first < defp[v]) {
-        free_s.push(busy.top().second);
-        busy.pop();
-      }
-      uint32_t s;
-      if (!free_s.empty()) {
-        s = free_s.top();
-        free_s.pop();
+      if (E.groups[g].kind == 0) unit_of[E.groups[g].v] = (int32_t)g;
+    auto uof = [&](uint32_t v) -> uint32_t {
+      if (unit_of[v] < 0) bad("internal: operand without a defining unit");
+      return (uint32_t)unit_of[v];
+    };
+    std::vector<uint32_t> opnds;
+    dag->units.resize(G);
+    for (size_t g = 0; g < G; ++g) {
+      const auto& gr = E.groups[g];
+      DagUnit& d = dag->units[g];
+      d.arg0 = (uint32_t)dag->pool.size();
+      if (gr.kind == 1) {
+        d.op = I_CHK;
+        d.aux = gr.obl;
+        dag->pool.push_back(uof(gr.l));
+        dag->pool.push_back(uof(gr.r));
+      } else if (gr.kind == 2) {
+        d.op = I_DEN;
+        dag->pool.push_back(uof(gr.v));
       } else {
-        s = n_spill++;
+        const Val& v = B.vals[gr.v];
+        if (v.kind == K_CONST) {
+          d.op = I_CONST;
+          d.aux = (uint32_t)v.aux;
+        } else if (v.kind == K_VAR) {
+          d.op = I_VAR;
+          d.aux = v.a;  // stage-relative: the device adds the stage's var_base
+        } else {
+          E.operands(gr.v, opnds);
+          for (uint32_t o : opnds) dag->pool.push_back(uof(o));
+          switch (v.op) {
+            case O_ADD: d.op = I_SUM; d.k = 2; break;
+            case O_SUMN: d.op = I_SUM; d.k = v.b; break;
+            case O_MUL: d.op = I_DOT; d.k = 1; break;
+            case O_DOT: d.op = I_DOT; d.k = v.b / 2; break;
+            case O_SUB: d.op = I_SUB; break;
+            case O_NEG: d.op = I_NEG; break;
+            case O_HASH: d.op = I_HASH; d.fn = (uint32_t)v.aux; break;
+            case O_INV:
+              d.op = I_INV;
+              d.guarded = (B.vals[v.a].flags & F_DEN) != 0;  // batch only checked denominators
+              break;
+            default: bad("internal: bad value op");
+          }
+          if (d.k > MAX_K) bad("internal: n-ary op wider than MAX_K");
+        }
       }
-      slot[v] = smem_slots + s;
-      busy.push({lastp[v], s});
+      d.nargs = (uint32_t)dag->pool.size() - d.arg0;
     }
   }
-
-  // emission: a table of per-warp stream offsets, then one stream per warp;
-  // every stream has one BAR per phase boundary and ends with END
-  std::vector<pqw_ins>& code = *st.code;
-  const uint32_t table = (NW + 3) / 4;
-  code.assign(table, pqw_ins{PQW_B_END, 0, 0, 0});
-  std::vector<std::vector<uint32_t>> per_warp_phase(NW);
-  auto put = [&](uint32_t op, uint32_t dst, uint32_t a, uint32_t b) {
-    code.push_back(pqw_ins{op, dst, a, b});
-  };
-  auto emit_unit = [&](uint32_t g) {
-    const auto& gr = E.groups[g];
-    if (gr.kind == 1) {
-      put(PQW_B_CHK, gr.obl, slot[gr.l], slot[gr.r]);
-      return;
-    }
-    if (gr.kind == 2) {
-      put(PQW_B_DEN, 0, slot[gr.v], 0);
-      return;
-    }
-    const uint32_t id = gr.v;
-    const Val& v = B.vals[id];
-    const uint32_t d = slot[id];
-    if (d == NONE) return;  // never read (cannot happen for scheduled values)
-    if (v.kind == K_CONST) {
-      put(PQW_B_CONST, d, (uint32_t)v.aux, 0);
-    } else if (v.kind == K_VAR) {
-      put(PQW_B_VAR, d, v.a, 0);  // stage-relative: the device adds the stage's var_base
-    } else {
-      switch (v.op) {
-        case O_ADD: put(PQW_B_ADD, d, slot[v.a], slot[v.b]); break;
-        case O_SUB: put(PQW_B_SUB, d, slot[v.a], slot[v.b]); break;
-        case O_MUL: put(PQW_B_MUL, d, slot[v.a], slot[v.b]); break;
-        case O_NEG: put(PQW_B_NEG, d, slot[v.a], 0); break;
-        case O_DIV: put(PQW_B_DIV, d, slot[v.a], slot[v.b]); break;
-        case O_INV: put(PQW_B_INV, d, slot[v.a], 0); break;
-        case O_HASH: put(PQW_B_HASH, d, slot[v.a], (uint32_t)v.aux); break;
-        case O_SUMN: {
-          put(PQW_B_ACC_LD, 0, slot[B.pool[v.a]], 0);
-          for (uint32_t i = 1; i < v.b; ++i) put(PQW_B_ACC_ADD, 0, slot[B.pool[v.a + i]], 0);
-          put(PQW_B_ACC_ST, d, 0, 0);
-          break;
-        }
-        case O_DOT: {
-          const uint32_t* L = &B.pool[v.a];
-          const uint32_t npair = v.b / 2;
-          bool narrow = true;  // two-product forms pack two slots as 16-bit fields
-          for (uint32_t i = 0; i < v.b; ++i) narrow &= slot[L[i]] < 0x10000u;
-          if (narrow && npair >= 2) {
-            auto pack = [&](uint32_t i) { return slot[L[2 * i]] | (slot[L[2 * i + 1]] << 16); };
-            // acc = p0 + p1 (< 2^63); then fold + two products per step (< 2^34 + 2^63)
-            put(PQW_B_ACC_MUL2, pack(1), slot[L[0]], slot[L[1]]);
-            uint32_t i = 2;
-            for (; i + 1 < npair; i += 2)
-              put(PQW_B_ACC_MAC2, pack(i + 1), slot[L[2 * i]], slot[L[2 * i + 1]]);
-            if (i < npair) put(PQW_B_ACC_MACF, 0, slot[L[2 * i]], slot[L[2 * i + 1]]);
-            put(PQW_B_ACC_ST, d, 0, 0);
-            break;
-          }
-          put(PQW_B_ACC_MUL, 0, slot[L[0]], slot[L[1]]);
-          // products < 2^62: three fit below 2^64; fold (to < 2^34) before a 4th
-          uint32_t since_fold = 1;
-          for (uint32_t i = 1; i < npair; ++i) {
-            if (since_fold == 3) {
-              put(PQW_B_ACC_MACF, 0, slot[L[2 * i]], slot[L[2 * i + 1]]);
-              since_fold = 1;
-            } else {
-              put(PQW_B_ACC_MAC, 0, slot[L[2 * i]], slot[L[2 * i + 1]]);
-              since_fold++;
-            }
-          }
-          put(PQW_B_ACC_ST, d, 0, 0);
-          break;
-        }
-        default:
-          bad("internal: bad value op");
-      }
-    }
-  };
-  std::vector<std::vector<std::vector<uint32_t>>> plan_units(
-      NW, std::vector<std::vector<uint32_t>>(phases.size()));
-  for (size_t p = 0; p < phases.size(); ++p)
-    for (uint32_t g : phases[p]) plan_units[warp_of[g]][p].push_back(g);
-  for (uint32_t w = 0; w < NW; ++w) {
-    const uint32_t off = (uint32_t)code.size();
-    uint32_t* tab = reinterpret_cast<uint32_t*>(code.data());
-    tab[w] = off;  // pqw_ins is four u32: the table is NW u32 offsets
-    for (size_t p = 0; p < phases.size(); ++p) {
-      for (uint32_t g : plan_units[w][p]) emit_unit(g);
-      put(p + 1 < phases.size() ? PQW_B_BAR : PQW_B_END, 0, 0, 0);
-    }
-    if (phases.empty()) put(PQW_B_END, 0, 0, 0);
-  }
-  st.n_slots = n_spill ? smem_slots + n_spill : fast_used;
-  st.n_fast_slots = fast_used;
-  st.n_phases = (uint32_t)phases.size();
-  uint64_t ops_count = 0;
-  for (size_t i = table; i < code.size(); ++i)
-    if (code[i].op != PQW_B_END && code[i].op != PQW_B_BAR) ops_count++;
-  st.field_ops = ops_count;
+  SchedOptions so = sched;
+  so.n_warps = n_warps;
+  so.smem_slots = smem_slots;
+  Program prog = schedule_program(*dag, so);
+  *st.code = std::move(prog.code);
+  st.n_slots = prog.n_slots;
+  st.n_spill = prog.n_spill;
+  st.n_spilled_values = prog.n_spilled_values;
+  st.n_bundles = prog.n_bundles;
+  st.n_waits = prog.n_waits;
+  st.makespan = prog.makespan;
+  for (int i = 0; i < 5; ++i) st.cls[i] = prog.cls[i];
+  for (int i = 0; i < (int)I_NUM_OPS; ++i) st.op_hist[i] = prog.op_hist[i];
+  st.field_ops = prog.cls[0] + prog.cls[1] + prog.cls[2] + prog.cls[3] + prog.cls[4];
+  st.dag = std::move(dag);
   return st;
-}
-
-// The streams of a cooperative program interleaved phase by phase (warp 0's
-// part of phase 0, warp 1's, ..., then phase 1): a sequential order with the
-// program's dataflow, used for backward slicing.
-static std::vector<pqw_ins> linearize(const CompiledStage& st) {
-  const auto& code = *st.code;
-  const uint32_t NW = st.n_warps;
-  const uint32_t* tab = reinterpret_cast<const uint32_t*>(code.data());
-  std::vector<size_t> pc(NW);
-  for (uint32_t w = 0; w < NW; ++w) pc[w] = tab[w];
-  std::vector<pqw_ins> out;
-  std::vector<bool> done(NW, false);
-  size_t live = NW;
-  while (live) {
-    for (uint32_t w = 0; w < NW; ++w) {
-      if (done[w]) continue;
-      for (;;) {
-        const pqw_ins& in = code[pc[w]++];
-        if (in.op == PQW_B_BAR) break;
-        if (in.op == PQW_B_END) {
-          done[w] = true;
-          live--;
-          break;
-        }
-        out.push_back(in);
-      }
-    }
-  }
-  out.push_back(pqw_ins{PQW_B_END, 0, 0, 0});
-  return out;
 }
 
 std::vector<uint32_t> obligation_support(const CompiledStage& st, uint32_t obl) {
   std::vector<uint32_t> vars;
-  const std::vector<pqw_ins> code = linearize(st);
-  long pc = -1;
-  for (long i = 0; i < (long)code.size(); ++i)
-    if (code[i].op == PQW_B_CHK && code[i].dst == obl) {
-      pc = i;
+  if (!st.dag) return vars;
+  const Dag& d = *st.dag;
+  std::vector<uint8_t> seen(d.units.size(), 0);
+  std::vector<uint32_t> stack;
+  for (uint32_t u = 0; u < d.units.size(); ++u)
+    if (d.units[u].op == I_CHK && d.units[u].aux == obl) {
+      stack.push_back(u);
+      seen[u] = 1;
       break;
     }
-  if (pc < 0) return vars;
-  std::unordered_set<uint32_t> need{code[pc].a, code[pc].b};
-  bool acc_needed = false;
-  for (long i = pc - 1; i >= 0; --i) {
-    const pqw_ins& in = code[i];
-    switch (in.op) {
-      case PQW_B_CHK:
-      case PQW_B_DEN:
-      case PQW_B_END:
-        break;
-      case PQW_B_ACC_ST:
-        if (need.erase(in.dst)) acc_needed = true;
-        break;
-      case PQW_B_ACC_MUL:
-      case PQW_B_ACC_MAC:
-      case PQW_B_ACC_MACF:
-        if (acc_needed) {
-          need.insert(in.a);
-          need.insert(in.b);
-          if (in.op == PQW_B_ACC_MUL) acc_needed = false;
-        }
-        break;
-      case PQW_B_ACC_ADD:
-        if (acc_needed) need.insert(in.a);
-        break;
-      case PQW_B_ACC_MUL2:
-      case PQW_B_ACC_MAC2:
-        if (acc_needed) {
-          need.insert(in.a);
-          need.insert(in.b);
-          need.insert(in.dst & 0xFFFFu);
-          need.insert(in.dst >> 16);
-          if (in.op == PQW_B_ACC_MUL2) acc_needed = false;
-        }
-        break;
-      case PQW_B_ACC_LD:
-        if (acc_needed) {
-          need.insert(in.a);
-          acc_needed = false;
-        }
-        break;
-      case PQW_B_VAR:
-        if (need.erase(in.dst)) vars.push_back(in.a);
-        break;
-      case PQW_B_CONST:
-        need.erase(in.dst);
-        break;
-      case PQW_B_NEG:
-      case PQW_B_HASH:
-      case PQW_B_INV:
-        if (need.erase(in.dst)) need.insert(in.a);
-        break;
-      default:  // binary
-        if (need.erase(in.dst)) {
-          need.insert(in.a);
-          need.insert(in.b);
-        }
+  while (!stack.empty()) {
+    const uint32_t u = stack.back();
+    stack.pop_back();
+    const DagUnit& x = d.units[u];
+    if (x.op == I_VAR) vars.push_back(x.aux);
+    for (uint32_t i = 0; i < x.nargs; ++i) {
+      const uint32_t p = d.pool[x.arg0 + i];
+      if (!seen[p]) {
+        seen[p] = 1;
+        stack.push_back(p);
+      }
     }
   }
   std::sort(vars.begin(), vars.end());

@@ -1,35 +1,39 @@
-// interp.cuh -- the sm_100a bytecode interpreter (device code of witness_kernel.cu).
+// interp.cuh -- the sm_100a stage interpreter (device code of witness_kernel.cu).
 //
-// Cooperative execution. A work item is (stage, tile of 32 witnesses). The CTA
-// (NW warps) evaluates the stage for the tile's 32 witnesses -- one witness per
-// lane -- out of ONE value file shared by all its warps: slot s of the file is
-// 32 consecutive u32 (128 B, one conflict-free LDS/STS per warp access) in
-// shared memory for s < smem_slots, or in the CTA's global spill region. The
-// compiler split the stage program into NW instruction streams and into phases
-// (list scheduling in depth-first order, so the live set stays that of a
-// sequential evaluation): within a phase the warps' instructions are mutually
-// independent, a BAR ends the phase (named CTA barrier), so the warps of the
-// CTA supply the instruction-level parallelism that one witness lacks while
-// the whole live set of a stage -- up to ~1600 values -- stays on chip.
+// Execution model. A work item is (stage, tile of 32 witnesses). The CTA's NW
+// warps evaluate the stage for the tile's witnesses -- one witness per lane --
+// out of ONE value file in shared memory: slot s is 32 consecutive u32 (128 B,
+// one conflict-free LDS/STS per warp access). The host back end
+// (schedule.cpp) list-scheduled the stage's DAG over the NW warps into
+// bundles of independent same-kind ops (isa.hpp) and made cross-warp
+// dependences explicit: a warp that reads a value another warp produced, or
+// overwrites a slot another warp still reads, first WAITs for that warp's
+// progress counter; producers SIGNAL after the bundles someone waits on. Every
+// wait targets a bundle that started earlier in the schedule, so the program is
+// deadlock-free, and no CTA-wide barrier is needed inside a stage.
 //
-// The grid is persistent (SMs x occupancy) and pulls items from an atomic
-// counter; stages are ordered by descending cost. Decode is a warp-uniform
-// broadcast 128-bit load (instruction streams are shared by all CTAs working
-// on the same program, so they live in L1/L2), prefetched one ahead, plus an
-// indirect branch that never diverges.
+// Decode is warp-uniform 128-bit loads of the shared instruction streams
+// (L1/L2-resident: all CTAs on one stage read the same code) and one indirect
+// branch per bundle; a bundle of n ops runs its payload group by group, 8 ops
+// at a time, all operand loads of a group issued before its arithmetic. Shared
+// addresses are 32-bit byte offsets prepared by the compiler (slot * 128), so an
+// operand costs one IADD + one LDS.
+//
+// The grid is persistent (one CTA per SM) and pulls items from an atomic
+// counter; stages are ordered by descending cost.
 #pragma once
 
 #include <stdint.h>
 
 #include "../../include/planeq_witness.h"
 #include "field.hpp"
+#include "isa.hpp"
 
 namespace pqw {
 namespace {
 
-constexpr int NW = 8;               // warps per CTA (must equal the compile-time n_warps)
-constexpr int BLOCK = 32 * NW;
-constexpr int TW = 32;              // witnesses per work item (one per lane)
+constexpr int TW = 32;  // witnesses per work item (one per lane)
+constexpr int MAX_NW = 32;
 
 struct StageDesc {
   uint32_t code_off;
@@ -45,15 +49,14 @@ struct Params {
   const uint64_t* var_keys;
   const uint64_t* fn_keys;   // 3 entries
   uint32_t* counter;         // work-item counter
-  uint32_t* scratch;         // per-CTA spill value files
+  uint32_t* scratch;         // per-CTA spill regions
   unsigned long long* first_bad;
   uint32_t* n_valid;
   uint32_t* n_bad;
   uint32_t n_items;
   uint32_t tiles;            // work items per stage
   uint32_t n_witness;
-  uint32_t smem_slots;       // fast slots (shared memory)
-  uint32_t overflow_slots;   // per-CTA spill capacity in slots
+  uint32_t spill_slots;      // per-CTA spill capacity in slots
   // probe mode
   uint32_t probe_w;
   uint32_t probe_obl;
@@ -61,126 +64,322 @@ struct Params {
   uint32_t* probe_vars;
 };
 
-__device__ __forceinline__ void cta_bar() { asm volatile("bar.sync 1, %0;" ::"r"(BLOCK) : "memory"); }
+struct F8 {
+  uint32_t v[8];
+};
+
+__device__ __forceinline__ F8 ld8(const uint4* q) {
+  const uint4 a = __ldg(q), b = __ldg(q + 1);
+  return F8{{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}};
+}
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared.u32 %0, [%1];"
+               : "=r"(v)
+               : "r"((uint32_t)__cvta_generic_to_shared(p))
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)),
+               "r"(v)
+               : "memory");
+}
+
+__device__ __forceinline__ uint32_t lds(const uint8_t* sl, uint32_t off) {
+  return *reinterpret_cast<const uint32_t*>(sl + off);
+}
+__device__ __forceinline__ void sts(uint8_t* sl, uint32_t off, uint32_t v) {
+  *reinterpret_cast<uint32_t*>(sl + off) = v;
+}
+
+// acc (< 2^64) -> [0, P)
+__device__ __forceinline__ uint32_t red64(uint64_t x) { return fred64(x); }
 
 // Runs this warp's stream of the stage program for witness w = tile*32 + lane,
 // folding the lane's definedness and first failing obligation into valid/bad.
 template <bool PROBE>
-__device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd, uint32_t* sfile,
-                                           uint32_t* gfile, uint32_t w, bool& valid,
-                                           uint32_t& bad) {
+__device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd, uint8_t* sl,
+                                           uint8_t* gl, uint32_t* prog, uint32_t w,
+                                           bool& valid, uint32_t& bad) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t warp = threadIdx.x >> 5;
-  const uint32_t nsm = p.smem_slots;
-  auto ld = [&](uint32_t s) -> uint32_t {
-    if (s < nsm) return sfile[s * 32u + lane];
-    return gfile[(size_t)(s - nsm) * 32u + lane];
-  };
-  auto st = [&](uint32_t s, uint32_t v) {
-    if (s < nsm)
-      sfile[s * 32u + lane] = v;
-    else
-      gfile[(size_t)(s - nsm) * 32u + lane] = v;
-  };
-  const uint4* base = p.code + sd.code_off;
-  const uint32_t off = __ldg(reinterpret_cast<const uint32_t*>(base) + warp);
-  const uint4* code = base + off;
-  uint64_t acc = 0;
-  uint4 nxt = __ldg(code);
-  for (uint32_t pc = 0;; ++pc) {
-    const uint4 in = nxt;
-    nxt = __ldg(code + pc + 1);  // every stream ends with END and the image is padded
-    switch (in.x) {
-      case PQW_B_END:
+  const uint4* code = p.code + sd.code_off;
+  const uint4* pc = code + __ldg(reinterpret_cast<const uint32_t*>(code) + warp);
+  const uint64_t* vkeys = p.var_keys + sd.var_base;
+  for (;;) {
+    const uint4 h = __ldg(pc);
+    ++pc;
+    const uint32_t op = h.x & 0xFFu;
+    const uint32_t n = h.y;
+    switch (op) {
+      case I_END:
         return;
-      case PQW_B_BAR:
-        cta_bar();
-        break;
-      case PQW_B_CONST:
-        st(in.y, in.z);
-        break;
-      case PQW_B_VAR: {
-        const uint32_t v = witness_value(__ldg(p.var_keys + sd.var_base + in.z), w);
-        if (PROBE && w == p.probe_w) p.probe_vars[in.z] = v;
-        st(in.y, v);
-        break;
-      }
-      case PQW_B_ADD:
-        st(in.y, fadd(ld(in.z), ld(in.w)));
-        break;
-      case PQW_B_SUB:
-        st(in.y, fsub(ld(in.z), ld(in.w)));
-        break;
-      case PQW_B_MUL:
-        st(in.y, fmul(ld(in.z), ld(in.w)));
-        break;
-      case PQW_B_NEG:
-        st(in.y, fneg(ld(in.z)));
-        break;
-      case PQW_B_DIV:
-        st(in.y, fmul(ld(in.z), finv(ld(in.w))));
-        break;
-      case PQW_B_INV:
-        st(in.y, finv(ld(in.z)));
-        break;
-      case PQW_B_HASH:
-        st(in.y, uf_apply(__ldg(p.fn_keys + in.w), ld(in.z)));
-        break;
-      case PQW_B_ACC_LD:
-        acc = ld(in.z);
-        break;
-      case PQW_B_ACC_ADD:
-        acc += ld(in.z);
-        break;
-      case PQW_B_ACC_MUL:
-        acc = (uint64_t)ld(in.z) * ld(in.w);
-        break;
-      case PQW_B_ACC_MACF:
-        acc = ffold64(acc);
-        // fallthrough
-      case PQW_B_ACC_MAC:
-        acc += (uint64_t)ld(in.z) * ld(in.w);
-        break;
-      case PQW_B_ACC_MUL2:  // acc = a*b + c*d  (< 2^63)
-        acc = (uint64_t)ld(in.z) * ld(in.w) + (uint64_t)ld(in.y & 0xFFFFu) * ld(in.y >> 16);
-        break;
-      case PQW_B_ACC_MAC2:  // acc = fold(acc) + a*b + c*d  (< 2^34 + 2^63)
-        acc = ffold64(acc) + (uint64_t)ld(in.z) * ld(in.w) +
-              (uint64_t)ld(in.y & 0xFFFFu) * ld(in.y >> 16);
-        break;
-      case PQW_B_ACC_ST:
-        st(in.y, fred64(acc));
-        break;
-      case PQW_B_CHK: {
-        const uint32_t a = ld(in.z), b = ld(in.w);
-        if (PROBE && in.y == p.probe_obl && w == p.probe_w) {
-          p.probe_out[0] = a;
-          p.probe_out[1] = b;
+      case I_DOT: {
+        const uint32_t k = h.x >> 16;
+        if (k == 1) {
+          for (uint32_t g = 0; g < n; g += 8, pc += 6) {
+            const F8 D = ld8(pc), A = ld8(pc + 2), B = ld8(pc + 4);
+            uint32_t a[8], b[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (g + i < n) {
+                a[i] = lds(sl, A.v[i]);
+                b[i] = lds(sl, B.v[i]);
+              }
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (g + i < n) sts(sl, D.v[i], fmul(a[i], b[i]));
+          }
+        } else {
+          for (uint32_t g = 0; g < n; g += 8) {
+            const F8 D = ld8(pc);
+            pc += 2;
+            uint64_t acc[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] = 0;
+            for (uint32_t j = 0; j < k; ++j, pc += 4) {
+              const F8 A = ld8(pc), B = ld8(pc + 2);
+              uint32_t a[8], b[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                if (g + i < n) {
+                  a[i] = lds(sl, A.v[i]);
+                  b[i] = lds(sl, B.v[i]);
+                }
+              // products < 2^62: fold (to < 2^34) before every third one
+              const bool fold = (j % 3u) == 2u;
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                if (g + i < n) {
+                  uint64_t t = fold ? ffold64(acc[i]) : acc[i];
+                  acc[i] = t + (uint64_t)a[i] * b[i];
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (g + i < n) sts(sl, D.v[i], red64(acc[i]));
+          }
         }
-        if (a != b) bad = min(bad, in.y);
         break;
       }
-      case PQW_B_DEN:
-        if (ld(in.z) == 0) valid = false;
+      case I_SUM: {
+        const uint32_t k = h.x >> 16;
+        if (k == 2) {
+          for (uint32_t g = 0; g < n; g += 8, pc += 6) {
+            const F8 D = ld8(pc), A = ld8(pc + 2), B = ld8(pc + 4);
+            uint32_t a[8], b[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (g + i < n) {
+                a[i] = lds(sl, A.v[i]);
+                b[i] = lds(sl, B.v[i]);
+              }
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (g + i < n) sts(sl, D.v[i], fadd(a[i], b[i]));
+          }
+        } else {
+          for (uint32_t g = 0; g < n; g += 8) {
+            const F8 D = ld8(pc);
+            pc += 2;
+            uint64_t acc[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] = 0;
+            for (uint32_t j = 0; j < k; ++j, pc += 2) {
+              const F8 A = ld8(pc);
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                if (g + i < n) acc[i] += lds(sl, A.v[i]);
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (g + i < n) sts(sl, D.v[i], red64(acc[i]));
+          }
+        }
         break;
+      }
+      case I_SUB:
+        for (uint32_t g = 0; g < n; g += 8, pc += 6) {
+          const F8 D = ld8(pc), A = ld8(pc + 2), B = ld8(pc + 4);
+          uint32_t a[8], b[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (g + i < n) {
+              a[i] = lds(sl, A.v[i]);
+              b[i] = lds(sl, B.v[i]);
+            }
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (g + i < n) sts(sl, D.v[i], fsub(a[i], b[i]));
+        }
+        break;
+      case I_NEG:
+        for (uint32_t g = 0; g < n; g += 8, pc += 4) {
+          const F8 D = ld8(pc), A = ld8(pc + 2);
+          uint32_t a[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (g + i < n) a[i] = lds(sl, A.v[i]);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (g + i < n) sts(sl, D.v[i], fneg(a[i]));
+        }
+        break;
+      case I_HASH: {
+        const uint64_t key = __ldg(p.fn_keys + ((h.x >> 8) & 0xFFu));
+        for (uint32_t g = 0; g < n; g += 8, pc += 4) {
+          const F8 D = ld8(pc), A = ld8(pc + 2);
+          uint32_t a[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (g + i < n) a[i] = lds(sl, A.v[i]);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (g + i < n) sts(sl, D.v[i], uf_apply(key, a[i]));
+        }
+        break;
+      }
+      case I_INV: {
+        // Montgomery batch inversion over the bundle: prefix products go to the
+        // destination slots, one inversion, then a backward sweep. Every operand
+        // is a guarded denominator (a DEN of the same stage), so a witness where
+        // one vanishes is invalid and its garbage never counts.
+        const uint4* base = pc;
+        const uint32_t ng = (n + 7u) / 8u;
+        uint32_t acc = 1;
+        for (uint32_t g = 0; g < n; g += 8, pc += 4) {
+          const F8 D = ld8(pc), A = ld8(pc + 2);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (g + i < n) {
+              acc = fmul(acc, lds(sl, A.v[i]));
+              sts(sl, D.v[i], acc);
+            }
+        }
+        uint32_t inv = finv(acc);
+        for (int32_t gi = (int32_t)ng - 1; gi >= 0; --gi) {
+          const uint32_t g = (uint32_t)gi * 8u;
+          const F8 D = ld8(base + 4 * gi), A = ld8(base + 4 * gi + 2);
+          const F8 Dp = gi > 0 ? ld8(base + 4 * (gi - 1)) : D;
+#pragma unroll
+          for (int i = 7; i >= 0; --i)
+            if (g + i < n) {
+              if (g + i == 0) {
+                sts(sl, D.v[i], inv);
+              } else {
+                const uint32_t prev = lds(sl, i > 0 ? D.v[i > 0 ? i - 1 : 0] : Dp.v[7]);  // prefix m-1
+                const uint32_t a = lds(sl, A.v[i]);
+                sts(sl, D.v[i], fmul(inv, prev));
+                inv = fmul(inv, a);
+              }
+            }
+        }
+        break;
+      }
+      case I_VAR:
+        for (uint32_t g = 0; g < n; g += 8, pc += 4) {
+          const F8 D = ld8(pc), V = ld8(pc + 2);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (g + i < n) {
+              const uint32_t v = witness_value(__ldg(vkeys + V.v[i]), w);
+              if (PROBE && w == p.probe_w) p.probe_vars[V.v[i]] = v;
+              sts(sl, D.v[i], v);
+            }
+        }
+        break;
+      case I_CONST:
+        for (uint32_t g = 0; g < n; g += 8, pc += 4) {
+          const F8 D = ld8(pc), C = ld8(pc + 2);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (g + i < n) sts(sl, D.v[i], C.v[i]);
+        }
+        break;
+      case I_CHK:
+        for (uint32_t g = 0; g < n; g += 8, pc += 6) {
+          const F8 O = ld8(pc), A = ld8(pc + 2), B = ld8(pc + 4);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (g + i < n) {
+              const uint32_t a = lds(sl, A.v[i]), b = lds(sl, B.v[i]);
+              if (PROBE && O.v[i] == p.probe_obl && w == p.probe_w) {
+                p.probe_out[0] = a;
+                p.probe_out[1] = b;
+              }
+              if (a != b) bad = min(bad, O.v[i]);
+            }
+        }
+        break;
+      case I_DEN:
+        for (uint32_t g = 0; g < n; g += 8, pc += 2) {
+          const F8 A = ld8(pc);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (g + i < n && lds(sl, A.v[i]) == 0) valid = false;
+        }
+        break;
+      case I_FILL:
+        for (uint32_t g = 0; g < n; g += 8, pc += 4) {
+          const F8 D = ld8(pc), G = ld8(pc + 2);
+          uint32_t a[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (g + i < n) a[i] = *reinterpret_cast<const uint32_t*>(gl + G.v[i]);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (g + i < n) sts(sl, D.v[i], a[i]);
+        }
+        break;
+      case I_SPILL:
+        for (uint32_t g = 0; g < n; g += 8, pc += 4) {
+          const F8 G = ld8(pc), A = ld8(pc + 2);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (g + i < n) *reinterpret_cast<uint32_t*>(gl + G.v[i]) = lds(sl, A.v[i]);
+        }
+        break;
+      case I_WAIT: {
+        // header: z = producer warp, w = progress it must have published
+        const uint32_t* flag = prog + h.z;
+        if (ld_acquire(flag) < h.w) {
+          do {
+            __nanosleep(32);
+          } while (ld_acquire(flag) < h.w);
+        }
+        break;
+      }
       default:
-        return;  // unreachable for a well-formed image
+        __builtin_unreachable();
+    }
+    // header.w of a bundle: progress to publish once it is done (0: none). The
+    // warp's lanes are ordered by __syncwarp, lane 0's release store carries
+    // their writes to the acquiring warps.
+    if (op != I_WAIT && h.w) {
+      __syncwarp();
+      if (lane == 0) st_release(prog + warp, h.w);
     }
   }
 }
 
-template <bool PROBE>
-__global__ void __launch_bounds__(BLOCK) eval_kernel(Params p) {
-  extern __shared__ uint32_t sfile[];
+template <int NW, bool PROBE>
+__global__ void __launch_bounds__(32 * NW) eval_kernel(Params p) {
+  extern __shared__ __align__(16) uint8_t sfile[];
   __shared__ uint32_t s_item;
   __shared__ uint32_t s_invalid;     // lanes with a vanished denominator (bitmask)
   __shared__ uint32_t s_bad[32];     // first failing obligation per lane
+  __shared__ uint32_t s_prog[MAX_NW];  // per-warp progress counters
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t warp = threadIdx.x >> 5;
-  uint32_t* gfile = p.scratch + (size_t)blockIdx.x * p.overflow_slots * 32u;
+  uint8_t* sl = sfile + lane * 4u;
+  uint8_t* gl = reinterpret_cast<uint8_t*>(p.scratch + (size_t)blockIdx.x * p.spill_slots * 32u) +
+                lane * 4u;
   for (;;) {
     if (threadIdx.x == 0) s_item = PROBE ? 0u : atomicAdd(p.counter, 1u);
     if (threadIdx.x < 32) s_bad[threadIdx.x] = 0xFFFFFFFFu;
+    if (threadIdx.x < MAX_NW) s_prog[threadIdx.x] = 0;
     if (threadIdx.x == 0) s_invalid = 0;
     __syncthreads();
     const uint32_t item = s_item;
@@ -191,7 +390,7 @@ __global__ void __launch_bounds__(BLOCK) eval_kernel(Params p) {
     const uint32_t w = tile * 32u + lane;
     bool valid = PROBE ? (w == p.probe_w) : (w < p.n_witness);
     uint32_t bad = 0xFFFFFFFFu;
-    run_stream<PROBE>(p, sd, sfile, gfile, w, valid, bad);
+    run_stream<PROBE>(p, sd, sl, gl, s_prog, w, valid, bad);
     // merge the warps' verdicts for each lane
     const uint32_t inval = __ballot_sync(0xFFFFFFFFu, !valid);
     if (lane == 0 && inval) atomicOr(&s_invalid, inval);
@@ -221,7 +420,7 @@ __global__ void __launch_bounds__(BLOCK) eval_kernel(Params p) {
 }
 
 // -- integer-pipe ceiling: register-resident field arithmetic, no decode, no memory.
-// KIND 0: fmul chains, 1: fadd chains, 2: keyed hash (mix64 + to_field).
+// KIND 0: fmul chains, 1: fadd chains, 2: keyed hash (mix64 + to_field), 3: inversions.
 template <int KIND>
 __global__ void __launch_bounds__(256) peak_kernel(uint32_t* sink, int iters, uint32_t salt) {
   uint32_t a[8], b[8];
@@ -238,7 +437,8 @@ __global__ void __launch_bounds__(256) peak_kernel(uint32_t* sink, int iters, ui
       for (int j = 0; j < 8; ++j) {
         if (KIND == 0) a[j] = fmul(a[j], b[j]);
         else if (KIND == 1) a[j] = fadd(a[j], b[j]);
-        else a[j] = uf_apply(0x9E3779B97F4A7C15ull + b[j], a[j]);
+        else if (KIND == 2) a[j] = uf_apply(0x9E3779B97F4A7C15ull + b[j], a[j]);
+        else a[j] = finv(a[j] + b[j]);
       }
     }
   }

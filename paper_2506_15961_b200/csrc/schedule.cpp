@@ -1,0 +1,583 @@
+// schedule.cpp -- back end of the stage compiler: value DAG -> v4 program.
+//
+// 1. List scheduling. Units are taken in priority order (the depth-first order
+//    of the obligation cones, which keeps the live set that of a sequential
+//    evaluation) by NW simulated warps. The warp that frees up first takes the
+//    highest-priority ready unit it can start now -- a unit whose operands a
+//    different warp produced is penalised by the cross-warp latency -- and
+//    bundles with it further ready units of the same kind (same op, function,
+//    arity) from a bounded look-ahead window, up to `bmax`. Every bundle gets a
+//    timestamp (start time, warp); every warp's stream is in timestamp order.
+// 2. Slot allocation. A value lives from its defining bundle to its last
+//    reading bundle; a slot is reused only by a bundle that starts strictly
+//    after the previous occupant's last read. Linear scan chooses values to
+//    keep in global memory when the shared file is too small ("spill
+//    everywhere": the defining bundle writes a temporary that a SPILL bundle
+//    stores right after it; every reading bundle is preceded by a FILL into a
+//    temporary); then all intervals are coloured exactly.
+// 3. Synchronisation. A bundle WAITs for the producer of every operand on
+//    another warp (read after write) and for the readers of the previous
+//    occupant of every slot it writes (write after read); waits implied by
+//    earlier ones (vector clocks) are dropped. All waits point to bundles with
+//    smaller timestamps, which makes the program deadlock-free. Producers
+//    SIGNAL after exactly the bundles someone waits on.
+#include "schedule.hpp"
+
+#include <algorithm>
+#include <queue>
+#include <set>
+#include <stdexcept>
+#include <unordered_map>
+
+namespace pqw {
+namespace {
+
+[[noreturn]] void fail(const char* m) { throw std::runtime_error(m); }
+
+constexpr uint64_t INF = ~0ull;
+
+// cost model (issue slots of one warp)
+uint32_t op_cost(const DagUnit& u) {
+  switch (u.op) {
+    case I_DOT: return u.k == 1 ? 9 : 5 + 4 * u.k;
+    case I_SUM: return u.k == 2 ? 8 : 4 + 3 * u.k;
+    case I_SUB: return 9;
+    case I_NEG: return 6;
+    case I_HASH: return 30;
+    case I_INV: return u.guarded ? 22 : 260;
+    case I_VAR: return 36;
+    case I_CONST: return 3;
+    case I_CHK: return 7;
+    case I_DEN: return 4;
+    default: return 4;
+  }
+}
+uint64_t bundle_cost(const DagUnit& h, size_t n) {
+  return 10 + n * op_cost(h) + (h.op == I_INV && h.guarded ? 250 : 0);
+}
+bool same_class(const DagUnit& a, const DagUnit& b) {
+  return a.op == b.op && a.fn == b.fn && a.k == b.k && !(a.op == I_INV && !(a.guarded && b.guarded));
+}
+
+struct Exec {             // one instruction bundle of a warp stream
+  uint32_t warp;
+  uint64_t ts;
+  uint8_t kind;           // 0 main, 1 fill, 2 spill
+  uint32_t main;          // main bundle index
+  uint32_t seq = 0;       // position in the warp's stream
+};
+
+struct Interval {
+  uint64_t start, end;
+  uint32_t writer;        // exec id
+  std::vector<uint32_t> readers;  // exec ids
+  uint32_t slot = 0;
+};
+
+// Exact colouring of intervals (a slot is free for `start` once its occupant's
+// end < start). Returns the number of slots; fills slot and, per interval, the
+// previous occupant of its slot (or -1).
+uint32_t colour(std::vector<Interval>& iv, std::vector<int32_t>& prev) {
+  std::vector<uint32_t> order(iv.size());
+  for (uint32_t i = 0; i < iv.size(); ++i) order[i] = i;
+  std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+    return iv[a].start != iv[b].start ? iv[a].start < iv[b].start : a < b;
+  });
+  using E = std::pair<uint64_t, uint32_t>;  // (end, slot)
+  std::priority_queue<E, std::vector<E>, std::greater<E>> busy;
+  std::priority_queue<uint32_t, std::vector<uint32_t>, std::greater<uint32_t>> free_s;
+  std::vector<int32_t> last_of_slot;
+  prev.assign(iv.size(), -1);
+  uint32_t n = 0;
+  for (uint32_t i : order) {
+    while (!busy.empty() && busy.top().first < iv[i].start) {
+      free_s.push(busy.top().second);
+      busy.pop();
+    }
+    uint32_t s;
+    if (!free_s.empty()) {
+      s = free_s.top();
+      free_s.pop();
+    } else {
+      s = n++;
+      last_of_slot.push_back(-1);
+    }
+    iv[i].slot = s;
+    prev[i] = last_of_slot[s];
+    last_of_slot[s] = (int32_t)i;
+    busy.push({iv[i].end, s});
+  }
+  return n;
+}
+
+}  // namespace
+
+Program schedule_program(const Dag& dag, const SchedOptions& opt) {
+  const auto& U = dag.units;
+  const uint32_t N = (uint32_t)U.size();
+  const uint32_t NW = opt.n_warps;
+  if (NW < 1 || NW > 32) fail("n_warps must be in [1, 32]");
+  const uint64_t X = opt.xlat;
+
+  // ---- producers / consumers ------------------------------------------------
+  std::vector<uint32_t> pred_off(N + 1, 0), preds;
+  std::vector<uint32_t> ncons(N, 0);
+  {
+    std::vector<uint32_t> tmp;
+    for (uint32_t u = 0; u < N; ++u) {
+      const DagUnit& d = U[u];
+      if ((uint64_t)d.arg0 + d.nargs > dag.pool.size()) fail("operand list out of range");
+      tmp.assign(dag.pool.begin() + d.arg0, dag.pool.begin() + d.arg0 + d.nargs);
+      std::sort(tmp.begin(), tmp.end());
+      tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+      for (uint32_t p : tmp) {
+        if (p >= u) fail("operand defined after its use");
+        if (!U[p].defines()) fail("operand is not a value");
+        preds.push_back(p);
+        ncons[p]++;
+      }
+      pred_off[u + 1] = (uint32_t)preds.size();
+    }
+  }
+  std::vector<uint32_t> cons_off(N + 1, 0), cons(preds.size());
+  for (uint32_t u = 0; u < N; ++u) cons_off[u + 1] = cons_off[u] + ncons[u];
+  {
+    std::vector<uint32_t> fillp(cons_off.begin(), cons_off.end() - 1);
+    for (uint32_t u = 0; u < N; ++u)
+      for (uint32_t i = pred_off[u]; i < pred_off[u + 1]; ++i) cons[fillp[preds[i]]++] = u;
+  }
+
+  // One scheduling attempt with look-ahead window o.window and bundle width
+  // o.bmax; false if the value file cannot hold even its temporaries.
+  auto try_once = [&](const SchedOptions& o, Program& prog) -> bool {
+    // ---- 1. list scheduling -------------------------------------------------
+    std::vector<uint64_t> fin(N, 0), F1(N, 0), F2(N, 0);
+    std::vector<int32_t> wof(N, -1), W1(N, -1);
+    std::vector<uint8_t> has2(N, 0), done(N, 0);
+    std::vector<uint32_t> npred(N), bundle_of(N, 0);
+    for (uint32_t u = 0; u < N; ++u) npred[u] = pred_off[u + 1] - pred_off[u];
+    std::set<uint32_t> ready;
+    auto make_ready = [&](uint32_t u) {
+      uint64_t f1 = 0;
+      int32_t w1 = -1;
+      for (uint32_t i = pred_off[u]; i < pred_off[u + 1]; ++i) {
+        const uint32_t p = preds[i];
+        if (w1 < 0 || fin[p] > f1) {
+          f1 = fin[p];
+          w1 = wof[p];
+        }
+      }
+      uint64_t f2 = 0;
+      bool h2 = false;
+      for (uint32_t i = pred_off[u]; i < pred_off[u + 1]; ++i) {
+        const uint32_t p = preds[i];
+        if (wof[p] != w1) {
+          f2 = std::max(f2, fin[p]);
+          h2 = true;
+        }
+      }
+      F1[u] = f1;
+      W1[u] = w1;
+      F2[u] = f2;
+      has2[u] = h2;
+      ready.insert(u);
+    };
+    auto est = [&](uint32_t u, uint32_t w) -> uint64_t {
+      if (W1[u] < 0) return 0;
+      if ((int32_t)w == W1[u]) return has2[u] ? std::max(F1[u], F2[u] + X) : F1[u];
+      return F1[u] + X;
+    };
+    for (uint32_t u = 0; u < N; ++u)
+      if (npred[u] == 0) make_ready(u);
+
+    struct Bundle {
+      uint32_t warp;
+      uint64_t start, finish;
+      std::vector<uint32_t> units;
+    };
+    std::vector<Bundle> bundles;
+    std::vector<uint64_t> T(NW, 0);
+    uint32_t frontier = 0, n_done = 0;
+    std::vector<uint32_t> cand;
+    uint64_t makespan = 0;
+    while (n_done < N) {
+      uint32_t w = 0;
+      for (uint32_t i = 1; i < std::min(NW, o.active_warps); ++i)
+        if (T[i] < T[w]) w = i;
+      const uint64_t t = T[w];
+      const uint64_t lim = (uint64_t)frontier + o.window;
+      auto it = ready.begin();
+      uint64_t tnext = INF;
+      for (; it != ready.end() && *it < lim; ++it) {
+        const uint64_t e = est(*it, w);
+        if (e <= t) break;
+        tnext = std::min(tnext, e);
+      }
+      if (it == ready.end() || *it >= lim) {
+        T[w] = tnext == INF ? t + 1 : std::max(t + 1, tnext);
+        continue;
+      }
+      const uint32_t head = *it;
+      const DagUnit& H = U[head];
+      cand.clear();
+      cand.push_back(head);
+      for (auto j = std::next(it); j != ready.end() && *j < lim && cand.size() < o.bmax; ++j)
+        if (same_class(U[*j], H) && est(*j, w) <= t) cand.push_back(*j);
+      const uint64_t cost = bundle_cost(H, cand.size());
+      const uint32_t bid = (uint32_t)bundles.size();
+      bundles.push_back({w, t, t + cost, cand});
+      for (uint32_t u : cand) {
+        ready.erase(u);
+        done[u] = 1;
+        fin[u] = t + cost;
+        wof[u] = (int32_t)w;
+        bundle_of[u] = bid;
+        n_done++;
+      }
+      for (uint32_t u : cand)
+        for (uint32_t i = cons_off[u]; i < cons_off[u + 1]; ++i)
+          if (--npred[cons[i]] == 0) make_ready(cons[i]);
+      T[w] = t + cost;
+      makespan = std::max(makespan, T[w]);
+      while (frontier < N && done[frontier]) frontier++;
+    }
+    const uint32_t NB = (uint32_t)bundles.size();
+    std::vector<uint64_t> bts(NB);
+    for (uint32_t b = 0; b < NB; ++b)
+      bts[b] = ((bundles[b].start * NW) + bundles[b].warp) * 4 + 1;
+    // a bundle's reads are over once it finishes: any bundle that starts at or
+    // after that time (timestamp > rend) may overwrite what it read
+    auto rend = [&](uint32_t b) -> uint64_t { return bundles[b].finish * NW * 4; };
+
+    // value intervals in timestamp space
+    std::vector<uint64_t> vdef(N, 0), vend(N, 0);
+    std::vector<uint32_t> values;
+    for (uint32_t u = 0; u < N; ++u) {
+      if (!U[u].defines()) continue;
+      values.push_back(u);
+      vdef[u] = bts[bundle_of[u]];
+      uint64_t e = rend(bundle_of[u]);
+      for (uint32_t i = cons_off[u]; i < cons_off[u + 1]; ++i)
+        e = std::max(e, rend(bundle_of[cons[i]]));
+      vend[u] = e;
+    }
+    std::sort(values.begin(), values.end(), [&](uint32_t a, uint32_t b) {
+      return vdef[a] != vdef[b] ? vdef[a] < vdef[b] : a < b;
+    });
+
+    // ---- 2. allocation: choose spills, then colour exactly -------------------
+    const uint32_t K = o.smem_slots;
+    for (uint32_t reserve = 0;; reserve = reserve ? reserve * 2 : 16) {
+      if (reserve >= K) break;  // give up on this schedule: re-schedule narrower
+      std::vector<uint8_t> spilled(N, 0);
+      {
+        const uint32_t keff = K - reserve;
+        std::set<std::pair<uint64_t, uint32_t>> active;
+        for (uint32_t v : values) {
+          while (!active.empty() && active.begin()->first < vdef[v]) active.erase(active.begin());
+          if (active.size() < keff) {
+            active.insert({vend[v], v});
+          } else {
+            auto last = std::prev(active.end());
+            if (last->first > vend[v]) {
+              spilled[last->second] = 1;
+              active.erase(last);
+              active.insert({vend[v], v});
+            } else {
+              spilled[v] = 1;
+            }
+          }
+        }
+      }
+      // exec bundles: [FILL] main [SPILL] per main bundle
+      std::vector<Exec> ex;
+      std::vector<int32_t> fill_of(NB, -1), spill_of(NB, -1), main_exec(NB, -1);
+      std::vector<uint8_t> needs_fill(NB, 0), needs_spill(NB, 0);
+      for (uint32_t v : values) {
+        if (!spilled[v]) continue;
+        needs_spill[bundle_of[v]] = 1;
+        for (uint32_t i = cons_off[v]; i < cons_off[v + 1]; ++i) needs_fill[bundle_of[cons[i]]] = 1;
+      }
+      for (uint32_t b = 0; b < NB; ++b) {
+        if (needs_fill[b]) {
+          fill_of[b] = (int32_t)ex.size();
+          ex.push_back({bundles[b].warp, bts[b] - 1, 1, b});
+        }
+        main_exec[b] = (int32_t)ex.size();
+        ex.push_back({bundles[b].warp, bts[b], 0, b});
+        if (needs_spill[b]) {
+          spill_of[b] = (int32_t)ex.size();
+          ex.push_back({bundles[b].warp, bts[b] + 1, 2, b});
+        }
+      }
+      // intervals
+      std::vector<Interval> sm, gm;
+      std::vector<uint32_t> v_iv(N, ~0u), v_giv(N, ~0u);
+      std::unordered_map<uint64_t, uint32_t> fill_iv;  // (bundle << 32 | value) -> interval
+      std::vector<uint32_t> rd;
+      for (uint32_t v : values) {
+        const uint32_t bdef = bundle_of[v];
+        rd.clear();
+        for (uint32_t i = cons_off[v]; i < cons_off[v + 1]; ++i) rd.push_back(bundle_of[cons[i]]);
+        std::sort(rd.begin(), rd.end());
+        rd.erase(std::unique(rd.begin(), rd.end()), rd.end());
+        if (!spilled[v]) {
+          Interval I{vdef[v], vend[v], (uint32_t)main_exec[bdef], {}};
+          for (uint32_t b : rd) I.readers.push_back((uint32_t)main_exec[b]);
+          v_iv[v] = (uint32_t)sm.size();
+          sm.push_back(std::move(I));
+        } else {
+          Interval T1{vdef[v], rend(bdef) + 1, (uint32_t)main_exec[bdef], {(uint32_t)spill_of[bdef]}};
+          v_iv[v] = (uint32_t)sm.size();
+          sm.push_back(std::move(T1));
+          Interval G{vdef[v] + 1, rend(bdef) + 1, (uint32_t)spill_of[bdef], {}};
+          for (uint32_t b : rd) {
+            G.end = std::max(G.end, bts[b]);
+            G.readers.push_back((uint32_t)fill_of[b]);
+            Interval Fi{bts[b] - 1, rend(b), (uint32_t)fill_of[b], {(uint32_t)main_exec[b]}};
+            fill_iv[((uint64_t)b << 32) | v] = (uint32_t)sm.size();
+            sm.push_back(std::move(Fi));
+          }
+          v_giv[v] = (uint32_t)gm.size();
+          gm.push_back(std::move(G));
+        }
+      }
+      std::vector<int32_t> sprev, gprev;
+      const uint32_t n_sm = colour(sm, sprev);
+      if (n_sm > K) continue;  // more temporaries than the reserve: spill more
+      const uint32_t n_gm = colour(gm, gprev);
+
+      // ---- 3. synchronisation -------------------------------------------------
+      const uint32_t NE = (uint32_t)ex.size();
+      std::vector<std::vector<uint32_t>> stream(NW);
+      {
+        std::vector<uint32_t> order(NE);
+        for (uint32_t i = 0; i < NE; ++i) order[i] = i;
+        std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return ex[a].ts < ex[b].ts; });
+        for (uint32_t e : order) {
+          ex[e].seq = (uint32_t)stream[ex[e].warp].size();
+          stream[ex[e].warp].push_back(e);
+        }
+      }
+      // requirements per exec: (warp, count) with count = producer seq + 1
+      std::vector<std::vector<std::pair<uint32_t, uint32_t>>> req(NE);
+      auto need = [&](uint32_t e, uint32_t producer) {
+        if (ex[producer].warp == ex[e].warp) return;
+        req[e].push_back({ex[producer].warp, ex[producer].seq + 1});
+      };
+      for (uint32_t v : values) {
+        const uint32_t bdef = bundle_of[v];
+        if (!spilled[v]) {
+          for (uint32_t r : sm[v_iv[v]].readers) need(r, (uint32_t)main_exec[bdef]);
+        } else {
+          for (uint32_t r : gm[v_giv[v]].readers) need(r, (uint32_t)spill_of[bdef]);
+        }
+      }
+      auto war = [&](std::vector<Interval>& iv, const std::vector<int32_t>& prv) {
+        for (uint32_t i = 0; i < iv.size(); ++i) {
+          if (prv[i] < 0) continue;
+          const Interval& P = iv[prv[i]];
+          if (P.readers.empty()) need(iv[i].writer, P.writer);
+          for (uint32_t r : P.readers) need(iv[i].writer, r);
+        }
+      };
+      war(sm, sprev);
+      war(gm, gprev);
+      // vector clocks in timestamp order
+      std::vector<uint32_t> snap((size_t)NE * NW, 0);
+      std::vector<std::vector<uint32_t>> vc(NW, std::vector<uint32_t>(NW, 0));
+      std::vector<std::vector<std::pair<uint32_t, uint32_t>>> waits(NE);
+      std::vector<uint8_t> signal_after(NE, 0);
+      {
+        std::vector<uint32_t> order(NE);
+        for (uint32_t i = 0; i < NE; ++i) order[i] = i;
+        std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return ex[a].ts < ex[b].ts; });
+        for (uint32_t e : order) {
+          const uint32_t w = ex[e].warp;
+          auto& rq = req[e];
+          std::sort(rq.begin(), rq.end(), [](auto& a, auto& b) {
+            return a.first != b.first ? a.first < b.first : a.second > b.second;
+          });
+          for (size_t i = 0; i < rq.size(); ++i) {
+            if (i && rq[i].first == rq[i - 1].first) continue;  // max count per warp first
+            const uint32_t pw = rq[i].first, c = rq[i].second;
+            if (vc[w][pw] >= c) continue;
+            waits[e].push_back({pw, c});
+            const uint32_t pe = stream[pw][c - 1];
+            signal_after[pe] = 1;
+            const uint32_t* s = &snap[(size_t)pe * NW];
+            for (uint32_t j = 0; j < NW; ++j) vc[w][j] = std::max(vc[w][j], s[j]);
+            vc[w][pw] = std::max(vc[w][pw], c);
+          }
+          vc[w][w] = ex[e].seq + 1;
+          std::copy(vc[w].begin(), vc[w].end(), &snap[(size_t)e * NW]);
+        }
+      }
+
+      // ---- 4. emission ------------------------------------------------------------
+      prog = Program{};
+      auto& code = prog.code;
+      const uint32_t table = (NW + 3) / 4;
+      code.assign(table, pqw_ins{0, 0, 0, 0});
+      std::vector<uint32_t> fields;
+      auto put_bundle = [&](uint32_t op, uint32_t fn, uint32_t k, uint32_t n, uint32_t aux,
+                            const std::vector<uint32_t>& f, uint32_t nf) {
+        // f: nf fields per op, op-major (f[i * nf + j])
+        code.push_back(pqw_ins{isa_header(op, fn, k), n, aux, 0});
+        for (uint32_t g = 0; g < n; g += GROUP)
+          for (uint32_t j = 0; j < nf; ++j) {
+            uint32_t v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (uint32_t i = 0; i < GROUP && g + i < n; ++i) v[i] = f[(size_t)(g + i) * nf + j];
+            code.push_back(pqw_ins{v[0], v[1], v[2], v[3]});
+            code.push_back(pqw_ins{v[4], v[5], v[6], v[7]});
+          }
+        prog.op_hist[op] += n;
+      };
+      auto soff = [&](uint32_t iv) { return sm[iv].slot * SLOT_BYTES; };
+      for (uint32_t w = 0; w < NW; ++w) {
+        reinterpret_cast<uint32_t*>(code.data())[w] = (uint32_t)code.size();
+        for (uint32_t e : stream[w]) {
+          const Exec& E = ex[e];
+          for (auto& pr : waits[e]) {
+            code.push_back(pqw_ins{isa_header(I_WAIT, 0, 0), 0, pr.first, pr.second});
+            prog.op_hist[I_WAIT]++;
+            prog.n_waits++;
+          }
+          const size_t hdr = code.size();  // header of this exec's instruction
+          const auto& B = bundles[E.main];
+          if (E.kind == 1 || E.kind == 2) {
+            fields.clear();
+            uint32_t n = 0;
+            if (E.kind == 1) {
+              std::vector<uint32_t> seen;
+              for (uint32_t u : B.units)
+                for (uint32_t a = 0; a < U[u].nargs; ++a) {
+                  const uint32_t v = dag.pool[U[u].arg0 + a];
+                  if (!spilled[v] || std::find(seen.begin(), seen.end(), v) != seen.end()) continue;
+                  seen.push_back(v);
+                  fields.push_back(soff(fill_iv.at(((uint64_t)E.main << 32) | v)));
+                  fields.push_back(gm[v_giv[v]].slot * SLOT_BYTES);
+                  n++;
+                }
+              put_bundle(I_FILL, 0, 0, n, 0, fields, 2);
+            } else {
+              for (uint32_t u : B.units)
+                if (U[u].defines() && spilled[u]) {
+                  fields.push_back(gm[v_giv[u]].slot * SLOT_BYTES);
+                  fields.push_back(soff(v_iv[u]));
+                  n++;
+                }
+              put_bundle(I_SPILL, 0, 0, n, 0, fields, 2);
+            }
+          } else {
+            const DagUnit& H = U[B.units[0]];
+            auto opnd = [&](uint32_t v) -> uint32_t {
+              if (!spilled[v]) return soff(v_iv[v]);
+              return soff(fill_iv.at(((uint64_t)E.main << 32) | v));
+            };
+            fields.clear();
+            uint32_t nf = isa_fields(H.op, H.k);
+            for (uint32_t u : B.units) {
+              const DagUnit& d = U[u];
+              const uint32_t* a = &dag.pool[d.arg0];
+              switch (d.op) {
+                case I_CHK:
+                  fields.push_back(d.aux);
+                  fields.push_back(opnd(a[0]));
+                  fields.push_back(opnd(a[1]));
+                  break;
+                case I_DEN:
+                  fields.push_back(opnd(a[0]));
+                  break;
+                case I_VAR:
+                case I_CONST:
+                  fields.push_back(soff(v_iv[u]));
+                  fields.push_back(d.aux);
+                  break;
+                default:
+                  fields.push_back(soff(v_iv[u]));
+                  for (uint32_t i = 0; i < d.nargs; ++i) fields.push_back(opnd(a[i]));
+              }
+              if (fields.size() % nf) fail("internal: operand count does not match the op");
+              // field ops per witness
+              switch (d.op) {
+                case I_DOT: prog.cls[0] += d.k; prog.cls[1] += d.k - 1; break;
+                case I_SUM: prog.cls[1] += d.k - 1; break;
+                case I_SUB: case I_NEG: prog.cls[1] += 1; break;
+                case I_HASH: case I_VAR: prog.cls[2] += 1; break;
+                case I_CHK: case I_DEN: prog.cls[4] += 1; break;
+                default: break;
+              }
+            }
+            if (H.op == I_INV) {
+              const uint64_t n = B.units.size();
+              if (n > 1 && !H.guarded) fail("internal: unguarded inversions bundled");
+              prog.cls[0] += 3 * (n - 1);
+              prog.cls[3] += 1;
+            }
+            put_bundle(H.op, H.fn, H.k, (uint32_t)B.units.size(), 0, fields, nf);
+          }
+          if (signal_after[e]) {
+            code[hdr].b = E.seq + 1;  // header.w: publish progress after this bundle
+            prog.op_hist[I_SIGNAL]++;
+          }
+        }
+        code.push_back(pqw_ins{I_END, 0, 0, 0});
+      }
+      prog.n_slots = n_sm;
+      prog.n_spill = n_gm;
+      prog.n_bundles = NB;
+      prog.makespan = makespan;
+      for (uint32_t v : values) prog.n_spilled_values += spilled[v];
+      return true;
+    }
+    return false;
+  };
+
+  // A wide look-ahead window exposes the most parallelism (and the widest
+  // bundles) but holds more values live; narrower windows trade parallelism
+  // for fewer spills. Take the best modelled time: makespan plus the
+  // FILL/SPILL traffic spread over the warps.
+  std::vector<uint32_t> windows;
+  if (opt.window) {
+    windows.push_back(opt.window);
+  } else {
+    for (uint32_t w : {N + 1, 4096u, 1024u, 384u, 64u, 8u, 1u})
+      if (windows.empty() || w < windows.back()) windows.push_back(std::max<uint32_t>(w, 1));
+  }
+  Program best;
+  bool have = false;
+  uint64_t best_score = INF;
+  for (uint32_t win : windows) {
+    if (have && win < 384) break;  // tiny windows only as a last resort
+    SchedOptions o = opt;
+    o.window = win;
+    Program cand;
+    bool ok = false;
+    for (uint32_t bm = opt.bmax; !ok; bm /= 2) {
+      o.bmax = std::max<uint32_t>(bm, 1);
+      ok = try_once(o, cand);
+      if (bm <= 1) break;
+    }
+    if (!ok) continue;
+    const uint64_t traffic = cand.op_hist[I_FILL] + cand.op_hist[I_SPILL];
+    const uint64_t score = cand.makespan + traffic * 8 / NW;
+    if (score < best_score) {
+      best_score = score;
+      best = std::move(cand);
+      have = true;
+    }
+    if (traffic == 0) break;  // narrower windows cannot do better without spills
+  }
+  if (!have) {
+    // last resort: one warp, one op per bundle (a sequential evaluation)
+    SchedOptions o = opt;
+    o.window = 1;
+    o.bmax = 1;
+    o.active_warps = 1;
+    if (!try_once(o, best)) fail("stage does not fit the shared value file");
+  }
+  return best;
+}
+
+}  // namespace pqw

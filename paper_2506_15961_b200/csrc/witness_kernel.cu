@@ -67,11 +67,14 @@ struct pqw_engine {
   uint32_t n_gpu_stages = 0;
   uint32_t max_slots = 0;
   uint32_t smem_slots = 0;
-  uint32_t fast_slots = pqw::DEFAULT_FAST_SLOTS;  // compile-time fast-file size
-  uint32_t overflow_slots = 0;
+  uint32_t n_warps = pqw::DEFAULT_WARPS;
+  uint32_t fast_slots = pqw::DEFAULT_FAST_SLOTS;  // shared value-file capacity (slots)
+  uint32_t spill_slots = 0;                        // per-CTA global spill capacity
+  pqw::SchedOptions sched;
   uint32_t grid = 0;
   uint64_t n_code = 0;
   uint64_t op_hist[PQW_B_NUM_OPS] = {};
+  uint64_t cls[5] = {};
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool timed = false;
   std::vector<unsigned long long> h_first_bad;
@@ -129,10 +132,18 @@ int pqw_engine_create(int device, uint64_t seed, const uint64_t fn_keys[3], pqw_
   e->device = device;
   e->seed = seed;
   for (int i = 0; i < 3; ++i) e->fn_keys[i] = fn_keys[i];
-  if (const char* fs = getenv("PQW_FAST_SLOTS")) {
-    int v = atoi(fs);
-    if (v >= 1 && v <= 1700) e->fast_slots = (uint32_t)v;
-  }
+  auto env = [](const char* name, int lo, int hi, uint32_t& out) {
+    if (const char* s = getenv(name)) {
+      int v = atoi(s);
+      if (v >= lo && v <= hi) out = (uint32_t)v;
+    }
+  };
+  env("PQW_FAST_SLOTS", 16, 1780, e->fast_slots);
+  env("PQW_WARPS", 8, 16, e->n_warps);
+  if (e->n_warps != 8 && e->n_warps != 16) e->n_warps = pqw::DEFAULT_WARPS;
+  env("PQW_WINDOW", 1, 1 << 20, e->sched.window);
+  env("PQW_BMAX", 1, 4096, e->sched.bmax);
+  env("PQW_XLAT", 0, 1 << 20, e->sched.xlat);
   *out = e;
   return PQW_OK;
 }
@@ -177,7 +188,7 @@ int pqw_stage_add(pqw_engine* e, const int32_t* ir, size_t ir_len, const int64_t
   if (!hit) {
     try {
       st = pqw::compile_stage(ir, ir_len, consts, n_consts, (uint32_t)n_vars, base, e->fn_keys,
-                              e->fast_slots, pqw::NW);
+                              e->fast_slots, e->n_warps, e->sched);
     } catch (const std::exception& ex) {
       return fail(PQW_EINVAL, std::string("stage compile: ") + ex.what());
     }
@@ -203,6 +214,8 @@ int pqw_stage_add(pqw_engine* e, const int32_t* ir, size_t ir_len, const int64_t
   out_status[11] = st.exact_rhs;
   out_status[12] = (int64_t)st.field_ops;
   out_status[13] = st.n_vars;
+  out_status[14] = st.n_spill;
+  out_status[15] = (int64_t)st.n_bundles;
   e->stages.push_back(std::move(st));
   e->uploaded = false;
   return (int)(e->stages.size() - 1);
@@ -264,10 +277,13 @@ int pqw_upload(pqw_engine* e) {
   std::vector<uint32_t> work;
   std::unordered_map<const std::vector<pqw_ins>*, uint32_t> placed;  // shared programs: one copy
   e->max_slots = 0;
+  e->spill_slots = 0;
   e->n_code = 0;
   std::fill(std::begin(e->op_hist), std::end(e->op_hist), 0);
+  std::fill(std::begin(e->cls), std::end(e->cls), 0);
   for (size_t r = 0; r < ids.size(); ++r) {
     const auto& st = e->stages[ids[r]];
+    if (st.n_warps != e->n_warps) return fail(PQW_EINVAL, "stage compiled for another warp count");
     auto pit = placed.find(st.code.get());
     uint32_t off;
     if (pit == placed.end()) {
@@ -280,33 +296,41 @@ int pqw_upload(pqw_engine* e) {
     descs.push_back({off, st.n_slots, st.var_base, (uint32_t)r});
     work.push_back((uint32_t)r);
     e->max_slots = std::max(e->max_slots, st.n_slots);
+    e->spill_slots = std::max(e->spill_slots, st.n_spill);
     e->n_code += st.code->size();
-    for (const auto& in : *st.code)
-      if (in.op < PQW_B_NUM_OPS) e->op_hist[in.op]++;
+    for (int i = 0; i < PQW_B_NUM_OPS; ++i) e->op_hist[i] += st.op_hist[i];
+    for (int i = 0; i < 5; ++i) e->cls[i] += st.cls[i];
   }
   e->n_code_unique = code.size();
   if (code.empty()) code.push_back(pqw_ins{PQW_B_END, 0, 0, 0});
-  code.push_back(pqw_ins{PQW_B_END, 0, 0, 0});  // the prefetching decoder reads one past END
   if (descs.empty()) descs.push_back({0, 0, 0, 0});
   if (work.empty()) work.push_back(0);
 
   cudaDeviceProp prop;
   CU(cudaGetDeviceProperties(&prop, e->device));
-  // the fast (shared-memory) slot file has the size the stages were compiled
-  // for; spill slots live in per-warp global scratch
-  const size_t slot_bytes = (size_t)pqw::TW * sizeof(uint32_t);  // one slot, all warps
-  if ((size_t)e->fast_slots * slot_bytes > prop.sharedMemPerBlockOptin - 2048)
-    return fail(PQW_EINVAL, "fast slot file does not fit in shared memory");
-  e->smem_slots = std::max<uint32_t>(e->fast_slots, 1);
-  e->overflow_slots = e->max_slots > e->smem_slots ? e->max_slots - e->smem_slots : 0;
+  // the shared value file is as large as the largest stage needs (at most the
+  // capacity the stages were compiled for); spills live in per-CTA scratch
+  const size_t slot_bytes = pqw::SLOT_BYTES;
+  e->smem_slots = std::max<uint32_t>(e->max_slots, 1);
   const size_t smem_bytes = (size_t)e->smem_slots * slot_bytes;
-  CU(cudaFuncSetAttribute(pqw::eval_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)smem_bytes));
-  CU(cudaFuncSetAttribute(pqw::eval_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)smem_bytes));
+  if (smem_bytes + 4096 > prop.sharedMemPerBlockOptin)
+    return fail(PQW_EINVAL, "value file does not fit in shared memory");
   int per_sm = 0;
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pqw::eval_kernel<false>, pqw::BLOCK,
-                                                   smem_bytes));
+  if (e->n_warps == 16) {
+    CU(cudaFuncSetAttribute(pqw::eval_kernel<16, false>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
+    CU(cudaFuncSetAttribute(pqw::eval_kernel<16, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pqw::eval_kernel<16, false>,
+                                                     16 * 32, smem_bytes));
+  } else {
+    CU(cudaFuncSetAttribute(pqw::eval_kernel<8, false>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
+    CU(cudaFuncSetAttribute(pqw::eval_kernel<8, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pqw::eval_kernel<8, false>, 8 * 32,
+                                                     smem_bytes));
+  }
   if (per_sm < 1) per_sm = 1;
   e->grid = (uint32_t)(prop.multiProcessorCount * per_sm);
 
@@ -325,7 +349,7 @@ int pqw_upload(pqw_engine* e) {
   CU(cudaMalloc(&e->d_fn_keys, 3 * sizeof(uint64_t)));
   CU(cudaMemcpy(e->d_fn_keys, e->fn_keys, 3 * sizeof(uint64_t), cudaMemcpyHostToDevice));
   CU(cudaMalloc(&e->d_counter, sizeof(uint32_t)));
-  e->scratch_bytes = (size_t)e->grid * std::max<uint32_t>(e->overflow_slots, 1) * slot_bytes;
+  e->scratch_bytes = (size_t)e->grid * std::max<uint32_t>(e->spill_slots, 1) * slot_bytes;
   CU(cudaMalloc(&e->d_scratch, e->scratch_bytes));
   size_t nr = std::max<size_t>(ids.size(), 1);
   CU(cudaMalloc(&e->d_first_bad, nr * sizeof(unsigned long long)));
@@ -336,6 +360,20 @@ int pqw_upload(pqw_engine* e) {
   if (!e->ev1) CU(cudaEventCreate(&e->ev1));
   e->uploaded = true;
   e->results_ready = false;
+  return PQW_OK;
+}
+
+static int launch_eval(pqw_engine* e, const pqw::Params& p, uint32_t grid, bool probe,
+                       cudaStream_t s) {
+  const size_t smem_bytes = (size_t)e->smem_slots * pqw::SLOT_BYTES;
+  if (e->n_warps == 16) {
+    if (probe) pqw::eval_kernel<16, true><<<1, 16 * 32, smem_bytes, s>>>(p);
+    else pqw::eval_kernel<16, false><<<grid, 16 * 32, smem_bytes, s>>>(p);
+  } else {
+    if (probe) pqw::eval_kernel<8, true><<<1, 8 * 32, smem_bytes, s>>>(p);
+    else pqw::eval_kernel<8, false><<<grid, 8 * 32, smem_bytes, s>>>(p);
+  }
+  CU(cudaGetLastError());
   return PQW_OK;
 }
 
@@ -367,13 +405,11 @@ int pqw_launch(pqw_engine* e, uint32_t n_witness, void* stream) {
   p.tiles = (n_witness + pqw::TW - 1) / pqw::TW;
   p.n_items = e->n_gpu_stages * p.tiles;
   p.n_witness = n_witness;
-  p.smem_slots = e->smem_slots;
-  p.overflow_slots = std::max<uint32_t>(e->overflow_slots, 1);
-  const size_t smem_bytes = (size_t)e->smem_slots * pqw::TW * sizeof(uint32_t);
+  p.spill_slots = std::max<uint32_t>(e->spill_slots, 1);
   uint32_t grid = std::min<uint32_t>(e->grid, std::max<uint32_t>(p.n_items, 1));
   CU(cudaEventRecord(e->ev0, s));
-  pqw::eval_kernel<false><<<grid, pqw::BLOCK, smem_bytes, s>>>(p);
-  CU(cudaGetLastError());
+  int rc = launch_eval(e, p, grid, false, s);
+  if (rc != PQW_OK) return rc;
   CU(cudaEventRecord(e->ev1, s));
   e->timed = true;
   return PQW_OK;
@@ -440,15 +476,15 @@ int pqw_probe(pqw_engine* e, int stage, uint32_t witness, uint32_t obl, uint32_t
   p.n_items = 1;
   p.tiles = 1;
   p.n_witness = witness + 1;
-  p.smem_slots = e->smem_slots;
-  p.overflow_slots = std::max<uint32_t>(e->overflow_slots, 1);
+  p.spill_slots = std::max<uint32_t>(e->spill_slots, 1);
   p.probe_w = witness;
   p.probe_obl = obl;
   p.probe_out = e->d_probe;
   p.probe_vars = d_vars;
-  const size_t smem_bytes = (size_t)e->smem_slots * pqw::TW * sizeof(uint32_t);
-  pqw::eval_kernel<true><<<1, pqw::BLOCK, smem_bytes>>>(p);
-  CU(cudaGetLastError());
+  {
+    int rc = launch_eval(e, p, 1, true, 0);
+    if (rc != PQW_OK) return rc;
+  }
   CU(cudaDeviceSynchronize());
   uint32_t got[2];
   CU(cudaMemcpy(got, e->d_probe, sizeof(got), cudaMemcpyDeviceToHost));
@@ -475,29 +511,34 @@ int pqw_last_launch_ms(pqw_engine* e, float* ms) {
 
 int pqw_image_stats(pqw_engine* e, uint64_t* out, size_t cap) {
   if (!e || !out) return fail(PQW_EINVAL, "null argument");
-  uint64_t buf[6 + PQW_B_NUM_OPS] = {};
-  uint64_t n_gpu = 0, n_code = 0, max_slots = 0;
-  uint64_t hist[PQW_B_NUM_OPS] = {};
+  constexpr int N = PQW_B_NUM_OPS;
+  uint64_t buf[PQW_IMAGE_STATS_LEN] = {};
+  uint64_t n_gpu = 0, n_code = 0, max_slots = 0, max_spill = 0, bundles = 0, waits = 0;
   for (const auto& st : e->stages) {
     if (st.status != PQW_STAGE_OK) continue;
     n_gpu++;
     n_code += st.code->size();
     max_slots = std::max<uint64_t>(max_slots, st.n_slots);
-    for (const auto& in : *st.code)
-      if (in.op < PQW_B_NUM_OPS) hist[in.op]++;
+    max_spill = std::max<uint64_t>(max_spill, st.n_spill);
+    bundles += st.n_bundles;
+    waits += st.n_waits;
+    for (int i = 0; i < N; ++i) buf[4 + i] += st.op_hist[i];
+    for (int i = 0; i < 5; ++i) buf[6 + N + i] += st.cls[i];
   }
   buf[0] = n_gpu;
   buf[1] = n_code;
   buf[2] = max_slots;
   buf[3] = e->smem_slots;
-  for (int i = 0; i < PQW_B_NUM_OPS; ++i) buf[4 + i] = hist[i];
-  buf[4 + PQW_B_NUM_OPS] = e->n_code_unique;
-  buf[5 + PQW_B_NUM_OPS] = e->cache_hits;
-  std::memcpy(out, buf, std::min(cap, (size_t)(6 + PQW_B_NUM_OPS)) * sizeof(uint64_t));
+  buf[4 + N] = e->n_code_unique;
+  buf[5 + N] = e->cache_hits;
+  buf[11 + N] = max_spill;
+  buf[12 + N] = bundles;
+  buf[13 + N] = waits;
+  std::memcpy(out, buf, std::min(cap, (size_t)PQW_IMAGE_STATS_LEN) * sizeof(uint64_t));
   return PQW_OK;
 }
 
-int pqw_peak_fieldops(int device, double out[3]) {
+int pqw_peak_fieldops(int device, double out[4]) {
   if (!out) return fail(PQW_EINVAL, "null argument");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device) {
@@ -513,21 +554,22 @@ int pqw_peak_fieldops(int device, double out[3]) {
   cudaEvent_t e0, e1;
   CU(cudaEventCreate(&e0));
   CU(cudaEventCreate(&e1));
-  for (int kind = 0; kind < 3; ++kind) {
+  for (int kind = 0; kind < 4; ++kind) {
     float best = 1e30f;
     for (int rep = 0; rep < 4; ++rep) {
-      int it = kind == 2 ? iters / 8 : iters;
+      int it = kind == 2 ? iters / 8 : kind == 3 ? iters / 32 : iters;
       CU(cudaEventRecord(e0));
       if (kind == 0) pqw::peak_kernel<0><<<blocks, threads>>>(sink, it, rep);
       else if (kind == 1) pqw::peak_kernel<1><<<blocks, threads>>>(sink, it, rep);
-      else pqw::peak_kernel<2><<<blocks, threads>>>(sink, it, rep);
+      else if (kind == 2) pqw::peak_kernel<2><<<blocks, threads>>>(sink, it, rep);
+      else pqw::peak_kernel<3><<<blocks, threads>>>(sink, it, rep);
       CU(cudaEventRecord(e1));
       CU(cudaEventSynchronize(e1));
       float ms = 0;
       CU(cudaEventElapsedTime(&ms, e0, e1));
       if (rep > 0 && ms < best) best = ms;  // rep 0 warms up
     }
-    double n_ops = (double)blocks * threads * (kind == 2 ? iters / 8 : iters) * 16 * 8;
+    double n_ops = (double)blocks * threads * (kind == 2 ? iters / 8 : kind == 3 ? iters / 32 : iters) * 16 * 8;
     out[kind] = n_ops / (best * 1e-3);
   }
   cudaEventDestroy(e0);

@@ -18,7 +18,7 @@ from .errors import EngineError, EngineUnavailable
 
 LIB_NAME = "libplaneq_witness.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 # PQW_STAGE_* codes
 STAGE_OK = 0
@@ -29,9 +29,11 @@ STAGE_LOG_DIV0 = 4
 STAGE_BAD_INDEX = 5
 
 # bytecode opcodes (pqw_bop)
-BOP_NAMES = ("END", "CONST", "VAR", "ADD", "SUB", "MUL", "NEG", "DIV", "HASH", "ACC_MUL",
-             "ACC_MAC", "ACC_LD", "ACC_ADD", "ACC_ST", "CHK", "DEN", "ACC_MACF", "INV", "ACC_MUL2", "ACC_MAC2", "BAR")
+BOP_NAMES = ("END", "DOT", "SUM", "SUB", "NEG", "HASH", "INV", "VAR", "CONST", "CHK", "DEN",
+             "FILL", "SPILL", "WAIT", "SIGNAL")
 N_BOPS = len(BOP_NAMES)
+IMAGE_STATS_LEN = 14 + N_BOPS
+FIELD_CLASSES = ("mul", "add", "hash", "inv", "cmp")
 
 EXPORTS = ("pqw_abi_version", "pqw_last_error", "pqw_device_count", "pqw_engine_create",
            "pqw_engine_destroy", "pqw_stage_add", "pqw_reset", "pqw_stage_bytecode",
@@ -108,12 +110,12 @@ def device_count() -> int:
 def peak_fieldops(device: int = 0) -> dict:
     """Measured register-resident F_p op rates of the device (ops/s)."""
     lib = load_library()
-    out = (C.c_double * 3)()
+    out = (C.c_double * 4)()
     rc = lib.pqw_peak_fieldops(device, out)
     if rc < 0:
         msg = lib.pqw_last_error().decode(errors="replace")
         raise (EngineUnavailable if rc == -2 else EngineError)(msg)
-    return {"mul": out[0], "add": out[1], "hash": out[2]}
+    return {"mul": out[0], "add": out[1], "hash": out[2], "inv": out[3]}
 
 
 def _ptr(a: np.ndarray, ct):
@@ -138,6 +140,8 @@ class StageCompile:
     exact_rhs: int | None
     field_ops: int
     n_vars: int
+    spill_slots: int = 0
+    bundles: int = 0
 
 
 class Engine:
@@ -195,14 +199,15 @@ class Engine:
                             const_lhs=int(st[8]), const_rhs=int(st[9]),
                             exact_lhs=None if st[10] == imin else int(st[10]),
                             exact_rhs=None if st[11] == imin else int(st[11]),
-                            field_ops=int(st[12]), n_vars=int(st[13]))
+                            field_ops=int(st[12]), n_vars=int(st[13]),
+                            spill_slots=int(st[14]), bundles=int(st[15]))
 
     def reset(self):
         self._check(self.lib.pqw_reset(self._h))
         self.n_stages = 0
 
     def bytecode(self, stage: int) -> tuple[np.ndarray, int]:
-        """(instructions as an (n, 4) uint32 array, slot count) of a stage."""
+        """(program records as an (n, 4) uint32 array, shared slot count) of a stage."""
         slots = C.c_uint32()
         n = self._check(self.lib.pqw_stage_bytecode(self._h, stage, None, 0, C.byref(slots)))
         buf = (_Ins * max(n, 1))()
@@ -245,9 +250,13 @@ class Engine:
         return float(ms.value)
 
     def image_stats(self) -> dict:
-        out = np.zeros(6 + N_BOPS, dtype=np.uint64)
+        out = np.zeros(IMAGE_STATS_LEN, dtype=np.uint64)
         self._check(self.lib.pqw_image_stats(self._h, _ptr(out, C.c_uint64), out.size))
+        n = N_BOPS
         return {"gpu_stages": int(out[0]), "instructions": int(out[1]),
                 "max_slots": int(out[2]), "smem_slots": int(out[3]),
-                "op_hist": {BOP_NAMES[i]: int(out[4 + i]) for i in range(N_BOPS)},
-                "unique_instructions": int(out[4 + N_BOPS]), "cache_hits": int(out[5 + N_BOPS])}
+                "op_hist": {BOP_NAMES[i]: int(out[4 + i]) for i in range(n)},
+                "unique_instructions": int(out[4 + n]), "cache_hits": int(out[5 + n]),
+                "field_ops": {FIELD_CLASSES[i]: int(out[6 + n + i]) for i in range(5)},
+                "max_spill_slots": int(out[11 + n]), "bundles": int(out[12 + n]),
+                "waits": int(out[13 + n])}

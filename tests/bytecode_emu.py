@@ -1,12 +1,16 @@
-"""TEST INFRASTRUCTURE ONLY: numpy emulation of the engine's cooperative bytecode.
+"""TEST INFRASTRUCTURE ONLY: numpy emulation of the engine's v4 stage programs.
 
-Lets the CPU test suite check the host compiler's output (barrier-phased F_p
-bytecode, one stream per warp, exported through pqw_stage_bytecode) against
-the independent oracle without a GPU. Semantics mirror the device interpreter
-in paper_2506_15961_b200/csrc/interp.cuh (run_stream / eval_kernel): the warps
-of one phase run in arbitrary order (here: warp 0 first, then 1, ...; the test
-also runs them in reverse to catch cross-warp hazards), each with its own
-64-bit accumulator, all sharing one value file. The product never calls this.
+Lets the CPU test suite check the host compiler's output (isa.hpp programs:
+one instruction stream per warp, bundles of independent ops, explicit
+WAIT/SIGNAL between warps; exported through pqw_stage_bytecode) against the
+independent oracle without a GPU. Semantics mirror the device interpreter in
+paper_2506_15961_b200/csrc/interp.cuh: all warps share one value file; a warp
+blocked in WAIT does not advance. The warps are interleaved instruction by
+instruction under a chosen policy -- "random" (seeded), "ahead" (run the
+lowest runnable warp until it blocks) or "behind" (the highest) -- so a
+missing wait (a read before the producer wrote, or a slot overwritten before
+its last reader read it) shows up as a wrong value under some policy. The
+product never calls this.
 """
 
 from __future__ import annotations
@@ -15,101 +19,161 @@ import numpy as np
 
 from oracle import m31
 
-OPS = ("END", "CONST", "VAR", "ADD", "SUB", "MUL", "NEG", "DIV", "HASH", "ACC_MUL", "ACC_MAC",
-       "ACC_LD", "ACC_ADD", "ACC_ST", "CHK", "DEN", "ACC_MACF", "INV", "ACC_MUL2", "ACC_MAC2",
-       "BAR")
+OPS = ("END", "DOT", "SUM", "SUB", "NEG", "HASH", "INV", "VAR", "CONST", "CHK", "DEN",
+       "FILL", "SPILL", "WAIT", "SIGNAL")
 FN = ("EXP", "RSQRT", "SIGMOID")
+SLOT = 128
+GROUP = 8
 
 
-def streams(code: np.ndarray, n_warps: int) -> list[list[list[tuple]]]:
-    """Split a cooperative program into per-warp lists of phases."""
+def fields(op: str, k: int) -> int:
+    return {"DOT": 1 + 2 * k, "SUM": 1 + k, "SUB": 3, "CHK": 3, "NEG": 2, "HASH": 2, "INV": 2,
+            "VAR": 2, "CONST": 2, "FILL": 2, "SPILL": 2, "DEN": 1}.get(op, 0)
+
+
+def decode(code: np.ndarray, n_warps: int) -> list[list[tuple]]:
+    """Per warp: list of (op, fn, k, aux, signal, cols) where cols[f] is the u32
+    array of field f over the bundle's n ops and signal the progress published
+    after the bundle (header.w; for WAIT: the progress waited for)."""
     flat = code.reshape(-1)
-    table = [int(x) for x in flat[:n_warps]]
     out = []
     for w in range(n_warps):
-        pc = table[w]
-        phases, cur = [], []
+        pc = int(flat[w])
+        ins = []
         while True:
-            op, d, a, b = (int(x) for x in code[pc])
+            h = code[pc]
             pc += 1
-            if OPS[op] in ("BAR", "END"):
-                phases.append(cur)
-                cur = []
-                if OPS[op] == "END":
-                    break
-                continue
-            cur.append((op, d, a, b))
-        out.append(phases)
+            op = OPS[int(h[0]) & 0xFF]
+            fn = (int(h[0]) >> 8) & 0xFF
+            k = int(h[0]) >> 16
+            n = int(h[1])
+            aux = int(h[2])
+            sig = int(h[3])
+            nf = fields(op, k)
+            ng = (n + GROUP - 1) // GROUP
+            cols = [np.zeros(ng * GROUP, dtype=np.int64) for _ in range(nf)]
+            for g in range(ng):
+                for f in range(nf):
+                    rec = code[pc:pc + 2].reshape(-1)
+                    cols[f][g * GROUP:(g + 1) * GROUP] = rec
+                    pc += 2
+            cols = [c[:n] for c in cols]
+            ins.append((op, fn, k, aux, sig, cols))
+            if op == "END":
+                break
+        out.append(ins)
     return out
 
 
 def run(code: np.ndarray, n_slots: int, var_keys: np.ndarray, var_base: int, seed: int,
-        witnesses: np.ndarray, n_warps: int = 8, reverse: bool = False):
+        witnesses: np.ndarray, n_warps: int = 16, policy: str = "random", rng_seed: int = 0,
+        n_spill: int = 64):
     """Returns (valid mask [W], first bad obligation per witness [W] or -1)."""
     W = len(witnesses)
-    slots = np.zeros((max(n_slots, 1), W), dtype=np.uint64)
+    sm = np.zeros((max(n_slots, 1), W), dtype=np.uint64)
+    gm = np.zeros((max(n_spill, 1), W), dtype=np.uint64)
     valid = np.ones(W, dtype=bool)
     bad = np.full(W, -1, dtype=np.int64)
     w1 = np.asarray(witnesses, dtype=np.uint64) + np.uint64(1)
-    per_warp = streams(code, n_warps)
-    n_phases = len(per_warp[0])
-    assert all(len(s) == n_phases for s in per_warp), "warps disagree on the phase count"
-    order = list(range(n_warps))[::-1] if reverse else list(range(n_warps))
-    for ph in range(n_phases):
-        for w in order:
-            acc = None
-            for op, dst, a, b in per_warp[w][ph]:
-                name = OPS[op]
-                if name == "CONST":
-                    slots[dst] = a
-                elif name == "VAR":
-                    key = np.uint64(var_keys[a])  # VAR operands are stage-relative
-                    with np.errstate(over="ignore"):
-                        slots[dst] = m31.to_field(m31.mix64(key + w1 * m31.GOLDEN))
-                elif name == "ADD":
-                    slots[dst] = m31.add(slots[a], slots[b])
-                elif name == "SUB":
-                    slots[dst] = m31.sub(slots[a], slots[b])
-                elif name == "MUL":
-                    slots[dst] = m31.mul(slots[a], slots[b])
-                elif name == "NEG":
-                    slots[dst] = (m31.P - slots[a]) % m31.P
-                elif name == "DIV":
-                    slots[dst] = m31.mul(slots[a], m31.inv(slots[b]))
-                elif name == "INV":
-                    slots[dst] = m31.inv(slots[a])
-                elif name == "HASH":
-                    slots[dst] = m31.uf(seed, FN[b], slots[a])
-                elif name == "ACC_LD":
-                    acc = slots[a].astype(object)
-                elif name == "ACC_ADD":
-                    acc = acc + slots[a].astype(object)
-                elif name == "ACC_MUL":
-                    acc = slots[a].astype(object) * slots[b].astype(object)
-                elif name in ("ACC_MAC", "ACC_MACF"):
-                    if name == "ACC_MACF":
-                        acc = np.array([(int(v) & m31.PI) + (int(v) >> 31) for v in acc], dtype=object)
-                    acc = acc + slots[a].astype(object) * slots[b].astype(object)
-                    assert all(int(v) < (1 << 64) for v in acc), "accumulator overflow"
-                elif name == "ACC_MUL2":
-                    c, d = dst & 0xFFFF, dst >> 16
-                    acc = slots[a].astype(object) * slots[b].astype(object) + \
-                        slots[c].astype(object) * slots[d].astype(object)
-                    assert all(int(v) < (1 << 64) for v in acc), "accumulator overflow"
-                elif name == "ACC_MAC2":
-                    c, d = dst & 0xFFFF, dst >> 16
-                    acc = np.array([(int(v) & m31.PI) + (int(v) >> 31) for v in acc], dtype=object)
-                    acc = acc + slots[a].astype(object) * slots[b].astype(object) + \
-                        slots[c].astype(object) * slots[d].astype(object)
-                    assert all(int(v) < (1 << 64) for v in acc), "accumulator overflow"
-                elif name == "ACC_ST":
-                    slots[dst] = np.array([int(v) % m31.PI for v in acc], dtype=np.uint64)
-                elif name == "CHK":
-                    diff = slots[a] != slots[b]
-                    upd = diff & ((bad < 0) | (bad > dst))
-                    bad[upd] = dst
-                elif name == "DEN":
-                    valid &= slots[a] != 0
-                else:
-                    raise ValueError(name)
+    streams = decode(code, n_warps)
+    pc = [0] * n_warps
+    prog = [0] * n_warps
+    rng = np.random.default_rng(rng_seed)
+    P = np.uint64(m31.PI)
+
+    def s(off):
+        assert off % SLOT == 0
+        return int(off) // SLOT
+
+    def runnable(w):
+        op, fn, k, aux, sig, cols = streams[w][pc[w]]
+        if op == "END":
+            return False
+        if op == "WAIT":
+            return prog[aux] >= sig
+        return True
+
+    def step(w):
+        nonlocal valid
+        op, fn, k, aux, sig, cols = streams[w][pc[w]]
+        pc[w] += 1
+        n = len(cols[0]) if cols else 0
+        if op == "DOT":
+            for i in range(n):
+                acc = np.zeros(W, dtype=np.uint64)
+                for j in range(k):
+                    acc = (acc + sm[s(cols[1 + 2 * j][i])] * sm[s(cols[2 + 2 * j][i])] % P) % P
+                sm[s(cols[0][i])] = acc
+        elif op == "SUM":
+            for i in range(n):
+                acc = np.zeros(W, dtype=np.uint64)
+                for j in range(k):
+                    acc = (acc + sm[s(cols[1 + j][i])]) % P
+                sm[s(cols[0][i])] = acc
+        elif op == "SUB":
+            for i in range(n):
+                sm[s(cols[0][i])] = m31.sub(sm[s(cols[1][i])], sm[s(cols[2][i])])
+        elif op == "NEG":
+            for i in range(n):
+                sm[s(cols[0][i])] = (P - sm[s(cols[1][i])]) % P
+        elif op == "HASH":
+            for i in range(n):
+                sm[s(cols[0][i])] = m31.uf(seed, FN[fn], sm[s(cols[1][i])])
+        elif op == "INV":
+            # Montgomery batch inversion, exactly as the device does it
+            acc = np.ones(W, dtype=np.uint64)
+            for i in range(n):
+                acc = acc * sm[s(cols[1][i])] % P
+                sm[s(cols[0][i])] = acc
+            inv = m31.inv(acc)
+            for i in range(n - 1, 0, -1):
+                prev = sm[s(cols[0][i - 1])].copy()
+                a = sm[s(cols[1][i])].copy()
+                sm[s(cols[0][i])] = inv * prev % P
+                inv = inv * a % P
+            if n:
+                sm[s(cols[0][0])] = inv
+        elif op == "VAR":
+            for i in range(n):
+                key = np.uint64(var_keys[int(cols[1][i])])  # stage-relative
+                with np.errstate(over="ignore"):
+                    sm[s(cols[0][i])] = m31.to_field(m31.mix64(key + w1 * m31.GOLDEN))
+        elif op == "CONST":
+            for i in range(n):
+                sm[s(cols[0][i])] = np.uint64(int(cols[1][i]))
+        elif op == "CHK":
+            for i in range(n):
+                diff = sm[s(cols[1][i])] != sm[s(cols[2][i])]
+                o = int(cols[0][i])
+                upd = diff & ((bad < 0) | (bad > o))
+                bad[upd] = o
+        elif op == "DEN":
+            for i in range(n):
+                valid &= sm[s(cols[0][i])] != 0
+        elif op == "FILL":
+            for i in range(n):
+                sm[s(cols[0][i])] = gm[s(cols[1][i])]
+        elif op == "SPILL":
+            for i in range(n):
+                gm[s(cols[0][i])] = sm[s(cols[1][i])]
+        elif op == "WAIT":
+            return
+        else:
+            raise ValueError(op)
+        if sig:
+            assert sig >= prog[w], "progress must be monotone"
+            prog[w] = sig
+
+    while True:
+        live = [w for w in range(n_warps) if runnable(w)]
+        if not live:
+            assert all(streams[w][pc[w]][0] == "END" for w in range(n_warps)), "deadlock"
+            break
+        if policy == "random":
+            w = int(rng.choice(live))
+        elif policy == "ahead":
+            w = live[0]
+        else:
+            w = live[-1]
+        step(w)
     return valid, bad

@@ -35,7 +35,10 @@ def test_bytecode_matches_oracle(lib, rec):
         o = check_stage(plan, st, owner, seed, wit)
         if c.status == STAGE_OK:
             code, ns = eng.bytecode(c.index)
-            valid, bad = bytecode_emu.run(code, ns, lw.var_keys, base, seed, wit)
+            policy = ("random", "ahead", "behind")[c.index % 3]
+            valid, bad = bytecode_emu.run(code, ns, lw.var_keys, base, seed, wit,
+                                          n_warps=16, policy=policy, rng_seed=c.index,
+                                          n_spill=c.spill_slots)
             assert int(valid.sum()) == o.valid, st.target
             emu_bad = (bad >= 0) & valid
             want = o.bad_mask.any(axis=0) if o.bad_mask is not None else np.zeros(W, bool)
@@ -48,4 +51,42 @@ def test_bytecode_matches_oracle(lib, rec):
         elif c.status == STAGE_REFUTED_CONST:
             assert o.status == "refuted", st.target
         base += lw.var_keys.size
+    eng.close()
+
+
+SPILL_PICK = [r for r in RECS if r["meta"]["source"] != "random_plan"][:4]
+
+
+@pytest.mark.parametrize("warps,slots", [(8, 48), (16, 64)])
+@pytest.mark.parametrize("rec", SPILL_PICK, ids=[r["name"] for r in SPILL_PICK])
+def test_small_value_file_spills_correctly(lib, rec, warps, slots, monkeypatch):
+    """A tiny shared value file forces the allocator to keep values in global
+    memory (FILL/SPILL) and the warps to synchronise on spill slots too."""
+    monkeypatch.setenv("PQW_FAST_SLOTS", str(slots))
+    monkeypatch.setenv("PQW_WARPS", str(warps))
+    seed, W = 7, 4
+    plan = load_plan(rec["work_plan"])
+    stages, _ = build_stages(plan)
+    owner = shard_owner(plan, entry_order(plan))
+    eng = Engine(0, seed, F.fn_keys(seed))
+    wit = np.arange(W, dtype=np.uint64)
+    spilled = 0
+    for st in stages:
+        lw = lower_stage(plan, st, owner, seed)
+        c = eng.add_stage(lw.ir, lw.consts, lw.var_keys)
+        if c.status != STAGE_OK:
+            continue
+        assert c.slots <= slots
+        spilled += c.spill_slots > 0
+        o = check_stage(plan, st, owner, seed, wit)
+        code, ns = eng.bytecode(c.index)
+        for policy in ("ahead", "behind", "random"):
+            valid, bad = bytecode_emu.run(code, ns, lw.var_keys, 0, seed, wit, n_warps=warps,
+                                          policy=policy, rng_seed=c.index,
+                                          n_spill=c.spill_slots)
+            assert int(valid.sum()) == o.valid, (st.target, policy)
+            emu_bad = (bad >= 0) & valid
+            want = o.bad_mask.any(axis=0) if o.bad_mask is not None else np.zeros(W, bool)
+            assert np.array_equal(emu_bad, want), (st.target, policy)
+    assert spilled, "expected at least one stage to spill"
     eng.close()
