@@ -87,20 +87,51 @@ __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
                : "memory");
 }
 
-__device__ __forceinline__ uint32_t lds(const uint8_t* sl, uint32_t off) {
-  return *reinterpret_cast<const uint32_t*>(sl + off);
+// Shared value-file access through 32-bit shared-window addresses: sb is this
+// lane's base (file start + 4 * lane), off a compiler-prepared slot offset.
+// volatile keeps the accesses in program order across bundles.
+__device__ __forceinline__ uint32_t lds(uint32_t sb, uint32_t off) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(sb + off));
+  return v;
 }
-__device__ __forceinline__ void sts(uint8_t* sl, uint32_t off, uint32_t v) {
-  *reinterpret_cast<uint32_t*>(sl + off) = v;
+__device__ __forceinline__ void sts(uint32_t sb, uint32_t off, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(sb + off), "r"(v));
 }
 
 // acc (< 2^64) -> [0, P)
 __device__ __forceinline__ uint32_t red64(uint64_t x) { return fred64(x); }
 
+// Elementwise bundle: per group of 8, load the fields' operands, compute, store.
+// Groups are full (the compiler pads the last one with copies of the last op).
+template <int NA, typename Fn>
+__device__ __forceinline__ const uint4* run_elementwise(const uint4* pc, uint32_t n, uint32_t sb,
+                                                        Fn f) {
+  for (uint32_t g = 0; g < n; g += 8, pc += 2 * (NA + 1)) {
+    const F8 D = ld8(pc);
+    F8 A[NA];
+#pragma unroll
+    for (int j = 0; j < NA; ++j) A[j] = ld8(pc + 2 + 2 * j);
+    uint32_t a[NA][8];
+#pragma unroll
+    for (int j = 0; j < NA; ++j)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[j][i] = lds(sb, A[j].v[i]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      uint32_t x[NA];
+#pragma unroll
+      for (int j = 0; j < NA; ++j) x[j] = a[j][i];
+      sts(sb, D.v[i], f(x));
+    }
+  }
+  return pc;
+}
+
 // Runs this warp's stream of the stage program for witness w = tile*32 + lane,
 // folding the lane's definedness and first failing obligation into valid/bad.
 template <bool PROBE>
-__device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd, uint8_t* sl,
+__device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd, uint32_t sb,
                                            uint8_t* gl, uint32_t* prog, uint32_t w,
                                            bool& valid, uint32_t& bad) {
   const uint32_t lane = threadIdx.x & 31u;
@@ -119,19 +150,11 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
       case I_DOT: {
         const uint32_t k = h.x >> 16;
         if (k == 1) {
-          for (uint32_t g = 0; g < n; g += 8, pc += 6) {
-            const F8 D = ld8(pc), A = ld8(pc + 2), B = ld8(pc + 4);
-            uint32_t a[8], b[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              if (g + i < n) {
-                a[i] = lds(sl, A.v[i]);
-                b[i] = lds(sl, B.v[i]);
-              }
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              if (g + i < n) sts(sl, D.v[i], fmul(a[i], b[i]));
-          }
+          pc = run_elementwise<2>(pc, n, sb, [](const uint32_t* x) { return fmul(x[0], x[1]); });
+        } else if (k == 2) {
+          pc = run_elementwise<4>(pc, n, sb, [](const uint32_t* x) {
+            return red64((uint64_t)x[0] * x[1] + (uint64_t)x[2] * x[3]);
+          });
         } else {
           for (uint32_t g = 0; g < n; g += 8) {
             const F8 D = ld8(pc);
@@ -143,23 +166,20 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
               const F8 A = ld8(pc), B = ld8(pc + 2);
               uint32_t a[8], b[8];
 #pragma unroll
-              for (int i = 0; i < 8; ++i)
-                if (g + i < n) {
-                  a[i] = lds(sl, A.v[i]);
-                  b[i] = lds(sl, B.v[i]);
-                }
+              for (int i = 0; i < 8; ++i) {
+                a[i] = lds(sb, A.v[i]);
+                b[i] = lds(sb, B.v[i]);
+              }
               // products < 2^62: fold (to < 2^34) before every third one
               const bool fold = (j % 3u) == 2u;
 #pragma unroll
-              for (int i = 0; i < 8; ++i)
-                if (g + i < n) {
-                  uint64_t t = fold ? ffold64(acc[i]) : acc[i];
-                  acc[i] = t + (uint64_t)a[i] * b[i];
-                }
+              for (int i = 0; i < 8; ++i) {
+                const uint64_t t = fold ? ffold64(acc[i]) : acc[i];
+                acc[i] = t + (uint64_t)a[i] * b[i];
+              }
             }
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
-              if (g + i < n) sts(sl, D.v[i], red64(acc[i]));
+            for (int i = 0; i < 8; ++i) sts(sb, D.v[i], red64(acc[i]));
           }
         }
         break;
@@ -167,19 +187,7 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
       case I_SUM: {
         const uint32_t k = h.x >> 16;
         if (k == 2) {
-          for (uint32_t g = 0; g < n; g += 8, pc += 6) {
-            const F8 D = ld8(pc), A = ld8(pc + 2), B = ld8(pc + 4);
-            uint32_t a[8], b[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              if (g + i < n) {
-                a[i] = lds(sl, A.v[i]);
-                b[i] = lds(sl, B.v[i]);
-              }
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              if (g + i < n) sts(sl, D.v[i], fadd(a[i], b[i]));
-          }
+          pc = run_elementwise<2>(pc, n, sb, [](const uint32_t* x) { return fadd(x[0], x[1]); });
         } else {
           for (uint32_t g = 0; g < n; g += 8) {
             const F8 D = ld8(pc);
@@ -190,55 +198,23 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
             for (uint32_t j = 0; j < k; ++j, pc += 2) {
               const F8 A = ld8(pc);
 #pragma unroll
-              for (int i = 0; i < 8; ++i)
-                if (g + i < n) acc[i] += lds(sl, A.v[i]);
+              for (int i = 0; i < 8; ++i) acc[i] += lds(sb, A.v[i]);
             }
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
-              if (g + i < n) sts(sl, D.v[i], red64(acc[i]));
+            for (int i = 0; i < 8; ++i) sts(sb, D.v[i], red64(acc[i]));
           }
         }
         break;
       }
       case I_SUB:
-        for (uint32_t g = 0; g < n; g += 8, pc += 6) {
-          const F8 D = ld8(pc), A = ld8(pc + 2), B = ld8(pc + 4);
-          uint32_t a[8], b[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            if (g + i < n) {
-              a[i] = lds(sl, A.v[i]);
-              b[i] = lds(sl, B.v[i]);
-            }
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            if (g + i < n) sts(sl, D.v[i], fsub(a[i], b[i]));
-        }
+        pc = run_elementwise<2>(pc, n, sb, [](const uint32_t* x) { return fsub(x[0], x[1]); });
         break;
       case I_NEG:
-        for (uint32_t g = 0; g < n; g += 8, pc += 4) {
-          const F8 D = ld8(pc), A = ld8(pc + 2);
-          uint32_t a[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            if (g + i < n) a[i] = lds(sl, A.v[i]);
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            if (g + i < n) sts(sl, D.v[i], fneg(a[i]));
-        }
+        pc = run_elementwise<1>(pc, n, sb, [](const uint32_t* x) { return fneg(x[0]); });
         break;
       case I_HASH: {
         const uint64_t key = __ldg(p.fn_keys + ((h.x >> 8) & 0xFFu));
-        for (uint32_t g = 0; g < n; g += 8, pc += 4) {
-          const F8 D = ld8(pc), A = ld8(pc + 2);
-          uint32_t a[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            if (g + i < n) a[i] = lds(sl, A.v[i]);
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            if (g + i < n) sts(sl, D.v[i], uf_apply(key, a[i]));
-        }
+        pc = run_elementwise<1>(pc, n, sb, [key](const uint32_t* x) { return uf_apply(key, x[0]); });
         break;
       }
       case I_INV: {
@@ -254,24 +230,25 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
 #pragma unroll
           for (int i = 0; i < 8; ++i)
             if (g + i < n) {
-              acc = fmul(acc, lds(sl, A.v[i]));
-              sts(sl, D.v[i], acc);
+              acc = fmul(acc, lds(sb, A.v[i]));
+              sts(sb, D.v[i], acc);
             }
         }
         uint32_t inv = finv(acc);
         for (int32_t gi = (int32_t)ng - 1; gi >= 0; --gi) {
           const uint32_t g = (uint32_t)gi * 8u;
           const F8 D = ld8(base + 4 * gi), A = ld8(base + 4 * gi + 2);
-          const F8 Dp = gi > 0 ? ld8(base + 4 * (gi - 1)) : D;
+          const uint32_t dprev = gi > 0 ? __ldg(reinterpret_cast<const uint32_t*>(base + 4 * gi - 3) + 3)
+                                        : 0u;  // D.v[7] of the previous group
 #pragma unroll
           for (int i = 7; i >= 0; --i)
             if (g + i < n) {
               if (g + i == 0) {
-                sts(sl, D.v[i], inv);
+                sts(sb, D.v[i], inv);
               } else {
-                const uint32_t prev = lds(sl, i > 0 ? D.v[i > 0 ? i - 1 : 0] : Dp.v[7]);  // prefix m-1
-                const uint32_t a = lds(sl, A.v[i]);
-                sts(sl, D.v[i], fmul(inv, prev));
+                const uint32_t prev = lds(sb, i > 0 ? D.v[i > 0 ? i - 1 : 0] : dprev);
+                const uint32_t a = lds(sb, A.v[i]);
+                sts(sb, D.v[i], fmul(inv, prev));
                 inv = fmul(inv, a);
               }
             }
@@ -282,43 +259,41 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
         for (uint32_t g = 0; g < n; g += 8, pc += 4) {
           const F8 D = ld8(pc), V = ld8(pc + 2);
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            if (g + i < n) {
-              const uint32_t v = witness_value(__ldg(vkeys + V.v[i]), w);
-              if (PROBE && w == p.probe_w) p.probe_vars[V.v[i]] = v;
-              sts(sl, D.v[i], v);
-            }
+          for (int i = 0; i < 8; ++i) {
+            const uint32_t v = witness_value(__ldg(vkeys + V.v[i]), w);
+            if (PROBE && w == p.probe_w) p.probe_vars[V.v[i]] = v;
+            sts(sb, D.v[i], v);
+          }
         }
         break;
       case I_CONST:
         for (uint32_t g = 0; g < n; g += 8, pc += 4) {
           const F8 D = ld8(pc), C = ld8(pc + 2);
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            if (g + i < n) sts(sl, D.v[i], C.v[i]);
+          for (int i = 0; i < 8; ++i) sts(sb, D.v[i], C.v[i]);
         }
         break;
       case I_CHK:
         for (uint32_t g = 0; g < n; g += 8, pc += 6) {
           const F8 O = ld8(pc), A = ld8(pc + 2), B = ld8(pc + 4);
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            if (g + i < n) {
-              const uint32_t a = lds(sl, A.v[i]), b = lds(sl, B.v[i]);
-              if (PROBE && O.v[i] == p.probe_obl && w == p.probe_w) {
-                p.probe_out[0] = a;
-                p.probe_out[1] = b;
-              }
-              if (a != b) bad = min(bad, O.v[i]);
+          for (int i = 0; i < 8; ++i) {
+            const uint32_t a = lds(sb, A.v[i]), b = lds(sb, B.v[i]);
+            if (PROBE && O.v[i] == p.probe_obl && w == p.probe_w) {
+              p.probe_out[0] = a;
+              p.probe_out[1] = b;
             }
+            if (a != b) bad = min(bad, O.v[i]);
+          }
         }
         break;
       case I_DEN:
         for (uint32_t g = 0; g < n; g += 8, pc += 2) {
           const F8 A = ld8(pc);
+          uint32_t z = 1;
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            if (g + i < n && lds(sl, A.v[i]) == 0) valid = false;
+          for (int i = 0; i < 8; ++i) z &= lds(sb, A.v[i]) != 0;
+          if (!z) valid = false;
         }
         break;
       case I_FILL:
@@ -326,11 +301,9 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
           const F8 D = ld8(pc), G = ld8(pc + 2);
           uint32_t a[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            if (g + i < n) a[i] = *reinterpret_cast<const uint32_t*>(gl + G.v[i]);
+          for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const volatile uint32_t*>(gl + G.v[i]);
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            if (g + i < n) sts(sl, D.v[i], a[i]);
+          for (int i = 0; i < 8; ++i) sts(sb, D.v[i], a[i]);
         }
         break;
       case I_SPILL:
@@ -338,7 +311,7 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
           const F8 G = ld8(pc), A = ld8(pc + 2);
 #pragma unroll
           for (int i = 0; i < 8; ++i)
-            if (g + i < n) *reinterpret_cast<uint32_t*>(gl + G.v[i]) = lds(sl, A.v[i]);
+            *reinterpret_cast<volatile uint32_t*>(gl + G.v[i]) = lds(sb, A.v[i]);
         }
         break;
       case I_WAIT: {
@@ -373,7 +346,7 @@ __global__ void __launch_bounds__(32 * NW) eval_kernel(Params p) {
   __shared__ uint32_t s_prog[MAX_NW];  // per-warp progress counters
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t warp = threadIdx.x >> 5;
-  uint8_t* sl = sfile + lane * 4u;
+  const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sfile) + lane * 4u;
   uint8_t* gl = reinterpret_cast<uint8_t*>(p.scratch + (size_t)blockIdx.x * p.spill_slots * 32u) +
                 lane * 4u;
   for (;;) {
@@ -390,7 +363,7 @@ __global__ void __launch_bounds__(32 * NW) eval_kernel(Params p) {
     const uint32_t w = tile * 32u + lane;
     bool valid = PROBE ? (w == p.probe_w) : (w < p.n_witness);
     uint32_t bad = 0xFFFFFFFFu;
-    run_stream<PROBE>(p, sd, sl, gl, s_prog, w, valid, bad);
+    run_stream<PROBE>(p, sd, sb, gl, s_prog, w, valid, bad);
     // merge the warps' verdicts for each lane
     const uint32_t inval = __ballot_sync(0xFFFFFFFFu, !valid);
     if (lane == 0 && inval) atomicOr(&s_invalid, inval);

@@ -424,10 +424,17 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
                             const std::vector<uint32_t>& f, uint32_t nf) {
         // f: nf fields per op, op-major (f[i * nf + j])
         code.push_back(pqw_ins{isa_header(op, fn, k), n, aux, 0});
+        // the last group is padded with copies of the bundle's last op (a
+        // repeated op rewrites the same value, a repeated check re-checks), so
+        // the device runs whole groups without per-op predicates; INV (whose
+        // destinations hold running products) is the one op that counts
         for (uint32_t g = 0; g < n; g += GROUP)
           for (uint32_t j = 0; j < nf; ++j) {
             uint32_t v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            for (uint32_t i = 0; i < GROUP && g + i < n; ++i) v[i] = f[(size_t)(g + i) * nf + j];
+            for (uint32_t i = 0; i < GROUP; ++i) {
+              const uint32_t src = g + i < n ? g + i : n - 1;
+              if (g + i < n || op != I_INV) v[i] = f[(size_t)src * nf + j];
+            }
             code.push_back(pqw_ins{v[0], v[1], v[2], v[3]});
             code.push_back(pqw_ins{v[4], v[5], v[6], v[7]});
           }

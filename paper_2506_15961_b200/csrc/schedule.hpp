@@ -33,7 +33,7 @@ struct SchedOptions {
   uint32_t smem_slots = 1760;  // shared-memory value file capacity (slots)
   uint32_t window = 0;         // look-ahead in units past the lowest unscheduled one (0: adaptive)
   uint32_t bmax = 32;          // max ops per bundle
-  uint32_t xlat = 24;          // cost-model penalty of a cross-warp dependence
+  uint32_t xlat = 64;          // cost-model penalty of a cross-warp dependence
   uint32_t active_warps = 32;  // warps that receive work (the rest run empty streams)
 };
 
