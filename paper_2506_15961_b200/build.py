@@ -28,7 +28,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     nvcc = os.environ.get("NVCC", "nvcc")
     cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
            "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v",
-           "-diag-suppress", "128", "-o", OUT + ".tmp"] + [os.path.join(CSRC, s) for s in SOURCES]
+           "-diag-suppress", "128", "-o", OUT + ".tmp"] + os.environ.get("PQW_NVCC_FLAGS", "").split() + \
+        [os.path.join(CSRC, s) for s in SOURCES]
     r = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

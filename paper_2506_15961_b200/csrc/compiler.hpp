@@ -48,8 +48,9 @@ CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* con
                             const SchedOptions& sched);
 
 // Defaults (overridable per engine: PQW_FAST_SLOTS, PQW_WARPS, PQW_WINDOW,
-// PQW_BMAX, PQW_XLAT env vars): 1760 slots = 220 KB of shared memory.
-constexpr uint32_t DEFAULT_FAST_SLOTS = 1760;
+// PQW_BMAX, PQW_XLAT env vars): 1680 slots = 210 KB of shared memory, which
+// leaves room for the per-warp code rings (16 x 1 KB).
+constexpr uint32_t DEFAULT_FAST_SLOTS = 1680;
 constexpr uint32_t DEFAULT_WARPS = 16;
 
 // Variables (stage-relative indices) in the cone of obligation `obl`.

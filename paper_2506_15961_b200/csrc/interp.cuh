@@ -57,11 +57,13 @@ struct Params {
   uint32_t tiles;            // work items per stage
   uint32_t n_witness;
   uint32_t spill_slots;      // per-CTA spill capacity in slots
+  uint32_t file_bytes;       // shared value file size (the code rings follow it)
   // probe mode
   uint32_t probe_w;
   uint32_t probe_obl;
   uint32_t* probe_out;       // [lhs, rhs]
   uint32_t* probe_vars;
+  unsigned long long* prof;  // PQW_PROF builds: [item cycles, wait cycles, barrier cycles, bundles]
 };
 
 struct F8 {
@@ -102,16 +104,73 @@ __device__ __forceinline__ void sts(uint32_t sb, uint32_t off, uint32_t v) {
 // acc (< 2^64) -> [0, P)
 __device__ __forceinline__ uint32_t red64(uint64_t x) { return fred64(x); }
 
+// Instruction-stream staging. Each warp streams its instructions through a
+// 1 KB ring in shared memory (two chunks of 32 records): lane l copies record
+// l of a chunk with cp.async, one chunk of look-ahead is always in flight, so
+// decode reads LDS.128 broadcasts instead of waiting out an L2 round trip per
+// group. Every read unit (a header, one payload group, or one pair/term of a
+// wide DOT/SUM) is at most 33 records, so it spans at most two chunks.
+constexpr uint32_t RING_RECS = 64;
+constexpr uint32_t RING_BYTES = RING_RECS * 16;
+
+struct CodeRing {
+  const uint4* src;   // global start of this warp's stream
+  uint32_t base;      // shared address of this warp's ring
+  uint32_t lane4;     // lane * 16
+  uint32_t issued;    // chunks requested
+  uint32_t ready;     // chunks known landed (and synced across the warp)
+
+  __device__ __forceinline__ void issue() {
+    const uint32_t r = issued * 32u;
+    const uint32_t dst = base + ((r & (RING_RECS - 1)) << 4) + lane4;
+    const char* g = reinterpret_cast<const char*>(src + r) + lane4;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n\tcp.async.commit_group;" ::"r"(dst),
+                 "l"(g)
+                 : "memory");
+    ++issued;
+  }
+  // make records [p, p + r) resident (r <= 33)
+  __device__ __forceinline__ void ensure(uint32_t p, uint32_t r) {
+    const uint32_t c0 = p >> 5, c1 = (p + r - 1) >> 5;
+    if (issued <= c0 + 1) issue();  // look-ahead: the slot of chunk c0+1 held c0-1
+    if (c1 >= ready) {
+      while (issued <= c1) issue();
+      if (issued - 1 - c1 >= 1)
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      else
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      __syncwarp();
+      ready = c1 + 1;
+    }
+  }
+  __device__ __forceinline__ uint4 rec(uint32_t p) const {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(base + ((p & (RING_RECS - 1)) << 4)));
+    return v;
+  }
+  __device__ __forceinline__ F8 rd8(uint32_t p) const {
+    const uint4 a = rec(p), b = rec(p + 1);
+    return F8{{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}};
+  }
+  __device__ __forceinline__ void drain() {
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+  }
+};
+
 // Elementwise bundle: per group of 8, load the fields' operands, compute, store.
 // Groups are full (the compiler pads the last one with copies of the last op).
 template <int NA, typename Fn>
-__device__ __forceinline__ const uint4* run_elementwise(const uint4* pc, uint32_t n, uint32_t sb,
-                                                        Fn f) {
+__device__ __forceinline__ uint32_t run_elementwise(CodeRing& cr, uint32_t pc, uint32_t n,
+                                                    uint32_t sb, Fn f) {
   for (uint32_t g = 0; g < n; g += 8, pc += 2 * (NA + 1)) {
-    const F8 D = ld8(pc);
+    cr.ensure(pc, 2 * (NA + 1));
+    const F8 D = cr.rd8(pc);
     F8 A[NA];
 #pragma unroll
-    for (int j = 0; j < NA; ++j) A[j] = ld8(pc + 2 + 2 * j);
+    for (int j = 0; j < NA; ++j) A[j] = cr.rd8(pc + 2 + 2 * j);
     uint32_t a[NA][8];
 #pragma unroll
     for (int j = 0; j < NA; ++j)
@@ -132,38 +191,44 @@ __device__ __forceinline__ const uint4* run_elementwise(const uint4* pc, uint32_
 // folding the lane's definedness and first failing obligation into valid/bad.
 template <bool PROBE>
 __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd, uint32_t sb,
-                                           uint8_t* gl, uint32_t* prog, uint32_t w,
-                                           bool& valid, uint32_t& bad) {
+                                           uint32_t ring, uint8_t* gl, uint32_t* prog,
+                                           uint32_t w, bool& valid, uint32_t& bad) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t warp = threadIdx.x >> 5;
   const uint4* code = p.code + sd.code_off;
-  const uint4* pc = code + __ldg(reinterpret_cast<const uint32_t*>(code) + warp);
+  const uint4* stream = code + __ldg(reinterpret_cast<const uint32_t*>(code) + warp);
   const uint64_t* vkeys = p.var_keys + sd.var_base;
+  CodeRing cr{stream, ring, lane * 16u, 0u, 0u};
+  uint32_t pc = 0;  // record position in the stream
   for (;;) {
-    const uint4 h = __ldg(pc);
+    cr.ensure(pc, 1);
+    const uint4 h = cr.rec(pc);
     ++pc;
     const uint32_t op = h.x & 0xFFu;
     const uint32_t n = h.y;
     switch (op) {
       case I_END:
+        cr.drain();  // no copy may land in the ring after this item
         return;
       case I_DOT: {
         const uint32_t k = h.x >> 16;
         if (k == 1) {
-          pc = run_elementwise<2>(pc, n, sb, [](const uint32_t* x) { return fmul(x[0], x[1]); });
+          pc = run_elementwise<2>(cr, pc, n, sb, [](const uint32_t* x) { return fmul(x[0], x[1]); });
         } else if (k == 2) {
-          pc = run_elementwise<4>(pc, n, sb, [](const uint32_t* x) {
+          pc = run_elementwise<4>(cr, pc, n, sb, [](const uint32_t* x) {
             return red64((uint64_t)x[0] * x[1] + (uint64_t)x[2] * x[3]);
           });
         } else {
           for (uint32_t g = 0; g < n; g += 8) {
-            const F8 D = ld8(pc);
+            cr.ensure(pc, 2);
+            const F8 D = cr.rd8(pc);
             pc += 2;
             uint64_t acc[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) acc[i] = 0;
             for (uint32_t j = 0; j < k; ++j, pc += 4) {
-              const F8 A = ld8(pc), B = ld8(pc + 2);
+              cr.ensure(pc, 4);
+              const F8 A = cr.rd8(pc), B = cr.rd8(pc + 2);
               uint32_t a[8], b[8];
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
@@ -187,16 +252,18 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
       case I_SUM: {
         const uint32_t k = h.x >> 16;
         if (k == 2) {
-          pc = run_elementwise<2>(pc, n, sb, [](const uint32_t* x) { return fadd(x[0], x[1]); });
+          pc = run_elementwise<2>(cr, pc, n, sb, [](const uint32_t* x) { return fadd(x[0], x[1]); });
         } else {
           for (uint32_t g = 0; g < n; g += 8) {
-            const F8 D = ld8(pc);
+            cr.ensure(pc, 2);
+            const F8 D = cr.rd8(pc);
             pc += 2;
             uint64_t acc[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) acc[i] = 0;
             for (uint32_t j = 0; j < k; ++j, pc += 2) {
-              const F8 A = ld8(pc);
+              cr.ensure(pc, 2);
+              const F8 A = cr.rd8(pc);
 #pragma unroll
               for (int i = 0; i < 8; ++i) acc[i] += lds(sb, A.v[i]);
             }
@@ -207,26 +274,29 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
         break;
       }
       case I_SUB:
-        pc = run_elementwise<2>(pc, n, sb, [](const uint32_t* x) { return fsub(x[0], x[1]); });
+        pc = run_elementwise<2>(cr, pc, n, sb, [](const uint32_t* x) { return fsub(x[0], x[1]); });
         break;
       case I_NEG:
-        pc = run_elementwise<1>(pc, n, sb, [](const uint32_t* x) { return fneg(x[0]); });
+        pc = run_elementwise<1>(cr, pc, n, sb, [](const uint32_t* x) { return fneg(x[0]); });
         break;
       case I_HASH: {
         const uint64_t key = __ldg(p.fn_keys + ((h.x >> 8) & 0xFFu));
-        pc = run_elementwise<1>(pc, n, sb, [key](const uint32_t* x) { return uf_apply(key, x[0]); });
+        pc = run_elementwise<1>(cr, pc, n, sb,
+                                [key](const uint32_t* x) { return uf_apply(key, x[0]); });
         break;
       }
       case I_INV: {
         // Montgomery batch inversion over the bundle: prefix products go to the
-        // destination slots, one inversion, then a backward sweep. Every operand
-        // is a guarded denominator (a DEN of the same stage), so a witness where
-        // one vanishes is invalid and its garbage never counts.
-        const uint4* base = pc;
+        // destination slots, one inversion, then a backward sweep (which reads
+        // the payload again from global memory). Every operand is a guarded
+        // denominator (a DEN of the same stage), so a witness where one
+        // vanishes is invalid and its garbage never counts.
+        const uint4* base = stream + pc;
         const uint32_t ng = (n + 7u) / 8u;
         uint32_t acc = 1;
         for (uint32_t g = 0; g < n; g += 8, pc += 4) {
-          const F8 D = ld8(pc), A = ld8(pc + 2);
+          cr.ensure(pc, 4);
+          const F8 D = cr.rd8(pc), A = cr.rd8(pc + 2);
 #pragma unroll
           for (int i = 0; i < 8; ++i)
             if (g + i < n) {
@@ -257,7 +327,8 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
       }
       case I_VAR:
         for (uint32_t g = 0; g < n; g += 8, pc += 4) {
-          const F8 D = ld8(pc), V = ld8(pc + 2);
+          cr.ensure(pc, 4);
+          const F8 D = cr.rd8(pc), V = cr.rd8(pc + 2);
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const uint32_t v = witness_value(__ldg(vkeys + V.v[i]), w);
@@ -268,14 +339,16 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
         break;
       case I_CONST:
         for (uint32_t g = 0; g < n; g += 8, pc += 4) {
-          const F8 D = ld8(pc), C = ld8(pc + 2);
+          cr.ensure(pc, 4);
+          const F8 D = cr.rd8(pc), C = cr.rd8(pc + 2);
 #pragma unroll
           for (int i = 0; i < 8; ++i) sts(sb, D.v[i], C.v[i]);
         }
         break;
       case I_CHK:
         for (uint32_t g = 0; g < n; g += 8, pc += 6) {
-          const F8 O = ld8(pc), A = ld8(pc + 2), B = ld8(pc + 4);
+          cr.ensure(pc, 6);
+          const F8 O = cr.rd8(pc), A = cr.rd8(pc + 2), B = cr.rd8(pc + 4);
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const uint32_t a = lds(sb, A.v[i]), b = lds(sb, B.v[i]);
@@ -289,7 +362,8 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
         break;
       case I_DEN:
         for (uint32_t g = 0; g < n; g += 8, pc += 2) {
-          const F8 A = ld8(pc);
+          cr.ensure(pc, 2);
+          const F8 A = cr.rd8(pc);
           uint32_t z = 1;
 #pragma unroll
           for (int i = 0; i < 8; ++i) z &= lds(sb, A.v[i]) != 0;
@@ -298,29 +372,37 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
         break;
       case I_FILL:
         for (uint32_t g = 0; g < n; g += 8, pc += 4) {
-          const F8 D = ld8(pc), G = ld8(pc + 2);
+          cr.ensure(pc, 4);
+          const F8 D = cr.rd8(pc), G = cr.rd8(pc + 2);
           uint32_t a[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const volatile uint32_t*>(gl + G.v[i]);
+          for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const uint32_t*>(gl + G.v[i]);
 #pragma unroll
           for (int i = 0; i < 8; ++i) sts(sb, D.v[i], a[i]);
         }
         break;
       case I_SPILL:
         for (uint32_t g = 0; g < n; g += 8, pc += 4) {
-          const F8 G = ld8(pc), A = ld8(pc + 2);
+          cr.ensure(pc, 4);
+          const F8 G = cr.rd8(pc), A = cr.rd8(pc + 2);
 #pragma unroll
           for (int i = 0; i < 8; ++i)
-            *reinterpret_cast<volatile uint32_t*>(gl + G.v[i]) = lds(sb, A.v[i]);
+            *reinterpret_cast<uint32_t*>(gl + G.v[i]) = lds(sb, A.v[i]);
         }
         break;
       case I_WAIT: {
         // header: z = producer warp, w = progress it must have published
         const uint32_t* flag = prog + h.z;
         if (ld_acquire(flag) < h.w) {
+#ifdef PQW_PROF
+          const long long t0 = clock64();
+#endif
           do {
             __nanosleep(32);
           } while (ld_acquire(flag) < h.w);
+#ifdef PQW_PROF
+          if (lane == 0) atomicAdd(p.prof + 1, (unsigned long long)(clock64() - t0));
+#endif
         }
         break;
       }
@@ -347,6 +429,7 @@ __global__ void __launch_bounds__(32 * NW) eval_kernel(Params p) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sfile) + lane * 4u;
+  const uint32_t ring = (uint32_t)__cvta_generic_to_shared(sfile) + p.file_bytes + warp * RING_BYTES;
   uint8_t* gl = reinterpret_cast<uint8_t*>(p.scratch + (size_t)blockIdx.x * p.spill_slots * 32u) +
                 lane * 4u;
   for (;;) {
@@ -363,7 +446,18 @@ __global__ void __launch_bounds__(32 * NW) eval_kernel(Params p) {
     const uint32_t w = tile * 32u + lane;
     bool valid = PROBE ? (w == p.probe_w) : (w < p.n_witness);
     uint32_t bad = 0xFFFFFFFFu;
-    run_stream<PROBE>(p, sd, sb, gl, s_prog, w, valid, bad);
+#ifdef PQW_PROF
+    const long long t_item = clock64();
+#endif
+    run_stream<PROBE>(p, sd, sb, ring, gl, s_prog, w, valid, bad);
+#ifdef PQW_PROF
+    const long long t_done = clock64();
+    __syncthreads();
+    if (lane == 0) {
+      atomicAdd(p.prof + 0, (unsigned long long)(clock64() - t_item));
+      atomicAdd(p.prof + 2, (unsigned long long)(clock64() - t_done));
+    }
+#endif
     // merge the warps' verdicts for each lane
     const uint32_t inval = __ballot_sync(0xFFFFFFFFu, !valid);
     if (lane == 0 && inval) atomicOr(&s_invalid, inval);

@@ -29,6 +29,12 @@
 #pragma once
 #include <stdint.h>
 
+#if defined(__CUDACC__)
+#define PQW_ISA_HD __host__ __device__
+#else
+#define PQW_ISA_HD
+#endif
+
 namespace pqw {
 
 enum IsaOp : uint32_t {
@@ -55,7 +61,7 @@ constexpr uint32_t GROUP = 8;         // ops per payload group
 constexpr uint32_t MAX_K = 64;        // max pairs of a DOT / terms of a SUM
 
 // Fields (of 8 u32 = two records) per payload group.
-inline constexpr uint32_t isa_fields(uint32_t op, uint32_t k) {
+PQW_ISA_HD inline constexpr uint32_t isa_fields(uint32_t op, uint32_t k) {
   return op == I_DOT ? 1 + 2 * k
        : op == I_SUM ? 1 + k
        : (op == I_SUB || op == I_CHK) ? 3
@@ -65,7 +71,7 @@ inline constexpr uint32_t isa_fields(uint32_t op, uint32_t k) {
        : 0;
 }
 
-inline constexpr uint32_t isa_header(uint32_t op, uint32_t fn, uint32_t k) {
+PQW_ISA_HD inline constexpr uint32_t isa_header(uint32_t op, uint32_t fn, uint32_t k) {
   return op | (fn << 8) | (k << 16);
 }
 

@@ -80,6 +80,7 @@ struct pqw_engine {
   std::vector<unsigned long long> h_first_bad;
   std::vector<uint32_t> h_valid, h_bad;
   bool results_ready = false;
+  unsigned long long* d_prof_last = nullptr;
 
   void free_device() {
     cudaFree(d_code);
@@ -138,7 +139,7 @@ int pqw_engine_create(int device, uint64_t seed, const uint64_t fn_keys[3], pqw_
       if (v >= lo && v <= hi) out = (uint32_t)v;
     }
   };
-  env("PQW_FAST_SLOTS", 16, 1780, e->fast_slots);
+  env("PQW_FAST_SLOTS", 16, 1760, e->fast_slots);
   env("PQW_WARPS", 8, 16, e->n_warps);
   if (e->n_warps != 8 && e->n_warps != 16) e->n_warps = pqw::DEFAULT_WARPS;
   env("PQW_WINDOW", 1, 1 << 20, e->sched.window);
@@ -303,6 +304,8 @@ int pqw_upload(pqw_engine* e) {
   }
   e->n_code_unique = code.size();
   if (code.empty()) code.push_back(pqw_ins{PQW_B_END, 0, 0, 0});
+  // the code rings fetch whole 32-record chunks, up to two past a stream's END
+  for (uint32_t i = 0; i < 2 * 32; ++i) code.push_back(pqw_ins{PQW_B_END, 0, 0, 0});
   if (descs.empty()) descs.push_back({0, 0, 0, 0});
   if (work.empty()) work.push_back(0);
 
@@ -312,8 +315,8 @@ int pqw_upload(pqw_engine* e) {
   // capacity the stages were compiled for); spills live in per-CTA scratch
   const size_t slot_bytes = pqw::SLOT_BYTES;
   e->smem_slots = std::max<uint32_t>(e->max_slots, 1);
-  const size_t smem_bytes = (size_t)e->smem_slots * slot_bytes;
-  if (smem_bytes + 4096 > prop.sharedMemPerBlockOptin)
+  const size_t smem_bytes = (size_t)e->smem_slots * slot_bytes + (size_t)e->n_warps * pqw::RING_BYTES;
+  if (smem_bytes + 512 > prop.sharedMemPerBlockOptin)
     return fail(PQW_EINVAL, "value file does not fit in shared memory");
   int per_sm = 0;
   if (e->n_warps == 16) {
@@ -365,7 +368,8 @@ int pqw_upload(pqw_engine* e) {
 
 static int launch_eval(pqw_engine* e, const pqw::Params& p, uint32_t grid, bool probe,
                        cudaStream_t s) {
-  const size_t smem_bytes = (size_t)e->smem_slots * pqw::SLOT_BYTES;
+  const size_t smem_bytes =
+      (size_t)e->smem_slots * pqw::SLOT_BYTES + (size_t)e->n_warps * pqw::RING_BYTES;
   if (e->n_warps == 16) {
     if (probe) pqw::eval_kernel<16, true><<<1, 16 * 32, smem_bytes, s>>>(p);
     else pqw::eval_kernel<16, false><<<grid, 16 * 32, smem_bytes, s>>>(p);
@@ -406,6 +410,14 @@ int pqw_launch(pqw_engine* e, uint32_t n_witness, void* stream) {
   p.n_items = e->n_gpu_stages * p.tiles;
   p.n_witness = n_witness;
   p.spill_slots = std::max<uint32_t>(e->spill_slots, 1);
+  p.file_bytes = e->smem_slots * pqw::SLOT_BYTES;
+#ifdef PQW_PROF
+  static unsigned long long* d_prof = nullptr;
+  if (!d_prof) CU(cudaMalloc(&d_prof, 4 * sizeof(unsigned long long)));
+  CU(cudaMemsetAsync(d_prof, 0, 4 * sizeof(unsigned long long), s));
+  p.prof = d_prof;
+  e->d_prof_last = d_prof;
+#endif
   uint32_t grid = std::min<uint32_t>(e->grid, std::max<uint32_t>(p.n_items, 1));
   CU(cudaEventRecord(e->ev0, s));
   int rc = launch_eval(e, p, grid, false, s);
@@ -433,6 +445,14 @@ int pqw_results(pqw_engine* e, uint64_t* first_bad, uint32_t* n_valid, uint32_t*
     CU(cudaMemcpy(e->h_valid.data(), e->d_n_valid, nr * sizeof(uint32_t), cudaMemcpyDeviceToHost));
     CU(cudaMemcpy(e->h_bad.data(), e->d_n_bad, nr * sizeof(uint32_t), cudaMemcpyDeviceToHost));
   }
+#ifdef PQW_PROF
+  if (e->d_prof_last) {
+    unsigned long long pr[4];
+    CU(cudaMemcpy(pr, e->d_prof_last, sizeof(pr), cudaMemcpyDeviceToHost));
+    fprintf(stderr, "PQW_PROF warp-cycles: item %.3e wait %.3e (%.1f%%) end-barrier %.3e (%.1f%%)\n",
+            (double)pr[0], (double)pr[1], 100.0 * pr[1] / pr[0], (double)pr[2], 100.0 * pr[2] / pr[0]);
+  }
+#endif
   for (size_t i = 0; i < n_stages; ++i) {
     if (first_bad) first_bad[i] = ~0ull;
     if (n_valid) n_valid[i] = 0;
@@ -477,6 +497,7 @@ int pqw_probe(pqw_engine* e, int stage, uint32_t witness, uint32_t obl, uint32_t
   p.tiles = 1;
   p.n_witness = witness + 1;
   p.spill_slots = std::max<uint32_t>(e->spill_slots, 1);
+  p.file_bytes = e->smem_slots * pqw::SLOT_BYTES;
   p.probe_w = witness;
   p.probe_obl = obl;
   p.probe_out = e->d_probe;

@@ -53,7 +53,7 @@ def load_library(path: str | None = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = path or LIB_PATH
+    p = path or os.environ.get("PQW_LIB") or LIB_PATH
     if not os.path.exists(p):
         raise EngineUnavailable(
             f"{LIB_NAME} not built (expected at {p}); run __graft_entry__.build()")
