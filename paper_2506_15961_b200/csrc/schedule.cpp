@@ -52,8 +52,9 @@ uint32_t op_cost(const DagUnit& u) {
     default: return 4;
   }
 }
+uint64_t g_bundle_base = 10;  // cost-model constant per bundle (dispatch + latency)
 uint64_t bundle_cost(const DagUnit& h, size_t n) {
-  return 10 + n * op_cost(h) + (h.op == I_INV && h.guarded ? 250 : 0);
+  return g_bundle_base + n * op_cost(h) + (h.op == I_INV && h.guarded ? 250 : 0);
 }
 bool same_class(const DagUnit& a, const DagUnit& b) {
   return a.op == b.op && a.fn == b.fn && a.k == b.k && !(a.op == I_INV && !(a.guarded && b.guarded));
@@ -118,6 +119,7 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
   const uint32_t NW = opt.n_warps;
   if (NW < 1 || NW > 32) fail("n_warps must be in [1, 32]");
   const uint64_t X = opt.xlat;
+  g_bundle_base = opt.bundle_base;
 
   // ---- producers / consumers ------------------------------------------------
   std::vector<uint32_t> pred_off(N + 1, 0), preds;
