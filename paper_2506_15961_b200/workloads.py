@@ -68,7 +68,16 @@ GENERATED = {
     "llama3-405b-tp8pp16dp2": LlamaPlanSpec(126, tp=8, pp=16, dp=2, nm=2, sp=False,
                                             desc="Llama3-405B (126 layers, GQA) TP=8 PP=16 DP=2 nm=2, "
                                                  "shape-reduced full stage sweep"),
+    # BASELINE configs[4]: DeepSeek-V3 (61 layers, 3 dense) with MLA and MoE,
+    # experts split over the tensor group, all_to_all token dispatch
+    "deepseek-v3-tp4pp4dp2-ep": LlamaPlanSpec(61, tp=4, pp=4, dp=2, nm=2, sp=True,
+                                              desc="DeepSeek-V3 (61 layers, MLA, 3 dense + 58 MoE, "
+                                                   "8 routed experts + 1 shared) TP=EP=4 PP=4 DP=2 "
+                                                   "nm=2 SP, shape-reduced", family="deepseek-v3"),
     # small members of the same families (tests)
+    "deepseek-2l-tp2dp2-sp": LlamaPlanSpec(2, tp=2, pp=1, dp=2, nm=1, sp=True,
+                                           desc="2-layer DeepSeek-style decoder (1 dense + 1 MoE), "
+                                                "TP=EP=2 DP=2 SP", family="deepseek-v3"),
     "llama-4l-tp2pp2dp2-sp": LlamaPlanSpec(4, tp=2, pp=2, dp=2, nm=2, sp=True,
                                            desc="4-layer Llama-style decoder, TP=2 PP=2 DP=2 nm=2 SP"),
 }
@@ -78,6 +87,28 @@ DEFAULT = "llama3-8b-tp4pp2dp2-sp"
 def llama_plan(spec: LlamaPlanSpec) -> Plan:
     lc = reduced_llama_config(spec.layers, spec.tp, spec.dp, spec.nm, spec.sp)
     g = completion.complete(builder.llama_forward(lc), completion.LossSpec("mean"))
+    cfg = ParallelConfig(dp=spec.dp, tp=spec.tp, pp=spec.pp, nm=spec.nm, sp=spec.sp)
+    return parallelize(g, cfg, lineage_interiors=builder.toy_interiors(g))
+
+
+def reduced_deepseek_config(layers: int, tp: int, dp: int, nm: int, sp: bool,
+                            name: str = "deepseek") -> builder.DeepSeekConfig:
+    """Minimal non-degenerate DeepSeek-V3 dimensions for a tp-way split: 2*tp
+    heads and routed experts (the expert axis is what expert parallelism
+    splits), 2-wide latent/rope/expert dims, the published 3 dense layers."""
+    batch = max(2, dp * nm)
+    seq = max(2, tp) if sp else 2
+    vocab = batch * seq
+    vocab += (-vocab) % tp
+    return builder.DeepSeekConfig(layers=layers, dense_layers=min(3, max(1, layers - 1)),
+                                  hidden=2, heads=2 * tp, head_dim=2, rope_dim=2, q_rank=2,
+                                  kv_rank=2, experts=2 * tp, expert_ffn=2, ffn=2 * tp, seq=seq,
+                                  vocab=vocab, batch=batch, name=name)
+
+
+def deepseek_plan(spec: LlamaPlanSpec) -> Plan:
+    dc = reduced_deepseek_config(spec.layers, spec.tp, spec.dp, spec.nm, spec.sp)
+    g = completion.complete(builder.deepseek_forward(dc), completion.LossSpec("mean"))
     cfg = ParallelConfig(dp=spec.dp, tp=spec.tp, pp=spec.pp, nm=spec.nm, sp=spec.sp)
     return parallelize(g, cfg, lineage_interiors=builder.toy_interiors(g))
 
@@ -95,5 +126,7 @@ def get_workload(name: str = "default") -> tuple[str, Plan]:
         return f"{name}: {desc}", _fixture(fname)
     if name in GENERATED:
         spec = GENERATED[name]
+        if spec.family == "deepseek-v3":
+            return f"{name}: {spec.desc}", deepseek_plan(spec)
         return f"{name}: {spec.desc}", llama_plan(spec)
     raise KeyError(f"unknown workload {name!r}; known: {sorted(FIXTURES) + sorted(GENERATED)}")

@@ -1,0 +1,57 @@
+"""Llama-family plans (BASELINE configs[0], a small member of configs[1]'s family,
+configs[2]'s bug-injected variants): per-stage parity with the reference.
+
+Plans come from this repo's generator; tests/golden/verdicts_deepseek.json holds
+the reference implementation's verify_plan outcome on each (bundled decision
+engine, no_cancel) -- see oracle/gen_golden_llama.py.
+"""
+
+import gzip
+import json
+import os
+
+import pytest
+
+from golden_io import GOLDEN, load_plan
+from paper_2506_15961_b200.plan import dumps
+from paper_2506_15961_b200.stages import build_stages
+
+_P = os.path.join(GOLDEN, "verdicts_deepseek.json")
+RECS = json.load(open(_P))["plans"] if os.path.exists(_P) else []
+
+
+@pytest.mark.parametrize("rec", RECS, ids=[r["name"] for r in RECS])
+def test_stage_partition_matches_reference(rec):
+    plan = load_plan(rec["plan"])
+    stages, _ = build_stages(plan)
+    got = [{"target": s.target, "logical": [n.id for n in s.logical_nodes],
+            "parallel": [n.id for n in s.parallel_nodes]} for s in stages]
+    assert got == rec["stages"]
+
+
+def test_generator_is_deterministic():
+    from oracle.gen_golden_deepseek import _plans
+    for name, plan, _meta in _plans():
+        with gzip.open(os.path.join(GOLDEN, "plans", f"{name}.json.gz"), "rt") as f:
+            assert dumps(plan) == f.read(), name
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rec", RECS, ids=[r["name"] for r in RECS])
+def test_gpu_stage_verdicts_match_reference(gpu, rec):
+    from paper_2506_15961_b200.verify import VerifyOptions, discharge, verify_plan
+    plan = load_plan(rec["plan"])
+    stages, _ = build_stages(plan)
+    results, cancelled, _ = discharge(plan, stages, VerifyOptions(no_cancel=True, witnesses=512))
+    assert cancelled == 0
+    assert [(r.target, r.status) for r in results] == [tuple(x) for x in rec["stage_status"]]
+    rep = verify_plan(plan, VerifyOptions(no_reduce=True, no_cancel=True))
+    assert rep["verdict"] == rec["verdict"]
+
+
+def test_plans_exercise_expert_all_to_all():
+    plan = load_plan(RECS[0]["plan"]) if RECS else None
+    if plan is None:
+        pytest.skip("no golden DeepSeek plans")
+    kinds = {n.kind for n in plan.parallel.nodes}
+    assert "all_to_all" in kinds and "reduce_scatter" in kinds and "all_gather" in kinds
