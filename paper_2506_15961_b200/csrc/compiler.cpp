@@ -1256,22 +1256,17 @@ CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* con
       d.nargs = (uint32_t)dag->pool.size() - d.arg0;
     }
   }
-  SchedOptions so = sched;
-  so.n_warps = n_warps;
-  so.smem_slots = smem_slots;
-  Program prog = schedule_program(*dag, so);
-  *st.code = std::move(prog.code);
-  st.n_slots = prog.n_slots;
-  st.n_spill = prog.n_spill;
-  st.n_spilled_values = prog.n_spilled_values;
-  st.n_bundles = prog.n_bundles;
-  st.n_waits = prog.n_waits;
-  st.makespan = prog.makespan;
-  for (int i = 0; i < 5; ++i) st.cls[i] = prog.cls[i];
-  for (int i = 0; i < (int)I_NUM_OPS; ++i) st.op_hist[i] = prog.op_hist[i];
-  st.field_ops = prog.cls[0] + prog.cls[1] + prog.cls[2] + prog.cls[3] + prog.cls[4];
+  st.sched = sched;
+  st.sched.n_warps = n_warps;
+  st.sched.smem_slots = smem_slots;
   st.dag = std::move(dag);
   return st;
+}
+
+void finalize_stage(CompiledStage& st) {
+  if (st.status != PQW_STAGE_OK || st.be->ready) return;
+  st.be->prog = schedule_program(*st.dag, st.sched);
+  st.be->ready = true;
 }
 
 std::vector<uint32_t> obligation_support(const CompiledStage& st, uint32_t obl) {

@@ -7,7 +7,9 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <atomic>
 #include <mutex>
+#include <thread>
 #include <numeric>
 #include <string>
 #include <unordered_map>
@@ -112,6 +114,45 @@ struct pqw_engine {
 
 using pqw::fail;
 
+// Run the compiler back end of every pending program, spread over host threads
+// (identical programs share one back end). PQW_THREADS caps the thread count.
+static int finalize_all(pqw_engine* e) {
+  std::vector<pqw::CompiledStage*> todo;
+  std::unordered_map<const pqw::StageBackend*, int> seen;
+  for (auto& st : e->stages)
+    if (st.status == PQW_STAGE_OK && !st.be->ready && seen.emplace(st.be.get(), 1).second)
+      todo.push_back(&st);
+  if (todo.empty()) return PQW_OK;
+  // largest first, handed out through a shared counter
+  std::sort(todo.begin(), todo.end(), [](const pqw::CompiledStage* a, const pqw::CompiledStage* b) {
+    return a->dag->units.size() > b->dag->units.size();
+  });
+  unsigned nt = std::max(1u, std::thread::hardware_concurrency());
+  if (const char* s = getenv("PQW_THREADS")) nt = std::max(1, atoi(s));
+  nt = std::min<unsigned>(nt, (unsigned)todo.size());
+  std::atomic<size_t> next{0};
+  std::mutex err_mu;
+  std::string err;
+  auto work = [&]() {
+    for (;;) {
+      const size_t i = next.fetch_add(1);
+      if (i >= todo.size()) return;
+      try {
+        pqw::finalize_stage(*todo[i]);
+      } catch (const std::exception& ex) {
+        std::lock_guard<std::mutex> g(err_mu);
+        if (err.empty()) err = ex.what();
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < nt; ++t) pool.emplace_back(work);
+  work();
+  for (auto& t : pool) t.join();
+  if (!err.empty()) return fail(PQW_EINVAL, std::string("stage compile: ") + err);
+  return PQW_OK;
+}
+
 extern "C" {
 
 int pqw_abi_version(void) { return PQW_ABI_VERSION; }
@@ -207,17 +248,17 @@ int pqw_stage_add(pqw_engine* e, const int32_t* ir, size_t ir_len, const int64_t
   out_status[2] = st.n_obligations;
   out_status[3] = st.n_fast;
   out_status[4] = st.n_residual;
-  out_status[5] = (int64_t)st.code->size();
-  out_status[6] = st.n_slots;
+  out_status[5] = 0;  // program size, slots, spills, bundles: known after finalization
+  out_status[6] = 0;
   out_status[7] = (int64_t)std::min<uint64_t>(st.degree, (uint64_t)INT64_MAX);
   out_status[8] = st.const_lhs;
   out_status[9] = st.const_rhs;
   out_status[10] = st.exact_lhs;
   out_status[11] = st.exact_rhs;
-  out_status[12] = (int64_t)st.field_ops;
+  out_status[12] = 0;
   out_status[13] = st.n_vars;
-  out_status[14] = st.n_spill;
-  out_status[15] = (int64_t)st.n_bundles;
+  out_status[14] = 0;
+  out_status[15] = 0;
   e->stages.push_back(std::move(st));
   e->uploaded = false;
   return (int)(e->stages.size() - 1);
@@ -242,9 +283,15 @@ int pqw_reset(pqw_engine* e) {
 long pqw_stage_bytecode(pqw_engine* e, int stage, pqw_ins* out, size_t cap, uint32_t* n_slots) {
   if (!e || stage < 0 || (size_t)stage >= e->stages.size()) return fail(PQW_EINVAL, "bad stage");
   const auto& st = e->stages[stage];
-  if (n_slots) *n_slots = st.n_slots;
-  if (out) std::memcpy(out, st.code->data(), std::min(cap, st.code->size()) * sizeof(pqw_ins));
-  return (long)st.code->size();
+  try {
+    pqw::finalize_stage(e->stages[stage]);
+  } catch (const std::exception& ex) {
+    return fail(PQW_EINVAL, std::string("stage compile: ") + ex.what());
+  }
+  const auto& code = st.prog().code;
+  if (n_slots) *n_slots = st.prog().n_slots;
+  if (out) std::memcpy(out, code.data(), std::min(cap, code.size()) * sizeof(pqw_ins));
+  return (long)code.size();
 }
 
 long pqw_obligation_support(pqw_engine* e, int stage, uint32_t obl, uint32_t* out, size_t cap) {
@@ -263,6 +310,10 @@ int pqw_upload(pqw_engine* e) {
     cudaGetLastError();
     return fail(PQW_ENODEV, "no CUDA device for the witness engine");
   }
+  {
+    int rc = finalize_all(e);
+    if (rc != PQW_OK) return rc;
+  }
   CU(cudaSetDevice(e->device));
   e->free_device();
   // stages that need the GPU, longest first (LPT order for the work queue)
@@ -270,7 +321,7 @@ int pqw_upload(pqw_engine* e) {
   for (size_t i = 0; i < e->stages.size(); ++i)
     if (e->stages[i].status == PQW_STAGE_OK) ids.push_back((int)i);
   std::stable_sort(ids.begin(), ids.end(), [&](int a, int b) {
-    return e->stages[a].code->size() > e->stages[b].code->size();
+    return e->stages[a].prog().code.size() > e->stages[b].prog().code.size();
   });
   e->gpu_stage_of = ids;
   e->n_gpu_stages = (uint32_t)ids.size();
@@ -286,22 +337,23 @@ int pqw_upload(pqw_engine* e) {
   for (size_t r = 0; r < ids.size(); ++r) {
     const auto& st = e->stages[ids[r]];
     if (st.n_warps != e->n_warps) return fail(PQW_EINVAL, "stage compiled for another warp count");
-    auto pit = placed.find(st.code.get());
+    const auto& pr = st.prog();
+    auto pit = placed.find(&pr.code);
     uint32_t off;
     if (pit == placed.end()) {
       off = (uint32_t)code.size();
-      placed.emplace(st.code.get(), off);
-      code.insert(code.end(), st.code->begin(), st.code->end());
+      placed.emplace(&pr.code, off);
+      code.insert(code.end(), pr.code.begin(), pr.code.end());
     } else {
       off = pit->second;
     }
-    descs.push_back({off, st.n_slots, st.var_base, (uint32_t)r});
+    descs.push_back({off, pr.n_slots, st.var_base, (uint32_t)r});
     work.push_back((uint32_t)r);
-    e->max_slots = std::max(e->max_slots, st.n_slots);
-    e->spill_slots = std::max(e->spill_slots, st.n_spill);
-    e->n_code += st.code->size();
-    for (int i = 0; i < PQW_B_NUM_OPS; ++i) e->op_hist[i] += st.op_hist[i];
-    for (int i = 0; i < 5; ++i) e->cls[i] += st.cls[i];
+    e->max_slots = std::max(e->max_slots, pr.n_slots);
+    e->spill_slots = std::max(e->spill_slots, pr.n_spill);
+    e->n_code += pr.code.size();
+    for (int i = 0; i < PQW_B_NUM_OPS; ++i) e->op_hist[i] += pr.op_hist[i];
+    for (int i = 0; i < 5; ++i) e->cls[i] += pr.cls[i];
   }
   e->n_code_unique = code.size();
   if (code.empty()) code.push_back(pqw_ins{PQW_B_END, 0, 0, 0});
@@ -535,17 +587,22 @@ int pqw_image_stats(pqw_engine* e, uint64_t* out, size_t cap) {
   if (!e || !out) return fail(PQW_EINVAL, "null argument");
   constexpr int N = PQW_B_NUM_OPS;
   uint64_t buf[PQW_IMAGE_STATS_LEN] = {};
+  {
+    int rc = finalize_all(e);
+    if (rc != PQW_OK) return rc;
+  }
   uint64_t n_gpu = 0, n_code = 0, max_slots = 0, max_spill = 0, bundles = 0, waits = 0;
   for (const auto& st : e->stages) {
     if (st.status != PQW_STAGE_OK) continue;
     n_gpu++;
-    n_code += st.code->size();
-    max_slots = std::max<uint64_t>(max_slots, st.n_slots);
-    max_spill = std::max<uint64_t>(max_spill, st.n_spill);
-    bundles += st.n_bundles;
-    waits += st.n_waits;
-    for (int i = 0; i < N; ++i) buf[4 + i] += st.op_hist[i];
-    for (int i = 0; i < 5; ++i) buf[6 + N + i] += st.cls[i];
+    const auto& pr = st.prog();
+    n_code += pr.code.size();
+    max_slots = std::max<uint64_t>(max_slots, pr.n_slots);
+    max_spill = std::max<uint64_t>(max_spill, pr.n_spill);
+    bundles += pr.n_bundles;
+    waits += pr.n_waits;
+    for (int i = 0; i < N; ++i) buf[4 + i] += pr.op_hist[i];
+    for (int i = 0; i < 5; ++i) buf[6 + N + i] += pr.cls[i];
   }
   buf[0] = n_gpu;
   buf[1] = n_code;

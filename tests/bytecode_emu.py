@@ -67,15 +67,19 @@ def decode(code: np.ndarray, n_warps: int) -> list[list[tuple]]:
 
 def run(code: np.ndarray, n_slots: int, var_keys: np.ndarray, var_base: int, seed: int,
         witnesses: np.ndarray, n_warps: int = 16, policy: str = "random", rng_seed: int = 0,
-        n_spill: int = 64):
+        n_spill: int | None = None):
     """Returns (valid mask [W], first bad obligation per witness [W] or -1)."""
     W = len(witnesses)
+    streams = decode(code, n_warps)
+    if n_spill is None:  # global spill slots the program addresses
+        n_spill = 1 + max([int(c.max()) // SLOT for st in streams
+                           for op, _f, _k, _a, _s, cols in st if op in ("FILL", "SPILL")
+                           for c in (cols[1] if op == "FILL" else cols[0],) if len(c)] or [0])
     sm = np.zeros((max(n_slots, 1), W), dtype=np.uint64)
     gm = np.zeros((max(n_spill, 1), W), dtype=np.uint64)
     valid = np.ones(W, dtype=bool)
     bad = np.full(W, -1, dtype=np.int64)
     w1 = np.asarray(witnesses, dtype=np.uint64) + np.uint64(1)
-    streams = decode(code, n_warps)
     pc = [0] * n_warps
     prog = [0] * n_warps
     rng = np.random.default_rng(rng_seed)

@@ -37,8 +37,7 @@ def test_bytecode_matches_oracle(lib, rec):
             code, ns = eng.bytecode(c.index)
             policy = ("random", "ahead", "behind")[c.index % 3]
             valid, bad = bytecode_emu.run(code, ns, lw.var_keys, base, seed, wit,
-                                          n_warps=16, policy=policy, rng_seed=c.index,
-                                          n_spill=c.spill_slots)
+                                          n_warps=16, policy=policy, rng_seed=c.index)
             assert int(valid.sum()) == o.valid, st.target
             emu_bad = (bad >= 0) & valid
             want = o.bad_mask.any(axis=0) if o.bad_mask is not None else np.zeros(W, bool)
@@ -76,14 +75,14 @@ def test_small_value_file_spills_correctly(lib, rec, warps, slots, monkeypatch):
         c = eng.add_stage(lw.ir, lw.consts, lw.var_keys)
         if c.status != STAGE_OK:
             continue
-        assert c.slots <= slots
-        spilled += c.spill_slots > 0
         o = check_stage(plan, st, owner, seed, wit)
         code, ns = eng.bytecode(c.index)
+        assert ns <= slots
+        spilled += any(ins[0] == "FILL" for stream in bytecode_emu.decode(code, warps)
+                       for ins in stream)
         for policy in ("ahead", "behind", "random"):
             valid, bad = bytecode_emu.run(code, ns, lw.var_keys, 0, seed, wit, n_warps=warps,
-                                          policy=policy, rng_seed=c.index,
-                                          n_spill=c.spill_slots)
+                                          policy=policy, rng_seed=c.index)
             assert int(valid.sum()) == o.valid, (st.target, policy)
             emu_bad = (bad >= 0) & valid
             want = o.bad_mask.any(axis=0) if o.bad_mask is not None else np.zeros(W, bool)
