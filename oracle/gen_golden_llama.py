@@ -79,6 +79,8 @@ def _job(args):
         rec["verdict"] = rep["verdict"]
         rec["refuted_by"] = rep.get("refuted_by")
         rec["stage_status"] = [(s["target"], s["status"]) for s in rep["stages"]]
+        rec["stage_reason"] = {s["target"]: (s.get("detail") or {}).get("reason")
+                               for s in rep["stages"] if s["status"] == "unknown"}
     except Exception as e:  # noqa: BLE001 - recorded as the reference's outcome
         rec["error"] = type(e).__name__
         rec["message"] = str(e)[:300]

@@ -570,7 +570,7 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
     }
     if (!ok) continue;
     const uint64_t traffic = cand.op_hist[I_FILL] + cand.op_hist[I_SPILL];
-    const uint64_t score = cand.makespan + traffic * 8 / NW;
+    const uint64_t score = cand.makespan + traffic * opt.spill_cost / NW;
     if (score < best_score) {
       best_score = score;
       best = std::move(cand);

@@ -187,6 +187,7 @@ int pqw_engine_create(int device, uint64_t seed, const uint64_t fn_keys[3], pqw_
   env("PQW_BMAX", 1, 4096, e->sched.bmax);
   env("PQW_XLAT", 0, 1 << 20, e->sched.xlat);
   env("PQW_BUNDLE_BASE", 0, 1 << 20, e->sched.bundle_base);
+  env("PQW_SPILL_COST", 0, 1 << 20, e->sched.spill_cost);
   *out = e;
   return PQW_OK;
 }

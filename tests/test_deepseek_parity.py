@@ -44,7 +44,18 @@ def test_gpu_stage_verdicts_match_reference(gpu, rec):
     stages, _ = build_stages(plan)
     results, cancelled, _ = discharge(plan, stages, VerifyOptions(no_cancel=True, witnesses=512))
     assert cancelled == 0
-    assert [(r.target, r.status) for r in results] == [tuple(x) for x in rec["stage_status"]]
+    want = [tuple(x) for x in rec["stage_status"]]
+    assert [r.target for r in results] == [t for t, _ in want]
+    for r, (target, status) in zip(results, want):
+        if status == "unknown":
+            # the reference left the stage undecided (its solver returned
+            # unknown, or its countermodel failed exact replay); the witness
+            # engine decides it -- refuted, with a concrete counterexample that
+            # tests/test_replay_reference.py replays in the reference evaluator
+            assert target in rec["stage_reason"]
+            assert r.status == "refuted", target
+        else:
+            assert r.status == status, target
     rep = verify_plan(plan, VerifyOptions(no_reduce=True, no_cancel=True))
     assert rep["verdict"] == rec["verdict"]
 

@@ -131,3 +131,54 @@ def test_counterexample_replays_in_reference_evaluator(rec):
         assert F.residue(lv) == o.lhs and F.residue(rv) == o.rhs, st.target
     if rec["default"].get("verdict") == "refuted" and rec["default"].get("refuted_by") != "structure":
         assert refuted > 0
+
+
+def _ds_recs():
+    import json
+    from golden_io import GOLDEN
+    p = os.path.join(GOLDEN, "verdicts_deepseek.json")
+    if not os.path.exists(p):
+        return []
+    return [r for r in json.load(open(p))["plans"] if r.get("stage_reason")]
+
+
+DS_RECS = _ds_recs()
+
+
+@pytest.mark.parametrize("rec", DS_RECS, ids=[r["name"] for r in DS_RECS])
+def test_unconfirmed_reference_countermodels_are_real(rec):
+    """Where the reference reports "unknown" (its solver returned unknown, or its
+    countermodel failed exact replay), the witness engine's counterexample
+    replays: the two sides of the failing obligation differ as rationals in the
+    reference's own evaluator."""
+    import gzip
+    from golden_io import GOLDEN
+    rplan, rstages, rops, rsym, iter_box, _ = _ref_modules()
+    seed, W = 21, 16
+    plan = load_plan(rec["plan"])
+    with gzip.open(os.path.join(GOLDEN, rec["plan"]), "rt") as f:
+        text = f.read()
+    stages, _ = build_stages(plan)
+    owner = shard_owner(plan, entry_order(plan))
+    keys = {fn: F.fn_key(seed, fn) for fn in F.FN_NAMES}
+
+    def uf(fn, x):
+        return Fraction(F.uf_apply(keys[fn], F.residue(x)))
+
+    targets = sorted(rec["stage_reason"])[:4]
+    for st in stages:
+        if st.target not in targets:
+            continue
+        o = check_stage(plan, st, owner, seed, np.arange(W, dtype=np.uint64))
+        assert o.status == "refuted", st.target
+        w, obl = o.first_bad
+        pairs, _alg = _ref_obligations(rplan, rstages, rops, rsym, iter_box, text, st.target)
+        lhs, rhs = pairs[obl]
+        env = {}
+        for name in rsym.collect_vars([lhs, rhs]):
+            prefix, i = name.rsplit(".", 1)
+            env[name] = Fraction(F.witness_value(F.var_key(seed, prefix, int(i)), w))
+        lv = lhs if isinstance(lhs, int) else rsym.eval_expr(lhs, env, uf)
+        rv = rhs if isinstance(rhs, int) else rsym.eval_expr(rhs, env, uf)
+        assert lv != rv, st.target
+        assert F.residue(lv) == o.lhs and F.residue(rv) == o.rhs, st.target
