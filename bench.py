@@ -65,19 +65,7 @@ def load_workload(name: str):
     return desc, plan, stages
 
 
-def partition(costs: list[int], n: int) -> list[list[int]]:
-    """LPT static partition of stage indices into n cost-balanced parts."""
-    parts = [[] for _ in range(n)]
-    load = [0] * n
-    for i in sorted(range(len(costs)), key=lambda i: -costs[i]):
-        k = min(range(n), key=lambda j: load[j])
-        parts[k].append(i)
-        load[k] += costs[i]
-    return [sorted(p) for p in parts]
-
-
-def stage_cost(st) -> int:
-    return sum(1 for _ in st.parallel_nodes) + sum(1 for _ in st.logical_nodes)
+from paper_2506_15961_b200.distributed import partition, stage_cost  # noqa: E402
 
 
 # -- clocks -------------------------------------------------------------------

@@ -44,6 +44,7 @@ class VerifyOptions:
     witnesses: int = DEFAULT_WITNESSES
     seed: int = 0
     device: int = 0
+    shard: bool = True  # under torch.distributed (world > 1): split stages over the ranks
 
 
 def _aggregate(results: list[StageResult], cancelled: int) -> str:
@@ -215,7 +216,11 @@ def verify_plan(plan: Plan, opts: VerifyOptions | None = None) -> dict[str, Any]
         report["warning"] = (f"{len(loose)} node(s) feed no checkpoint and are "
                              f"not checked: {loose[:8]}")
 
-    results, cancelled, stats = discharge(work, stages, opts)
+    from .distributed import discharge_sharded, world_info
+    if opts.shard and world_info()[1] > 1:
+        results, cancelled, stats = discharge_sharded(work, stages, opts)
+    else:
+        results, cancelled, stats = discharge(work, stages, opts)
     verdict = _aggregate(results, cancelled)
     total_ob = sum(r.obligations for r in results)
     total_fast = sum(r.fastpath for r in results)
