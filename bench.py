@@ -248,6 +248,7 @@ def main():
 
     # e2e through the C-ABI with host buffers (compile + H2D + launch + D2H)
     e2e_ms = []
+    e2e_parts = []
     h2d = d2h = 0
     for _ in range(args.e2e_steps):
         torch.cuda.synchronize()
@@ -255,10 +256,14 @@ def main():
         e2 = Engine(local, seed, F.fn_keys(seed))
         for lw in lowered:
             e2.add_stage(lw.ir, lw.consts, lw.var_keys)
+        t1 = time.perf_counter()
         e2.upload()
+        t2 = time.perf_counter()
         e2.launch(W, sptr)
         r = e2.results()
-        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        t3 = time.perf_counter()
+        e2e_ms.append((t3 - t0) * 1e3)
+        e2e_parts.append(((t1 - t0) * 1e3, (t2 - t1) * 1e3, (t3 - t2) * 1e3))
         st2 = e2.image_stats()
         h2d = 16 * st2["unique_instructions"] + 8 * sum(lw.var_keys.size for lw in lowered) + \
             16 * st2["gpu_stages"]
@@ -311,7 +316,10 @@ def main():
             "clocks": clk.summary(),
             "e2e": {"value": round(e2e_val, 3), "unit": "stage-checks/s",
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                    "what": "C-ABI compile of host stage programs + H2D + launch + D2H"},
+                    "what": "C-ABI compile of host stage programs + H2D + launch + D2H",
+                    "ms_parts": {k: round(float(np.mean([p[i] for p in e2e_parts])), 3)
+                                 for i, k in enumerate(("stage_add", "upload", "launch_results"))}
+                    if e2e_parts else None},
             "roofline": {"bound": "int", "achieved": round(achieved / 1e9, 3),
                          "peak": round(peak / 1e9, 3), "unit": "Gfieldop/s",
                          "frac": round(achieved / peak, 4), "traffic": None,

@@ -111,7 +111,11 @@ __device__ __forceinline__ uint32_t red64(uint64_t x) { return fred64(x); }
 // group. Every read unit (a header, one payload group, or one pair/term of a
 // wide DOT/SUM) is at most 33 records, so it spans at most two chunks.
 constexpr uint32_t RING_RECS = 64;
+#ifdef PQW_NO_RING
+constexpr uint32_t RING_BYTES = 0;
+#else
 constexpr uint32_t RING_BYTES = RING_RECS * 16;
+#endif
 
 struct CodeRing {
   const uint4* src;   // global start of this warp's stream
@@ -131,6 +135,9 @@ struct CodeRing {
   }
   // make records [p, p + r) resident (r <= 33)
   __device__ __forceinline__ void ensure(uint32_t p, uint32_t r) {
+#ifdef PQW_NO_RING
+    return;
+#endif
     const uint32_t c0 = p >> 5, c1 = (p + r - 1) >> 5;
     if (issued <= c0 + 1) issue();  // look-ahead: the slot of chunk c0+1 held c0-1
     if (c1 >= ready) {
@@ -144,6 +151,9 @@ struct CodeRing {
     }
   }
   __device__ __forceinline__ uint4 rec(uint32_t p) const {
+#ifdef PQW_NO_RING
+    return __ldg(src + p);
+#endif
     uint4 v;
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
@@ -155,6 +165,9 @@ struct CodeRing {
     return F8{{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}};
   }
   __device__ __forceinline__ void drain() {
+#ifdef PQW_NO_RING
+    return;
+#endif
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncwarp();
   }
@@ -200,12 +213,22 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
   const uint64_t* vkeys = p.var_keys + sd.var_base;
   CodeRing cr{stream, ring, lane * 16u, 0u, 0u};
   uint32_t pc = 0;  // record position in the stream
+#ifdef PQW_PROF
+  long long t_end = clock64();
+#endif
   for (;;) {
     cr.ensure(pc, 1);
     const uint4 h = cr.rec(pc);
     ++pc;
     const uint32_t op = h.x & 0xFFu;
     const uint32_t n = h.y;
+#ifdef PQW_PROF
+    const long long t_start = clock64();
+    const uint32_t kk = h.x >> 16;
+    const uint32_t cls = op == I_DOT ? (kk == 1 ? 0 : kk == 2 ? 1 : 2)
+                       : op == I_SUM ? (kk == 2 ? 3 : 4)
+                       : op + 2;  // SUB 5 .. WAIT 15
+#endif
     switch (op) {
       case I_END:
         cr.drain();  // no copy may land in the ring after this item
@@ -416,6 +439,19 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
       __syncwarp();
       if (lane == 0) st_release(prog + warp, h.w);
     }
+#ifdef PQW_PROF
+    {
+      const long long t_now = clock64();
+      if (lane == 0) {
+        unsigned long long* c = p.prof + 8 + 4 * cls;
+        atomicAdd(c + 0, (unsigned long long)(t_now - t_start));   // bundle cycles
+        atomicAdd(c + 1, (unsigned long long)((n + 7) / 8));        // groups
+        atomicAdd(c + 2, 1ull);                                     // bundles
+        atomicAdd(c + 3, (unsigned long long)(t_start - t_end));    // dispatch cycles
+      }
+      t_end = t_now;
+    }
+#endif
   }
 }
 

@@ -27,6 +27,7 @@
 #include <queue>
 #include <set>
 #include <stdexcept>
+#include <thread>
 #include <unordered_map>
 
 namespace pqw {
@@ -52,7 +53,7 @@ uint32_t op_cost(const DagUnit& u) {
     default: return 4;
   }
 }
-uint64_t g_bundle_base = 10;  // cost-model constant per bundle (dispatch + latency)
+thread_local uint64_t g_bundle_base = 10;  // cost-model constant per bundle (dispatch + latency)
 uint64_t bundle_cost(const DagUnit& h, size_t n) {
   return g_bundle_base + n * op_cost(h) + (h.op == I_INV && h.guarded ? 250 : 0);
 }
@@ -269,7 +270,10 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
 
     // ---- 2. allocation: choose spills, then colour exactly -------------------
     const uint32_t K = o.smem_slots;
-    for (uint32_t reserve = 0;; reserve = reserve ? reserve * 2 : 16) {
+    // the reserve for FILL/SPILL temporaries grows by what the last colouring
+    // overshot (each extra spilled value frees about one slot)
+    uint32_t overshoot = 0;
+    for (uint32_t reserve = 0;; reserve = std::max(reserve * 2, reserve + 2 * overshoot + 16)) {
       if (reserve >= K) break;  // give up on this schedule: re-schedule narrower
       std::vector<uint8_t> spilled(N, 0);
       {
@@ -346,7 +350,10 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
       }
       std::vector<int32_t> sprev, gprev;
       const uint32_t n_sm = colour(sm, sprev);
-      if (n_sm > K) continue;  // more temporaries than the reserve: spill more
+      if (n_sm > K) {  // more temporaries than the reserve: spill more
+        overshoot = n_sm - K;
+        continue;
+      }
       const uint32_t n_gm = colour(gm, gprev);
 
       // ---- 3. synchronisation -------------------------------------------------
@@ -557,18 +564,17 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
   Program best;
   bool have = false;
   uint64_t best_score = INF;
-  for (uint32_t win : windows) {
-    if (have && win < 384) break;  // tiny windows only as a last resort
+  auto attempt = [&](uint32_t win, Program& cand) -> bool {
+    g_bundle_base = opt.bundle_base;  // thread_local: attempts may run on worker threads
     SchedOptions o = opt;
     o.window = win;
-    Program cand;
-    bool ok = false;
-    for (uint32_t bm = opt.bmax; !ok; bm /= 2) {
+    for (uint32_t bm = opt.bmax;; bm /= 2) {
       o.bmax = std::max<uint32_t>(bm, 1);
-      ok = try_once(o, cand);
-      if (bm <= 1) break;
+      if (try_once(o, cand)) return true;
+      if (bm <= 1) return false;
     }
-    if (!ok) continue;
+  };
+  auto consider = [&](Program& cand) {
     const uint64_t traffic = cand.op_hist[I_FILL] + cand.op_hist[I_SPILL];
     const uint64_t score = cand.makespan + traffic * opt.spill_cost / NW;
     if (score < best_score) {
@@ -576,7 +582,27 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
       best = std::move(cand);
       have = true;
     }
-    if (traffic == 0) break;  // narrower windows cannot do better without spills
+  };
+  // the widest window first; only when it spills are the narrower ones tried
+  size_t wi = 0;
+  {
+    Program cand;
+    if (attempt(windows[0], cand)) {
+      const bool spills = cand.op_hist[I_FILL] + cand.op_hist[I_SPILL] != 0;
+      consider(cand);
+      wi = spills ? 1 : windows.size();
+    } else {
+      wi = 1;
+    }
+  }
+  // (sequential: the engine already compiles distinct programs on parallel threads)
+  for (; wi < windows.size(); ++wi) {
+    if (have && windows[wi] < 384) break;  // tiny windows: last resort only
+    Program cand;
+    if (!attempt(windows[wi], cand)) continue;
+    const bool spills = cand.op_hist[I_FILL] + cand.op_hist[I_SPILL] != 0;
+    consider(cand);
+    if (!spills) break;  // narrower windows cannot do better without spills
   }
   if (!have) {
     // last resort: one warp, one op per bundle (a sequential evaluation)

@@ -2,6 +2,7 @@
 // extern "C" API of include/planeq_witness.h (compile, upload, launch, results,
 // probe). The device interpreter lives in interp.cuh.
 #include <cuda_runtime.h>
+#include <sched.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -127,7 +128,12 @@ static int finalize_all(pqw_engine* e) {
   std::sort(todo.begin(), todo.end(), [](const pqw::CompiledStage* a, const pqw::CompiledStage* b) {
     return a->dag->units.size() > b->dag->units.size();
   });
+  // the CPUs this process may run on (hardware_concurrency reports the host's)
   unsigned nt = std::max(1u, std::thread::hardware_concurrency());
+  {
+    cpu_set_t cs;
+    if (sched_getaffinity(0, sizeof(cs), &cs) == 0) nt = std::max(1, CPU_COUNT(&cs));
+  }
   if (const char* s = getenv("PQW_THREADS")) nt = std::max(1, atoi(s));
   nt = std::min<unsigned>(nt, (unsigned)todo.size());
   std::atomic<size_t> next{0};
@@ -180,9 +186,12 @@ int pqw_engine_create(int device, uint64_t seed, const uint64_t fn_keys[3], pqw_
       if (v >= lo && v <= hi) out = (uint32_t)v;
     }
   };
-  env("PQW_FAST_SLOTS", 16, 1760, e->fast_slots);
-  env("PQW_WARPS", 8, 16, e->n_warps);
-  if (e->n_warps != 8 && e->n_warps != 16) e->n_warps = pqw::DEFAULT_WARPS;
+  env("PQW_WARPS", 8, 32, e->n_warps);
+  if (e->n_warps != 8 && e->n_warps != 16 && e->n_warps != 32) e->n_warps = pqw::DEFAULT_WARPS;
+  // the shared value file gets what the per-warp code rings leave of 227 KB
+  e->fast_slots = std::min<uint32_t>(
+      pqw::DEFAULT_FAST_SLOTS, (232448u - 512u - e->n_warps * pqw::RING_BYTES) / pqw::SLOT_BYTES);
+  env("PQW_FAST_SLOTS", 16, 1800, e->fast_slots);
   env("PQW_WINDOW", 1, 1 << 20, e->sched.window);
   env("PQW_BMAX", 1, 4096, e->sched.bmax);
   env("PQW_XLAT", 0, 1 << 20, e->sched.xlat);
@@ -373,21 +382,22 @@ int pqw_upload(pqw_engine* e) {
   if (smem_bytes + 512 > prop.sharedMemPerBlockOptin)
     return fail(PQW_EINVAL, "value file does not fit in shared memory");
   int per_sm = 0;
-  if (e->n_warps == 16) {
-    CU(cudaFuncSetAttribute(pqw::eval_kernel<16, false>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
-    CU(cudaFuncSetAttribute(pqw::eval_kernel<16, true>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pqw::eval_kernel<16, false>,
-                                                     16 * 32, smem_bytes));
-  } else {
-    CU(cudaFuncSetAttribute(pqw::eval_kernel<8, false>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
-    CU(cudaFuncSetAttribute(pqw::eval_kernel<8, true>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pqw::eval_kernel<8, false>, 8 * 32,
-                                                     smem_bytes));
-  }
+  auto setup = [&](auto kern_false, auto kern_true, int threads) -> cudaError_t {
+    cudaError_t err = cudaFuncSetAttribute(kern_false, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem_bytes);
+    if (err == cudaSuccess)
+      err = cudaFuncSetAttribute(kern_true, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem_bytes);
+    if (err == cudaSuccess)
+      err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern_false, threads, smem_bytes);
+    return err;
+  };
+  if (e->n_warps == 32)
+    CU(setup(pqw::eval_kernel<32, false>, pqw::eval_kernel<32, true>, 32 * 32));
+  else if (e->n_warps == 16)
+    CU(setup(pqw::eval_kernel<16, false>, pqw::eval_kernel<16, true>, 16 * 32));
+  else
+    CU(setup(pqw::eval_kernel<8, false>, pqw::eval_kernel<8, true>, 8 * 32));
   if (per_sm < 1) per_sm = 1;
   e->grid = (uint32_t)(prop.multiProcessorCount * per_sm);
 
@@ -424,7 +434,10 @@ static int launch_eval(pqw_engine* e, const pqw::Params& p, uint32_t grid, bool 
                        cudaStream_t s) {
   const size_t smem_bytes =
       (size_t)e->smem_slots * pqw::SLOT_BYTES + (size_t)e->n_warps * pqw::RING_BYTES;
-  if (e->n_warps == 16) {
+  if (e->n_warps == 32) {
+    if (probe) pqw::eval_kernel<32, true><<<1, 32 * 32, smem_bytes, s>>>(p);
+    else pqw::eval_kernel<32, false><<<grid, 32 * 32, smem_bytes, s>>>(p);
+  } else if (e->n_warps == 16) {
     if (probe) pqw::eval_kernel<16, true><<<1, 16 * 32, smem_bytes, s>>>(p);
     else pqw::eval_kernel<16, false><<<grid, 16 * 32, smem_bytes, s>>>(p);
   } else {
@@ -467,8 +480,8 @@ int pqw_launch(pqw_engine* e, uint32_t n_witness, void* stream) {
   p.file_bytes = e->smem_slots * pqw::SLOT_BYTES;
 #ifdef PQW_PROF
   static unsigned long long* d_prof = nullptr;
-  if (!d_prof) CU(cudaMalloc(&d_prof, 4 * sizeof(unsigned long long)));
-  CU(cudaMemsetAsync(d_prof, 0, 4 * sizeof(unsigned long long), s));
+  if (!d_prof) CU(cudaMalloc(&d_prof, 80 * sizeof(unsigned long long)));
+  CU(cudaMemsetAsync(d_prof, 0, 80 * sizeof(unsigned long long), s));
   p.prof = d_prof;
   e->d_prof_last = d_prof;
 #endif
@@ -501,10 +514,21 @@ int pqw_results(pqw_engine* e, uint64_t* first_bad, uint32_t* n_valid, uint32_t*
   }
 #ifdef PQW_PROF
   if (e->d_prof_last) {
-    unsigned long long pr[4];
+    unsigned long long pr[80];
     CU(cudaMemcpy(pr, e->d_prof_last, sizeof(pr), cudaMemcpyDeviceToHost));
     fprintf(stderr, "PQW_PROF warp-cycles: item %.3e wait %.3e (%.1f%%) end-barrier %.3e (%.1f%%)\n",
             (double)pr[0], (double)pr[1], 100.0 * pr[1] / pr[0], (double)pr[2], 100.0 * pr[2] / pr[0]);
+    static const char* names[18] = {"DOT1", "DOT2", "DOTk", "SUM2", "SUMk", "SUB", "NEG", "HASH",
+                                    "INV", "VAR", "CONST", "CHK", "DEN", "FILL", "SPILL", "WAIT",
+                                    "?", "?"};
+    for (int c = 0; c < 16; ++c) {
+      const unsigned long long* q = pr + 8 + 4 * c;
+      if (!q[2]) continue;
+      fprintf(stderr, "PQW_PROF %-5s bundles %10llu groups %10llu cyc/group %8.1f cyc/bundle %8.1f "
+              "dispatch/bundle %7.1f share %.1f%%\n", names[c], q[2], q[1],
+              q[1] ? (double)q[0] / q[1] : 0.0, (double)q[0] / q[2], (double)q[3] / q[2],
+              100.0 * (q[0] + q[3]) / pr[0]);
+    }
   }
 #endif
   for (size_t i = 0; i < n_stages; ++i) {
