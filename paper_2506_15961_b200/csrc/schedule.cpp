@@ -273,8 +273,7 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
     // the reserve for FILL/SPILL temporaries grows by what the last colouring
     // overshot (each extra spilled value frees about one slot)
     uint32_t overshoot = 0;
-    for (uint32_t reserve = 0;; reserve = std::max(reserve * 2, reserve + 2 * overshoot + 16)) {
-      if (reserve >= K) break;  // give up on this schedule: re-schedule narrower
+    for (uint32_t reserve = 0;;) {
       std::vector<uint8_t> spilled(N, 0);
       {
         const uint32_t keff = K - reserve;
@@ -352,6 +351,8 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
       const uint32_t n_sm = colour(sm, sprev);
       if (n_sm > K) {  // more temporaries than the reserve: spill more
         overshoot = n_sm - K;
+        if (reserve + 1 >= K) break;  // give up on this schedule: re-schedule narrower
+        reserve = std::min(K - 1, std::max(reserve * 2, reserve + 2 * overshoot + 16));
         continue;
       }
       const uint32_t n_gm = colour(gm, gprev);
