@@ -200,6 +200,22 @@ __device__ __forceinline__ uint32_t run_elementwise(CodeRing& cr, uint32_t pc, u
   return pc;
 }
 
+// Wait (all lanes) until a warp's published progress reaches `target`.
+__device__ __forceinline__ void wait_progress(const Params& p, const uint32_t* flag,
+                                              uint32_t target) {
+  if (ld_acquire(flag) < target) {
+#ifdef PQW_PROF
+    const long long t0 = clock64();
+#endif
+    do {
+      __nanosleep(32);
+    } while (ld_acquire(flag) < target);
+#ifdef PQW_PROF
+    if ((threadIdx.x & 31u) == 0) atomicAdd(p.prof + 1, (unsigned long long)(clock64() - t0));
+#endif
+  }
+}
+
 // Runs this warp's stream of the stage program for witness w = tile*32 + lane,
 // folding the lane's definedness and first failing obligation into valid/bad.
 template <bool PROBE>
@@ -222,6 +238,8 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
     ++pc;
     const uint32_t op = h.x & 0xFFu;
     const uint32_t n = h.y;
+    if (op != I_WAIT && h.z)  // a wait folded into the bundle header
+      wait_progress(p, prog + (h.z >> 24) - 1, h.z & 0xFFFFFFu);
 #ifdef PQW_PROF
     const long long t_start = clock64();
     const uint32_t kk = h.x >> 16;
@@ -413,22 +431,10 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
             *reinterpret_cast<uint32_t*>(gl + G.v[i]) = lds(sb, A.v[i]);
         }
         break;
-      case I_WAIT: {
+      case I_WAIT:
         // header: z = producer warp, w = progress it must have published
-        const uint32_t* flag = prog + h.z;
-        if (ld_acquire(flag) < h.w) {
-#ifdef PQW_PROF
-          const long long t0 = clock64();
-#endif
-          do {
-            __nanosleep(32);
-          } while (ld_acquire(flag) < h.w);
-#ifdef PQW_PROF
-          if (lane == 0) atomicAdd(p.prof + 1, (unsigned long long)(clock64() - t0));
-#endif
-        }
+        wait_progress(p, prog + h.z, h.w);
         break;
-      }
       default:
         __builtin_unreachable();
     }

@@ -9,8 +9,9 @@
 //
 // Instruction = one header record + payload records.
 //   header.x = op | fn << 8 | k << 16,  header.y = n (ops in the bundle),
-//   header.z = aux,  header.w = progress this warp publishes after the bundle
-//   (0: none) -- WAIT uses z = producer warp, w = progress to wait for.
+//   header.z = a wait folded into the bundle ((warp + 1) << 24 | progress; 0:
+//   none), header.w = progress this warp publishes after the bundle (0: none)
+//   -- a WAIT instruction uses z = producer warp, w = progress to wait for.
 // A bundle holds n independent ops of one kind. Its payload is ceil(n / 8)
 // groups; a group lists, field by field, 8 u32 values (two records) for the 8
 // ops of the group (unused entries of the last group are 0):

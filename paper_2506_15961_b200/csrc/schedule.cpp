@@ -455,11 +455,15 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
         reinterpret_cast<uint32_t*>(code.data())[w] = (uint32_t)code.size();
         for (uint32_t e : stream[w]) {
           const Exec& E = ex[e];
-          for (auto& pr : waits[e]) {
-            code.push_back(pqw_ins{isa_header(I_WAIT, 0, 0), 0, pr.first, pr.second});
+          // all but the last wait become WAIT instructions; the last one rides in
+          // the bundle header (z = (warp + 1) << 24 | count), saving a dispatch
+          const size_t nwait = waits[e].size();
+          for (size_t i = 0; i + 1 < nwait; ++i) {
+            code.push_back(pqw_ins{isa_header(I_WAIT, 0, 0), 0, waits[e][i].first,
+                                   waits[e][i].second});
             prog.op_hist[I_WAIT]++;
-            prog.n_waits++;
           }
+          prog.n_waits += (uint32_t)nwait;
           const size_t hdr = code.size();  // header of this exec's instruction
           const auto& B = bundles[E.main];
           if (E.kind == 1 || E.kind == 2) {
@@ -533,6 +537,11 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
               prog.cls[3] += 1;
             }
             put_bundle(H.op, H.fn, H.k, (uint32_t)B.units.size(), 0, fields, nf);
+          }
+          if (nwait) {
+            const auto& pr = waits[e][nwait - 1];
+            if (pr.second >= (1u << 24)) fail("stream too long for a folded wait");
+            code[hdr].a = ((pr.first + 1) << 24) | pr.second;
           }
           if (signal_after[e]) {
             code[hdr].b = E.seq + 1;  // header.w: publish progress after this bundle

@@ -95,6 +95,8 @@ def run(code: np.ndarray, n_slots: int, var_keys: np.ndarray, var_base: int, see
             return False
         if op == "WAIT":
             return prog[aux] >= sig
+        if aux:  # a wait folded into the bundle header
+            return prog[(aux >> 24) - 1] >= (aux & 0xFFFFFF)
         return True
 
     def step(w):
