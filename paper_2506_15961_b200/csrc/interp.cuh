@@ -57,6 +57,7 @@ struct Params {
   uint32_t tiles;            // work items per stage
   uint32_t n_witness;
   uint32_t spill_slots;      // per-CTA spill capacity in slots
+  uint32_t sleep_ns;         // back-off of a waiting warp between progress polls
   uint32_t file_bytes;       // shared value file size (the code rings follow it)
   // probe mode
   uint32_t probe_w;
@@ -208,7 +209,7 @@ __device__ __forceinline__ void wait_progress(const Params& p, const uint32_t* f
     const long long t0 = clock64();
 #endif
     do {
-      __nanosleep(32);
+      __nanosleep(p.sleep_ns);
     } while (ld_acquire(flag) < target);
 #ifdef PQW_PROF
     if ((threadIdx.x & 31u) == 0) atomicAdd(p.prof + 1, (unsigned long long)(clock64() - t0));

@@ -71,6 +71,7 @@ struct pqw_engine {
   uint32_t max_slots = 0;
   uint32_t smem_slots = 0;
   uint32_t n_warps = pqw::DEFAULT_WARPS;
+  uint32_t sleep_ns = 32;
   uint32_t fast_slots = pqw::DEFAULT_FAST_SLOTS;  // shared value-file capacity (slots)
   uint32_t spill_slots = 0;                        // per-CTA global spill capacity
   pqw::SchedOptions sched;
@@ -197,6 +198,7 @@ int pqw_engine_create(int device, uint64_t seed, const uint64_t fn_keys[3], pqw_
   env("PQW_XLAT", 0, 1 << 20, e->sched.xlat);
   env("PQW_BUNDLE_BASE", 0, 1 << 20, e->sched.bundle_base);
   env("PQW_SPILL_COST", 0, 1 << 20, e->sched.spill_cost);
+  env("PQW_SLEEP", 0, 100000, e->sleep_ns);
   *out = e;
   return PQW_OK;
 }
@@ -478,6 +480,7 @@ int pqw_launch(pqw_engine* e, uint32_t n_witness, void* stream) {
   p.n_witness = n_witness;
   p.spill_slots = std::max<uint32_t>(e->spill_slots, 1);
   p.file_bytes = e->smem_slots * pqw::SLOT_BYTES;
+  p.sleep_ns = e->sleep_ns;
 #ifdef PQW_PROF
   static unsigned long long* d_prof = nullptr;
   if (!d_prof) CU(cudaMalloc(&d_prof, 80 * sizeof(unsigned long long)));
@@ -576,6 +579,7 @@ int pqw_probe(pqw_engine* e, int stage, uint32_t witness, uint32_t obl, uint32_t
   p.n_witness = witness + 1;
   p.spill_slots = std::max<uint32_t>(e->spill_slots, 1);
   p.file_bytes = e->smem_slots * pqw::SLOT_BYTES;
+  p.sleep_ns = e->sleep_ns;
   p.probe_w = witness;
   p.probe_obl = obl;
   p.probe_out = e->d_probe;
