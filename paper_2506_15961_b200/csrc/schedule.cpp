@@ -78,36 +78,53 @@ struct Interval {
 
 // Exact colouring of intervals (a slot is free for `start` once its occupant's
 // end < start). Returns the number of slots; fills slot and, per interval, the
-// previous occupant of its slot (or -1).
-uint32_t colour(std::vector<Interval>& iv, std::vector<int32_t>& prev) {
+// previous occupant of its slot (or -1). Among free slots a writer prefers one
+// whose previous occupant was only touched by its own warp (`owner`: the warp
+// of all of an interval's readers, or -1 when several), so the slot reuse needs
+// no cross-warp write-after-read wait; the slot count is optimal either way.
+uint32_t colour(std::vector<Interval>& iv, std::vector<int32_t>& prev,
+                const std::vector<int32_t>& owner, const std::vector<uint32_t>& writer_warp,
+                uint32_t NW) {
   std::vector<uint32_t> order(iv.size());
   for (uint32_t i = 0; i < iv.size(); ++i) order[i] = i;
   std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
     return iv[a].start != iv[b].start ? iv[a].start < iv[b].start : a < b;
   });
-  using E = std::pair<uint64_t, uint32_t>;  // (end, slot)
+  using E = std::pair<uint64_t, uint32_t>;  // (end, interval)
   std::priority_queue<E, std::vector<E>, std::greater<E>> busy;
-  std::priority_queue<uint32_t, std::vector<uint32_t>, std::greater<uint32_t>> free_s;
+  // free slots per owning warp (index NW: shared by several warps)
+  std::vector<std::vector<uint32_t>> free_s(NW + 1);
   std::vector<int32_t> last_of_slot;
   prev.assign(iv.size(), -1);
   uint32_t n = 0;
   for (uint32_t i : order) {
     while (!busy.empty() && busy.top().first < iv[i].start) {
-      free_s.push(busy.top().second);
+      const uint32_t j = busy.top().second;
       busy.pop();
+      free_s[owner[j] >= 0 ? (uint32_t)owner[j] : NW].push_back(iv[j].slot);
     }
-    uint32_t s;
-    if (!free_s.empty()) {
-      s = free_s.top();
-      free_s.pop();
+    const uint32_t w = writer_warp[i];
+    uint32_t s = UINT32_MAX;
+    if (!free_s[w].empty()) {
+      s = free_s[w].back();
+      free_s[w].pop_back();
     } else {
+      for (uint32_t k = 0; k <= NW && s == UINT32_MAX; ++k) {
+        auto& f = free_s[k == 0 ? NW : k - 1];
+        if (!f.empty()) {
+          s = f.back();
+          f.pop_back();
+        }
+      }
+    }
+    if (s == UINT32_MAX) {
       s = n++;
       last_of_slot.push_back(-1);
     }
     iv[i].slot = s;
     prev[i] = last_of_slot[s];
     last_of_slot[s] = (int32_t)i;
-    busy.push({iv[i].end, s});
+    busy.push({iv[i].end, i});
   }
   return n;
 }
@@ -348,14 +365,33 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
         }
       }
       std::vector<int32_t> sprev, gprev;
-      const uint32_t n_sm = colour(sm, sprev);
+      auto owners = [&](const std::vector<Interval>& iv, std::vector<int32_t>& own,
+                        std::vector<uint32_t>& wr) {
+        own.assign(iv.size(), -1);
+        wr.resize(iv.size());
+        for (uint32_t i = 0; i < iv.size(); ++i) {
+          wr[i] = ex[iv[i].writer].warp;
+          int32_t o = (int32_t)ex[iv[i].writer].warp;  // no readers: the writer's warp
+          if (!iv[i].readers.empty()) {
+            o = (int32_t)ex[iv[i].readers[0]].warp;
+            for (uint32_t r : iv[i].readers)
+              if ((int32_t)ex[r].warp != o) o = -1;
+          }
+          own[i] = o < 0 ? -1 : o;
+        }
+      };
+      std::vector<int32_t> s_own, g_own;
+      std::vector<uint32_t> s_wr, g_wr;
+      owners(sm, s_own, s_wr);
+      const uint32_t n_sm = colour(sm, sprev, s_own, s_wr, NW);
       if (n_sm > K) {  // more temporaries than the reserve: spill more
         overshoot = n_sm - K;
         if (reserve + 1 >= K) break;  // give up on this schedule: re-schedule narrower
         reserve = std::min(K - 1, std::max(reserve * 2, reserve + 2 * overshoot + 16));
         continue;
       }
-      const uint32_t n_gm = colour(gm, gprev);
+      owners(gm, g_own, g_wr);
+      const uint32_t n_gm = colour(gm, gprev, g_own, g_wr, NW);
 
       // ---- 3. synchronisation -------------------------------------------------
       const uint32_t NE = (uint32_t)ex.size();
