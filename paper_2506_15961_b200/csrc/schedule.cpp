@@ -24,6 +24,7 @@
 #include "schedule.hpp"
 
 #include <algorithm>
+#include <deque>
 #include <queue>
 #include <set>
 #include <stdexcept>
@@ -92,8 +93,11 @@ uint32_t colour(std::vector<Interval>& iv, std::vector<int32_t>& prev,
   });
   using E = std::pair<uint64_t, uint32_t>;  // (end, interval)
   std::priority_queue<E, std::vector<E>, std::greater<E>> busy;
-  // free slots per owning warp (index NW: shared by several warps)
-  std::vector<std::vector<uint32_t>> free_s(NW + 1);
+  // free slots per owning warp (index NW: shared by several warps), in release
+  // order: the own warp's list is used LIFO (no wait either way), the others
+  // oldest-first (the longer ago a slot was released, the likelier its readers
+  // are done and the wait is free)
+  std::vector<std::deque<std::pair<uint64_t, uint32_t>>> free_s(NW + 1);
   std::vector<int32_t> last_of_slot;
   prev.assign(iv.size(), -1);
   uint32_t n = 0;
@@ -101,20 +105,22 @@ uint32_t colour(std::vector<Interval>& iv, std::vector<int32_t>& prev,
     while (!busy.empty() && busy.top().first < iv[i].start) {
       const uint32_t j = busy.top().second;
       busy.pop();
-      free_s[owner[j] >= 0 ? (uint32_t)owner[j] : NW].push_back(iv[j].slot);
+      free_s[owner[j] >= 0 ? (uint32_t)owner[j] : NW].push_back({iv[j].end, iv[j].slot});
     }
     const uint32_t w = writer_warp[i];
     uint32_t s = UINT32_MAX;
     if (!free_s[w].empty()) {
-      s = free_s[w].back();
+      s = free_s[w].back().second;
       free_s[w].pop_back();
     } else {
-      for (uint32_t k = 0; k <= NW && s == UINT32_MAX; ++k) {
-        auto& f = free_s[k == 0 ? NW : k - 1];
-        if (!f.empty()) {
-          s = f.back();
-          f.pop_back();
-        }
+      int32_t best = -1;
+      for (uint32_t k = 0; k <= NW; ++k)
+        if (!free_s[k].empty() &&
+            (best < 0 || free_s[k].front().first < free_s[best].front().first))
+          best = (int32_t)k;
+      if (best >= 0) {
+        s = free_s[best].front().second;
+        free_s[best].pop_front();
       }
     }
     if (s == UINT32_MAX) {
