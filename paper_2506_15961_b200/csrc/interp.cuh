@@ -118,6 +118,31 @@ constexpr uint32_t RING_BYTES = 0;
 constexpr uint32_t RING_BYTES = RING_RECS * 16;
 #endif
 
+__device__ __noinline__ uint2 ring_refill(const uint4* src, uint32_t base, uint32_t lane4,
+                                          uint32_t issued, uint32_t ready, uint32_t c0,
+                                          uint32_t c1) {
+  auto issue = [&]() {
+    const uint32_t r = issued * 32u;
+    const uint32_t dst = base + ((r & (RING_RECS - 1)) << 4) + lane4;
+    const char* g = reinterpret_cast<const char*>(src + r) + lane4;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n\tcp.async.commit_group;" ::"r"(dst),
+                 "l"(g)
+                 : "memory");
+    ++issued;
+  };
+  if (issued <= c0 + 1) issue();  // look-ahead: the slot of chunk c0+1 held c0-1
+  if (c1 >= ready) {
+    while (issued <= c1) issue();
+    if (issued - 1 - c1 >= 1)
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+    ready = c1 + 1;
+  }
+  return make_uint2(issued, ready);
+}
+
 struct CodeRing {
   const uint4* src;   // global start of this warp's stream
   uint32_t base;      // shared address of this warp's ring
@@ -134,21 +159,20 @@ struct CodeRing {
                  : "memory");
     ++issued;
   }
-  // make records [p, p + r) resident (r <= 33)
+  // make records [p, p + r) resident (r <= 33). The common case -- the range
+  // is in landed chunks and the look-ahead chunk is in flight -- is two
+  // compares inline; the refill is one out-of-line function shared by every
+  // call site (inlining it everywhere tripled the kernel's code size and made
+  // it miss in the instruction cache).
   __device__ __forceinline__ void ensure(uint32_t p, uint32_t r) {
 #ifdef PQW_NO_RING
     return;
 #endif
     const uint32_t c0 = p >> 5, c1 = (p + r - 1) >> 5;
-    if (issued <= c0 + 1) issue();  // look-ahead: the slot of chunk c0+1 held c0-1
-    if (c1 >= ready) {
-      while (issued <= c1) issue();
-      if (issued - 1 - c1 >= 1)
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-      else
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-      __syncwarp();
-      ready = c1 + 1;
+    if (issued <= c0 + 1 || c1 >= ready) {
+      const uint2 st = ring_refill(src, base, lane4, issued, ready, c0, c1);
+      issued = st.x;
+      ready = st.y;
     }
   }
   __device__ __forceinline__ uint4 rec(uint32_t p) const {
