@@ -58,9 +58,6 @@ thread_local uint64_t g_bundle_base = 10;  // cost-model constant per bundle (di
 uint64_t bundle_cost(const DagUnit& h, size_t n) {
   return g_bundle_base + n * op_cost(h) + (h.op == I_INV && h.guarded ? 250 : 0);
 }
-bool same_class(const DagUnit& a, const DagUnit& b) {
-  return a.op == b.op && a.fn == b.fn && a.k == b.k && !(a.op == I_INV && !(a.guarded && b.guarded));
-}
 
 struct Exec {             // one instruction bundle of a warp stream
   uint32_t warp;
@@ -173,6 +170,21 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
       for (uint32_t i = pred_off[u]; i < pred_off[u + 1]; ++i) cons[fillp[preds[i]]++] = u;
   }
 
+  // bundle classes: units of one class may share a bundle
+  std::vector<uint32_t> cls(N);
+  uint32_t n_cls = 0;
+  {
+    std::unordered_map<uint64_t, uint32_t> ids;
+    for (uint32_t u = 0; u < N; ++u) {
+      const DagUnit& d = U[u];
+      const uint64_t key = (uint64_t)d.op | ((uint64_t)d.fn << 8) | ((uint64_t)d.k << 16) |
+                           ((uint64_t)(d.op == I_INV && !d.guarded) << 40);
+      auto it = ids.find(key);
+      if (it == ids.end()) it = ids.emplace(key, n_cls++).first;
+      cls[u] = it->second;
+    }
+  }
+
   // One scheduling attempt with look-ahead window o.window and bundle width
   // o.bmax; false if the value file cannot hold even its temporaries.
   auto try_once = [&](const SchedOptions& o, Program& prog) -> bool {
@@ -183,6 +195,7 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
     std::vector<uint32_t> npred(N), bundle_of(N, 0);
     for (uint32_t u = 0; u < N; ++u) npred[u] = pred_off[u + 1] - pred_off[u];
     std::set<uint32_t> ready;
+    std::vector<std::set<uint32_t>> ready_cls(n_cls);  // the ready units of each class
     auto make_ready = [&](uint32_t u) {
       uint64_t f1 = 0;
       int32_t w1 = -1;
@@ -207,6 +220,7 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
       F2[u] = f2;
       has2[u] = h2;
       ready.insert(u);
+      ready_cls[cls[u]].insert(u);
     };
     auto est = [&](uint32_t u, uint32_t w) -> uint64_t {
       if (W1[u] < 0) return 0;
@@ -247,13 +261,17 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
       const DagUnit& H = U[head];
       cand.clear();
       cand.push_back(head);
-      for (auto j = std::next(it); j != ready.end() && *j < lim && cand.size() < o.bmax; ++j)
-        if (same_class(U[*j], H) && est(*j, w) <= t) cand.push_back(*j);
+      if (!(H.op == I_INV && !H.guarded)) {
+        const auto& rc = ready_cls[cls[head]];
+        for (auto j = rc.upper_bound(head); j != rc.end() && *j < lim && cand.size() < o.bmax; ++j)
+          if (est(*j, w) <= t) cand.push_back(*j);
+      }
       const uint64_t cost = bundle_cost(H, cand.size());
       const uint32_t bid = (uint32_t)bundles.size();
       bundles.push_back({w, t, t + cost, cand});
       for (uint32_t u : cand) {
         ready.erase(u);
+        ready_cls[cls[u]].erase(u);
         done[u] = 1;
         fin[u] = t + cost;
         wof[u] = (int32_t)w;
@@ -640,7 +658,10 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
   {
     Program cand;
     if (attempt(windows[0], cand)) {
-      const bool spills = cand.op_hist[I_FILL] + cand.op_hist[I_SPILL] != 0;
+      // a handful of spills (< 1 % of the ops) is not worth a narrower window
+      uint64_t ops = 0;
+      for (uint32_t k = 0; k < I_FILL; ++k) ops += cand.op_hist[k];
+      const bool spills = (cand.op_hist[I_FILL] + cand.op_hist[I_SPILL]) * 100 > ops;
       consider(cand);
       wi = spills ? 1 : windows.size();
     } else {

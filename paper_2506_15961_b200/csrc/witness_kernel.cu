@@ -2,6 +2,7 @@
 // extern "C" API of include/planeq_witness.h (compile, upload, launch, results,
 // probe). The device interpreter lives in interp.cuh.
 #include <cuda_runtime.h>
+#include <malloc.h>
 #include <sched.h>
 
 #include <algorithm>
@@ -177,6 +178,15 @@ int pqw_device_count(void) {
 
 int pqw_engine_create(int device, uint64_t seed, const uint64_t fn_keys[3], pqw_engine** out) {
   if (!out || !fn_keys) return fail(PQW_EINVAL, "null argument");
+  {
+    // the compiler allocates and frees large scratch vectors per program on
+    // many threads: keep them in the heap instead of mmap/munmap round trips
+    static std::once_flag once;
+    std::call_once(once, [] {
+      mallopt(M_MMAP_THRESHOLD, 512 << 20);
+      mallopt(M_TRIM_THRESHOLD, 1 << 30);
+    });
+  }
   auto* e = new pqw_engine();
   e->device = device;
   e->seed = seed;
