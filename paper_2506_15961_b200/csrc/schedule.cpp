@@ -668,7 +668,22 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
       wi = 1;
     }
   }
-  // (sequential: the engine already compiles distinct programs on parallel threads)
+  if (opt.parallel_attempts && have && wi < windows.size()) {
+    // idle host threads: try the remaining (>= 384) windows concurrently
+    std::vector<uint32_t> rest;
+    for (size_t i = wi; i < windows.size(); ++i)
+      if (windows[i] >= 384) rest.push_back(windows[i]);
+    std::vector<Program> cands(rest.size());
+    std::vector<char> oks(rest.size(), 0);
+    std::vector<std::thread> th;
+    for (size_t i = 1; i < rest.size(); ++i)
+      th.emplace_back([&, i]() { oks[i] = attempt(rest[i], cands[i]); });
+    if (!rest.empty()) oks[0] = attempt(rest[0], cands[0]);
+    for (auto& t : th) t.join();
+    for (size_t i = 0; i < rest.size(); ++i)
+      if (oks[i]) consider(cands[i]);
+    wi = windows.size();
+  }
   for (; wi < windows.size(); ++wi) {
     if (have && windows[wi] < 384) break;  // tiny windows: last resort only
     Program cand;
