@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define PQW_ABI_VERSION 2
+#define PQW_ABI_VERSION 3
 #define PQW_PRIME 2147483647u /* 2^31 - 1 */
 
 /* error codes */
@@ -47,6 +47,7 @@ extern "C" {
 #define PQW_STAGE_PAR_DIV0 3      /* parallel side divides by a constant zero      */
 #define PQW_STAGE_LOG_DIV0 4      /* logical side divides by a constant zero       */
 #define PQW_STAGE_BAD_INDEX 5     /* embedding id outside its table                 */
+#define PQW_STAGE_PENDING 6       /* pqw_stage_add: not compiled yet (pqw_stage_status) */
 
 /* tensor-op program opcodes (pqw_stage_add ir stream) */
 enum pqw_top {
@@ -122,24 +123,33 @@ int pqw_engine_create(int device, uint64_t seed, const uint64_t fn_keys[3],
 void pqw_engine_destroy(pqw_engine* e);
 
 /*
- * Compile one stage's tensor-op program (stream layout documented in
- * paper_2506_15961_b200/lower.py). consts: n_consts triples
+ * Add one stage's tensor-op program (stream layout documented in
+ * paper_2506_15961_b200/stages.py). consts: n_consts triples
  * (residue, exact_num, exact_den) -- exact_den == 0 marks an inexact constant.
- * var_keys: per-variable 64-bit keys. out_status[0] = PQW_STAGE_*,
- * out_status[1] = info (obligation id for REFUTED_CONST / BAD_INDEX),
- * out_status[2] = obligation count, out_status[3] = obligations closed by value
- * numbering, out_status[4] = residual obligations, out_status[5] = bytecode
- * length in records, out_status[6] = shared-memory slots, out_status[7] = max numerator degree of a
- * residual obligation (saturating), out_status[8..9] = lhs/rhs residues of the
- * REFUTED_CONST obligation, out_status[10..11] = their exact integer values
- * (INT64_MIN when not an exact integer), out_status[12] = field ops executed
- * per witness, out_status[13] = variables, out_status[14] = global spill
- * slots, out_status[15] = instruction bundles.
- * Returns the stage index (>= 0) or a negative error.
+ * var_keys: per-variable 64-bit keys. Identical programs are recognised here
+ * (they compile once); the compilation itself is deferred and runs, spread over
+ * host threads, at the first pqw_stage_status / pqw_upload / inspection call.
+ * out_status[0] = PQW_STAGE_PENDING, out_status[13] = variables.
+ * Returns the stage index (>= 0) or a negative error (malformed header).
  */
 int pqw_stage_add(pqw_engine* e, const int32_t* ir, size_t ir_len,
                   const int64_t* consts, size_t n_consts,
                   const uint64_t* var_keys, size_t n_vars, int64_t out_status[16]);
+
+/*
+ * Compile status of a stage (compiles every pending stage first):
+ * out_status[0] = PQW_STAGE_*, out_status[1] = info (obligation id for
+ * REFUTED_CONST / BAD_INDEX), out_status[2] = obligation count, out_status[3] =
+ * obligations closed by value numbering, out_status[4] = residual obligations,
+ * out_status[7] = max numerator degree of a residual obligation (saturating),
+ * out_status[8..9] = lhs/rhs residues of the REFUTED_CONST obligation,
+ * out_status[10..11] = their exact integer values (INT64_MIN when not an exact
+ * integer), out_status[13] = variables; once the GPU program exists (after
+ * pqw_upload): out_status[5] = program records, out_status[6] = shared-memory
+ * slots, out_status[12] = field ops per witness, out_status[14] = global spill
+ * slots, out_status[15] = instruction bundles.
+ */
+int pqw_stage_status(pqw_engine* e, int stage, int64_t out_status[16]);
 
 /* Drop every compiled stage (device image included). */
 int pqw_reset(pqw_engine* e);

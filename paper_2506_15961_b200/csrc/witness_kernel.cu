@@ -47,6 +47,12 @@ struct pqw_engine {
   uint64_t seed = 0;
   uint64_t fn_keys[3] = {0, 0, 0};
   std::vector<pqw::CompiledStage> stages;
+  // deferred front ends: per stage, the stage it duplicates (-1: compile its
+  // own text, kept in cache_src) and its var base; front_done once compiled
+  std::vector<int> alias;
+  std::vector<uint32_t> pend_nvars, pend_base;
+  std::vector<char> front_done;
+  size_t n_front_pending = 0;
   std::vector<uint64_t> var_keys;
   // program cache: text hash -> first stage compiled from it (+ its source for exact compare)
   std::unordered_map<uint64_t, size_t> cache;
@@ -119,7 +125,15 @@ using pqw::fail;
 
 // Run the compiler back end of every pending program, spread over host threads
 // (identical programs share one back end). PQW_THREADS caps the thread count.
+extern "C" {
+static int finalize_front(pqw_engine* e);
+}
+
 static int finalize_all(pqw_engine* e) {
+  {
+    int rc = finalize_front(e);
+    if (rc != PQW_OK) return rc;
+  }
   std::vector<pqw::CompiledStage*> todo;
   std::unordered_map<const pqw::StageBackend*, int> seen;
   for (auto& st : e->stages)
@@ -235,60 +249,125 @@ int pqw_stage_add(pqw_engine* e, const int32_t* ir, size_t ir_len, const int64_t
   if (!e || !ir || !out_status) return fail(PQW_EINVAL, "null argument");
   if (n_vars && !var_keys) return fail(PQW_EINVAL, "null var_keys");
   if (n_consts && !consts) return fail(PQW_EINVAL, "null consts");
+  if (ir_len < 4 || ir[0] != 0x50515701) return fail(PQW_EINVAL, "stage compile: bad program magic");
   const uint32_t base = (uint32_t)e->var_keys.size();
+  const int idx = (int)e->stages.size();
   // identical programs (e.g. the same layer repeated) compile once: the cache
-  // key is the program text; a hit shares the bytecode and only rebases vars
+  // key is the program text; a hit shares the compiled program and only
+  // rebases vars. The compilation itself is deferred: every distinct program
+  // is compiled on a host thread pool at the first pqw_stage_status,
+  // pqw_upload or inspection call.
   uint64_t h = pqw::mix64(0x5157ull ^ ir_len ^ ((uint64_t)n_consts << 32) ^ ((uint64_t)n_vars << 48));
   for (size_t i = 0; i < ir_len; ++i) h = pqw::mix64(h + (uint32_t)ir[i]);
   for (size_t i = 0; i < 3 * n_consts; ++i) h = pqw::mix64(h + (uint64_t)consts[i]);
-  pqw::CompiledStage st;
-  bool hit = false;
+  int alias = -1;
   auto it = e->cache.find(h);
   if (it != e->cache.end()) {
     const auto& ent = e->cache_src[it->second];
     if (ent.first.size() == ir_len && std::equal(ent.first.begin(), ent.first.end(), ir) &&
         ent.second.size() == 3 * n_consts &&
         std::equal(ent.second.begin(), ent.second.end(), consts)) {
-      st = e->stages[it->second];
-      st.var_base = base;
-      hit = true;
+      alias = (int)it->second;
       e->cache_hits++;
     }
   }
-  if (!hit) {
-    try {
-      st = pqw::compile_stage(ir, ir_len, consts, n_consts, (uint32_t)n_vars, base, e->fn_keys,
-                              e->fast_slots, e->n_warps, e->sched);
-    } catch (const std::exception& ex) {
-      return fail(PQW_EINVAL, std::string("stage compile: ") + ex.what());
-    }
-    if (it == e->cache.end()) {
-      e->cache.emplace(h, e->stages.size());
-      e->cache_src[e->stages.size()] = {std::vector<int32_t>(ir, ir + ir_len),
-                                        std::vector<int64_t>(consts, consts + 3 * n_consts)};
-    }
+  if (alias < 0) {
+    if (it == e->cache.end()) e->cache.emplace(h, (size_t)idx);
+    e->cache_src[(size_t)idx] = {std::vector<int32_t>(ir, ir + ir_len),
+                                 std::vector<int64_t>(consts, consts + 3 * n_consts)};
   }
+  e->stages.emplace_back();
+  e->alias.push_back(alias);
+  e->pend_nvars.push_back((uint32_t)n_vars);
+  e->pend_base.push_back(base);
+  e->front_done.push_back(0);
+  e->n_front_pending++;
   e->var_keys.insert(e->var_keys.end(), var_keys, var_keys + n_vars);
+  for (int i = 0; i < 16; ++i) out_status[i] = 0;
+  out_status[0] = PQW_STAGE_PENDING;
+  out_status[13] = (int64_t)n_vars;
+  e->uploaded = false;
+  return idx;
+}
+
+// Compile the front ends of every pending stage (distinct programs on host
+// threads, duplicates copy their original and rebase their vars).
+static int finalize_front(pqw_engine* e) {
+  if (!e->n_front_pending) return PQW_OK;
+  std::vector<size_t> todo;
+  for (size_t i = 0; i < e->stages.size(); ++i)
+    if (!e->front_done[i] && e->alias[i] < 0) todo.push_back(i);
+  unsigned nt = std::max(1u, std::thread::hardware_concurrency());
+  {
+    cpu_set_t cs;
+    if (sched_getaffinity(0, sizeof(cs), &cs) == 0) nt = std::max(1, CPU_COUNT(&cs));
+  }
+  if (const char* s = getenv("PQW_THREADS")) nt = std::max(1, atoi(s));
+  nt = std::max(1u, std::min<unsigned>(nt, (unsigned)todo.size()));
+  std::atomic<size_t> next{0};
+  std::mutex err_mu;
+  std::string err;
+  auto work = [&]() {
+    for (;;) {
+      const size_t k = next.fetch_add(1);
+      if (k >= todo.size()) return;
+      const size_t i = todo[k];
+      const auto& src = e->cache_src.at(i);
+      try {
+        e->stages[i] = pqw::compile_stage(src.first.data(), src.first.size(), src.second.data(),
+                                          src.second.size() / 3, e->pend_nvars[i], e->pend_base[i],
+                                          e->fn_keys, e->fast_slots, e->n_warps, e->sched);
+        e->front_done[i] = 1;
+      } catch (const std::exception& ex) {
+        std::lock_guard<std::mutex> g(err_mu);
+        if (err.empty()) err = "stage " + std::to_string(i) + " compile: " + ex.what();
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < nt; ++t) pool.emplace_back(work);
+  work();
+  for (auto& t : pool) t.join();
+  if (!err.empty()) return fail(PQW_EINVAL, err);
+  for (size_t i = 0; i < e->stages.size(); ++i) {
+    if (e->front_done[i]) continue;
+    e->stages[i] = e->stages[(size_t)e->alias[i]];
+    e->stages[i].var_base = e->pend_base[i];
+    e->front_done[i] = 1;
+  }
+  e->n_front_pending = 0;
+  return PQW_OK;
+}
+
+int pqw_stage_status(pqw_engine* e, int stage, int64_t out_status[16]) {
+  if (!e || !out_status) return fail(PQW_EINVAL, "null argument");
+  if (stage < 0 || (size_t)stage >= e->stages.size()) return fail(PQW_EINVAL, "bad stage");
+  {
+    int rc = finalize_front(e);
+    if (rc != PQW_OK) return rc;
+  }
+  const auto& st = e->stages[stage];
   for (int i = 0; i < 16; ++i) out_status[i] = 0;
   out_status[0] = st.status;
   out_status[1] = st.info;
   out_status[2] = st.n_obligations;
   out_status[3] = st.n_fast;
   out_status[4] = st.n_residual;
-  out_status[5] = 0;  // program size, slots, spills, bundles: known after finalization
-  out_status[6] = 0;
   out_status[7] = (int64_t)std::min<uint64_t>(st.degree, (uint64_t)INT64_MAX);
   out_status[8] = st.const_lhs;
   out_status[9] = st.const_rhs;
   out_status[10] = st.exact_lhs;
   out_status[11] = st.exact_rhs;
-  out_status[12] = 0;
   out_status[13] = st.n_vars;
-  out_status[14] = 0;
-  out_status[15] = 0;
-  e->stages.push_back(std::move(st));
-  e->uploaded = false;
-  return (int)(e->stages.size() - 1);
+  if (st.status == PQW_STAGE_OK && st.be->ready) {
+    const auto& pr = st.prog();
+    out_status[5] = (int64_t)pr.code.size();
+    out_status[6] = pr.n_slots;
+    out_status[12] = (int64_t)(pr.cls[0] + pr.cls[1] + pr.cls[2] + pr.cls[3] + pr.cls[4]);
+    out_status[14] = pr.n_spill;
+    out_status[15] = pr.n_bundles;
+  }
+  return PQW_OK;
 }
 
 int pqw_reset(pqw_engine* e) {
@@ -298,6 +377,11 @@ int pqw_reset(pqw_engine* e) {
     e->free_device();
   }
   e->stages.clear();
+  e->alias.clear();
+  e->pend_nvars.clear();
+  e->pend_base.clear();
+  e->front_done.clear();
+  e->n_front_pending = 0;
   e->var_keys.clear();
   e->cache.clear();
   e->cache_src.clear();
@@ -309,6 +393,10 @@ int pqw_reset(pqw_engine* e) {
 
 long pqw_stage_bytecode(pqw_engine* e, int stage, pqw_ins* out, size_t cap, uint32_t* n_slots) {
   if (!e || stage < 0 || (size_t)stage >= e->stages.size()) return fail(PQW_EINVAL, "bad stage");
+  {
+    int rc = finalize_front(e);
+    if (rc != PQW_OK) return rc;
+  }
   const auto& st = e->stages[stage];
   try {
     pqw::finalize_stage(e->stages[stage]);
@@ -323,6 +411,10 @@ long pqw_stage_bytecode(pqw_engine* e, int stage, pqw_ins* out, size_t cap, uint
 
 long pqw_obligation_support(pqw_engine* e, int stage, uint32_t obl, uint32_t* out, size_t cap) {
   if (!e || stage < 0 || (size_t)stage >= e->stages.size()) return fail(PQW_EINVAL, "bad stage");
+  {
+    int rc = finalize_front(e);
+    if (rc != PQW_OK) return rc;
+  }
   const auto& st = e->stages[stage];
   auto vars = pqw::obligation_support(st, obl);
   if (out)

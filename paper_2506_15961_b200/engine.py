@@ -18,7 +18,7 @@ from .errors import EngineError, EngineUnavailable
 
 LIB_NAME = "libplaneq_witness.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 # PQW_STAGE_* codes
 STAGE_OK = 0
@@ -27,6 +27,7 @@ STAGE_REFUTED_CONST = 2
 STAGE_PAR_DIV0 = 3
 STAGE_LOG_DIV0 = 4
 STAGE_BAD_INDEX = 5
+STAGE_PENDING = 6
 
 # bytecode opcodes (pqw_bop)
 BOP_NAMES = ("END", "DOT", "SUM", "SUB", "NEG", "HASH", "INV", "VAR", "CONST", "CHK", "DEN",
@@ -36,7 +37,7 @@ IMAGE_STATS_LEN = 14 + N_BOPS
 FIELD_CLASSES = ("mul", "add", "hash", "inv", "cmp")
 
 EXPORTS = ("pqw_abi_version", "pqw_last_error", "pqw_device_count", "pqw_engine_create",
-           "pqw_engine_destroy", "pqw_stage_add", "pqw_reset", "pqw_stage_bytecode",
+           "pqw_engine_destroy", "pqw_stage_add", "pqw_stage_status", "pqw_reset", "pqw_stage_bytecode",
            "pqw_obligation_support", "pqw_upload", "pqw_launch", "pqw_results", "pqw_probe",
            "pqw_last_launch_ms", "pqw_image_stats", "pqw_peak_fieldops")
 
@@ -75,6 +76,8 @@ def load_library(path: str | None = None):
     lib.pqw_stage_add.argtypes = [C.c_void_p, i32p, C.c_size_t, i64p, C.c_size_t, u64p,
                                   C.c_size_t, i64p]
     lib.pqw_stage_add.restype = C.c_int
+    lib.pqw_stage_status.argtypes = [C.c_void_p, C.c_int, i64p]
+    lib.pqw_stage_status.restype = C.c_int
     lib.pqw_reset.argtypes = [C.c_void_p]
     lib.pqw_reset.restype = C.c_int
     lib.pqw_stage_bytecode.argtypes = [C.c_void_p, C.c_int, C.POINTER(_Ins), C.c_size_t, u32p]
@@ -144,6 +147,23 @@ class StageCompile:
     bundles: int = 0
 
 
+class _LazyStage:
+    """StageCompile of a queued stage, fetched (compiling every pending stage
+    of the engine at once) on first attribute access."""
+
+    __slots__ = ("_eng", "index", "_sc")
+
+    def __init__(self, eng: "Engine", index: int):
+        self._eng = eng
+        self.index = index
+        self._sc = None
+
+    def __getattr__(self, name):
+        if self._sc is None:
+            self._sc = self._eng.stage_status(self.index)
+        return getattr(self._sc, name)
+
+
 class Engine:
     """One engine = one compiled device image of many stages on one GPU."""
 
@@ -183,7 +203,10 @@ class Engine:
         self.close()
 
     # -- compile ---------------------------------------------------------------
-    def add_stage(self, ir: np.ndarray, consts: np.ndarray, var_keys: np.ndarray) -> StageCompile:
+    def add_stage(self, ir: np.ndarray, consts: np.ndarray, var_keys: np.ndarray) -> "StageCompile":
+        """Queue one stage; compilation is deferred (all distinct programs are
+        compiled together on host threads). The returned object resolves its
+        fields through pqw_stage_status on first access."""
         ir = np.ascontiguousarray(ir, dtype=np.int32)
         consts = np.ascontiguousarray(consts, dtype=np.int64).reshape(-1)
         var_keys = np.ascontiguousarray(var_keys, dtype=np.uint64)
@@ -192,6 +215,11 @@ class Engine:
             self._h, _ptr(ir, C.c_int32), ir.size, _ptr(consts, C.c_int64), consts.size // 3,
             _ptr(var_keys, C.c_uint64), var_keys.size, _ptr(st, C.c_int64)))
         self.n_stages += 1
+        return _LazyStage(self, idx)
+
+    def stage_status(self, idx: int) -> StageCompile:
+        st = np.zeros(16, dtype=np.int64)
+        self._check(self.lib.pqw_stage_status(self._h, idx, _ptr(st, C.c_int64)))
         imin = np.iinfo(np.int64).min
         return StageCompile(index=idx, status=int(st[0]), info=int(st[1]),
                             obligations=int(st[2]), fast=int(st[3]), residual=int(st[4]),
