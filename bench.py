@@ -179,6 +179,19 @@ class PortPool:
         self.pool.join()
 
 
+def traffic_bytes(args, desc):
+    """DRAM bytes per eval_kernel launch (read + write) from the committed ncu
+    --set full capture of this workload (profiles/traffic.json), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+    except (OSError, ValueError):
+        return None
+    if not desc.startswith(t.get("workload", "?")) or t.get("witnesses") != args.witnesses:
+        return None
+    return int(t["dram_bytes_read"]) + int(t["dram_bytes_write"])
+
+
 # -- main -----------------------------------------------------------------------
 
 
@@ -340,7 +353,7 @@ def main():
                     if e2e_parts else None},
             "roofline": {"bound": "int", "achieved": round(achieved / 1e9, 3),
                          "peak": round(peak / 1e9, 3), "unit": "Gfieldop/s",
-                         "frac": round(achieved / peak, 4), "traffic": None,
+                         "frac": round(achieved / peak, 4), "traffic": traffic_bytes(args, desc),
                          "peak_source": "measured register-resident F_p mul/add/hash kernels "
                                         "(pqw_peak_fieldops) weighted by this image's op mix",
                          "kernel_ms": round(kern_s * 1e3, 4)},
