@@ -185,6 +185,15 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
     }
   }
 
+  // bottom level: the cost-model length of the longest path from a unit to
+  // the end of the program (critical-path priority among eligible units)
+  std::vector<uint64_t> blevel(N, 0);
+  for (uint32_t u = N; u-- > 0;) {
+    uint64_t m = 0;
+    for (uint32_t i = cons_off[u]; i < cons_off[u + 1]; ++i) m = std::max(m, blevel[cons[i]]);
+    blevel[u] = m + op_cost(U[u]);
+  }
+
   // One scheduling attempt with look-ahead window o.window and bundle width
   // o.bmax; false if the value file cannot hold even its temporaries.
   auto try_once = [&](const SchedOptions& o, Program& prog) -> bool {
@@ -257,14 +266,23 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
         T[w] = tnext == INF ? t + 1 : std::max(t + 1, tnext);
         continue;
       }
-      const uint32_t head = *it;
+      uint32_t head = *it;
+      if (o.pick_scan) {
+        // among the next few eligible units, the one on the longest remaining path
+        uint32_t seen = 0;
+        for (auto j = std::next(it); j != ready.end() && *j < lim && seen < o.pick_scan; ++j)
+          if (est(*j, w) <= t) {
+            ++seen;
+            if (blevel[*j] > blevel[head]) head = *j;
+          }
+      }
       const DagUnit& H = U[head];
       cand.clear();
       cand.push_back(head);
       if (!(H.op == I_INV && !H.guarded)) {
         const auto& rc = ready_cls[cls[head]];
-        for (auto j = rc.upper_bound(head); j != rc.end() && *j < lim && cand.size() < o.bmax; ++j)
-          if (est(*j, w) <= t) cand.push_back(*j);
+        for (auto j = rc.begin(); j != rc.end() && *j < lim && cand.size() < o.bmax; ++j)
+          if (*j != head && est(*j, w) <= t) cand.push_back(*j);
       }
       const uint64_t cost = bundle_cost(H, cand.size());
       const uint32_t bid = (uint32_t)bundles.size();

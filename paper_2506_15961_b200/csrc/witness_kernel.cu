@@ -228,6 +228,7 @@ int pqw_engine_create(int device, uint64_t seed, const uint64_t fn_keys[3], pqw_
   env("PQW_BUNDLE_BASE", 0, 1 << 20, e->sched.bundle_base);
   env("PQW_SPILL_COST", 0, 1 << 20, e->sched.spill_cost);
   env("PQW_SLEEP", 0, 100000, e->sleep_ns);
+  env("PQW_PICK", 0, 1 << 20, e->sched.pick_scan);
   *out = e;
   return PQW_OK;
 }
