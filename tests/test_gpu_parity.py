@@ -110,3 +110,63 @@ def test_verify_plan_end_to_end_matches_reference(gpu):
         if rep["verdict"] == "refuted" and rep.get("counterexample", {}).get("witness") is not None:
             cx = rep["counterexample"]
             assert cx["lhs_value"] != cx["rhs_value"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n_w", [1, 33, 4096])
+def test_witness_counts_at_edge_sizes(gpu, n_w):
+    """One witness, a ragged single-lane last tile, and many tiles per stage:
+    outcomes equal the oracle's on the same witness list."""
+    seed = 17
+    rec = next(r for r in RECS if r["name"] == "dp2tp2pp2nm2.wrong_scaling.8")
+    plan = load_plan(rec["work_plan"])
+    stages, _ = build_stages(plan)
+    owner = shard_owner(plan, entry_order(plan))
+    eng = Engine(0, seed, F.fn_keys(seed))
+    comps = [eng.add_stage(*(lambda lw: (lw.ir, lw.consts, lw.var_keys))(
+        lower_stage(plan, st, owner, seed))) for st in stages]
+    eng.upload()
+    eng.launch(n_w)
+    fb, nv, nb = eng.results()
+    wit = np.arange(min(n_w, 512), dtype=np.uint64)
+    for st, c in zip(stages, comps):
+        if c.status != STAGE_OK:
+            continue
+        if n_w <= 512:
+            o = check_stage(plan, st, owner, seed, wit)
+            assert (int(nv[c.index]), int(nb[c.index])) == (o.valid, o.bad), st.target
+            want = 0xFFFFFFFFFFFFFFFF if o.first_bad is None else \
+                (o.first_bad[0] << 32) | o.first_bad[1]
+            assert int(fb[c.index]) == want, st.target
+        else:
+            # counts are monotone in the witness range; the first failure of
+            # the 4096-witness run lies in the oracle's first 512 if any does
+            o = check_stage(plan, st, owner, seed, wit)
+            assert int(nv[c.index]) >= o.valid and int(nb[c.index]) >= o.bad
+            if o.first_bad is not None:
+                assert int(fb[c.index]) == (o.first_bad[0] << 32) | o.first_bad[1]
+    eng.close()
+
+
+@pytest.mark.gpu
+def test_engine_with_no_gpu_stage(gpu):
+    """A plan whose every stage closes at compile time uploads and launches an
+    empty image without error."""
+    rec = next(r for r in RECS if r["name"] == "tp2")
+    plan = load_plan(rec["work_plan"])
+    stages, _ = build_stages(plan)
+    owner = shard_owner(plan, entry_order(plan))
+    eng = Engine(0, 1, F.fn_keys(1))
+    n_ok = 0
+    for st in stages:
+        lw = lower_stage(plan, st, owner, 1)
+        c = eng.add_stage(lw.ir, lw.consts, lw.var_keys)
+        if c.status == STAGE_OK:
+            eng.reset()
+            continue
+        n_ok += 1
+    eng.upload()
+    eng.launch(64)
+    fb, nv, nb = eng.results()
+    assert len(fb) == eng.n_stages
+    eng.close()
