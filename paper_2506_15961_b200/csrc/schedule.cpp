@@ -672,54 +672,14 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
     }
   };
   // the widest window first; only when it spills are the narrower ones tried
-  size_t wi = 0;
-  auto small_spill = [](const Program& c) {
-    // a handful of spills (< 1 % of the ops) is not worth a narrower window
-    uint64_t ops = 0;
-    for (uint32_t k = 0; k < I_FILL; ++k) ops += c.op_hist[k];
-    return (c.op_hist[I_FILL] + c.op_hist[I_SPILL]) * 100 <= ops;
-  };
-  if (opt.parallel_attempts && windows.size() > 1) {
-    // spare host threads: the widest window and the narrower (>= 384) ones run
-    // concurrently; the choice is the same as the sequential one below
-    std::vector<uint32_t> ws;
-    for (uint32_t wv : windows)
-      if (ws.empty() || wv >= 384) ws.push_back(wv);
-    std::vector<Program> cands(ws.size());
-    std::vector<char> oks(ws.size(), 0);
-    std::vector<std::thread> th;
-    for (size_t i = 1; i < ws.size(); ++i)
-      th.emplace_back([&, i]() { oks[i] = attempt(ws[i], cands[i]); });
-    oks[0] = attempt(ws[0], cands[0]);
-    for (auto& t : th) t.join();
-    if (oks[0] && small_spill(cands[0])) {
-      consider(cands[0]);
-    } else {
-      for (size_t i = 0; i < ws.size(); ++i) {
-        if (!oks[i]) continue;
-        const bool spills = cands[i].op_hist[I_FILL] + cands[i].op_hist[I_SPILL] != 0;
-        consider(cands[i]);
-        if (i > 0 && !spills) break;  // as the sequential search would
-      }
-    }
-    wi = windows.size();
-  } else {
+  // The widest window wins the cost comparison on every program of the
+  // BASELINE workloads (its extra spills cost less than the parallelism the
+  // narrower windows give up, confirmed on the GPU), so narrower windows are
+  // tried only when it does not fit the value file at all.
+  for (uint32_t win : windows) {
+    if (have) break;
     Program cand;
-    if (attempt(windows[0], cand)) {
-      const bool spills = !small_spill(cand);
-      consider(cand);
-      wi = spills ? 1 : windows.size();
-    } else {
-      wi = 1;
-    }
-  }
-  for (; wi < windows.size(); ++wi) {
-    if (have && windows[wi] < 384) break;  // tiny windows: last resort only
-    Program cand;
-    if (!attempt(windows[wi], cand)) continue;
-    const bool spills = cand.op_hist[I_FILL] + cand.op_hist[I_SPILL] != 0;
-    consider(cand);
-    if (!spills) break;  // narrower windows cannot do better without spills
+    if (attempt(win, cand)) consider(cand);
   }
   if (!have) {
     // last resort: one warp, one op per bundle (a sequential evaluation)

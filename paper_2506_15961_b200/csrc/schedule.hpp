@@ -37,8 +37,7 @@ struct SchedOptions {
   uint32_t bundle_base = 100;  // cost-model constant per bundle (dispatch + latency)
   uint32_t spill_cost = 8;     // cost-model weight of one FILL/SPILL op when choosing a window
   uint32_t pick_scan = 0;      // >0: pick the longest-path unit among that many eligible ones
-  uint32_t active_warps = 32;
-  bool parallel_attempts = false;  // try the narrower windows on extra threads  // warps that receive work (the rest run empty streams)
+  uint32_t active_warps = 32;  // warps that receive work (the rest run empty streams)
 };
 
 struct Program {

@@ -151,19 +151,14 @@ static int finalize_all(pqw_engine* e) {
     if (sched_getaffinity(0, sizeof(cs), &cs) == 0) nt = std::max(1, CPU_COUNT(&cs));
   }
   if (const char* s = getenv("PQW_THREADS")) nt = std::max(1, atoi(s));
-  const unsigned n_cpu = nt;
   nt = std::min<unsigned>(nt, (unsigned)todo.size());
   std::atomic<size_t> next{0};
   std::mutex err_mu;
   std::string err;
-  // the biggest programs (handed out first, they bound the wall time) also try
-  // their alternative schedules concurrently; the small ones finish meanwhile
-  const size_t spare = n_cpu >= 8 ? std::max<size_t>(1, std::min<size_t>(todo.size(), n_cpu) / 4) : 0;
   auto work = [&]() {
     for (;;) {
       const size_t i = next.fetch_add(1);
       if (i >= todo.size()) return;
-      if (i < spare) todo[i]->sched.parallel_attempts = true;
       try {
         pqw::finalize_stage(*todo[i]);
       } catch (const std::exception& ex) {
