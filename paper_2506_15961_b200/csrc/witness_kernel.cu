@@ -253,9 +253,24 @@ int pqw_stage_add(pqw_engine* e, const int32_t* ir, size_t ir_len, const int64_t
   // rebases vars. The compilation itself is deferred: every distinct program
   // is compiled on a host thread pool at the first pqw_stage_status,
   // pqw_upload or inspection call.
-  uint64_t h = pqw::mix64(0x5157ull ^ ir_len ^ ((uint64_t)n_consts << 32) ^ ((uint64_t)n_vars << 48));
-  for (size_t i = 0; i < ir_len; ++i) h = pqw::mix64(h + (uint32_t)ir[i]);
-  for (size_t i = 0; i < 3 * n_consts; ++i) h = pqw::mix64(h + (uint64_t)consts[i]);
+  // (a cheap multiply-xorshift over 64-bit words: this runs over every stage's
+  // text, the full mix only finalises)
+  auto absorb = [](uint64_t h, uint64_t w) {
+    h = (h ^ w) * 0x9E3779B97F4A7C15ull;
+    return h ^ (h >> 29);
+  };
+  uint64_t h = 0x5157ull ^ ir_len ^ ((uint64_t)n_consts << 32) ^ ((uint64_t)n_vars << 48);
+  {
+    size_t i = 0;
+    for (; i + 2 <= ir_len; i += 2) {
+      uint64_t w;
+      std::memcpy(&w, ir + i, 8);
+      h = absorb(h, w);
+    }
+    if (i < ir_len) h = absorb(h, (uint32_t)ir[i]);
+    for (size_t j = 0; j < 3 * n_consts; ++j) h = absorb(h, (uint64_t)consts[j]);
+    h = pqw::mix64(h);
+  }
   int alias = -1;
   auto it = e->cache.find(h);
   if (it != e->cache.end()) {
