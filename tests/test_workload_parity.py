@@ -89,3 +89,48 @@ def test_bug_injected_llama3_8b_is_refuted_with_the_oracles_counterexample(gpu):
         o = check_stage(mutant, st, owner, 3, np.arange(64, dtype=np.uint64))
         assert o.first_bad == (cx["witness"], cx["obligation"]), cat
         assert (str(o.lhs), str(o.rhs)) == (cx["lhs_value"], cx["rhs_value"]), cat
+
+
+def _full_records():
+    import glob
+    import json
+    import os
+    from golden_io import GOLDEN
+    return [json.load(open(p)) for p in sorted(glob.glob(os.path.join(GOLDEN, "verdicts_full_*.json")))]
+
+
+FULL = _full_records()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rec", FULL, ids=[r["name"] for r in FULL])
+def test_full_workload_stage_verdicts_match_reference(gpu, rec):
+    """Every stage of a full BASELINE workload: the engine's verdict equals the
+    reference's own (its bundled solver, all stages, tests/golden/
+    verdicts_full_*.json); stages the reference left undecided must be decided."""
+    import hashlib
+    from paper_2506_15961_b200.plan import dumps
+    from paper_2506_15961_b200.verify import VerifyOptions, discharge
+    _desc, plan = get_workload(rec["name"])
+    assert hashlib.sha256(dumps(plan).encode()).hexdigest() == rec["plan_sha256"], \
+        "the generator no longer reproduces the plan the reference verified"
+    stages, _ = build_stages(plan)
+    results, cancelled, _ = discharge(plan, stages, VerifyOptions(no_cancel=True, witnesses=256))
+    assert cancelled == 0
+    want = [tuple(x) for x in rec["stage_status"]]
+    assert [r.target for r in results] == [t for t, _ in want]
+    for r, (target, status) in zip(results, want):
+        if status in ("proven", "refuted"):
+            assert r.status == status, target
+        else:
+            assert r.status in ("proven", "refuted"), target
+
+
+@pytest.mark.parametrize("rec", FULL, ids=[r["name"] for r in FULL])
+def test_full_workload_generator_reproduces_the_verified_plan(rec):
+    """CPU: the generator still emits, byte for byte, the plan whose stage
+    verdicts the reference computed (so the GPU comparison is meaningful)."""
+    import hashlib
+    from paper_2506_15961_b200.plan import dumps
+    _desc, plan = get_workload(rec["name"])
+    assert hashlib.sha256(dumps(plan).encode()).hexdigest() == rec["plan_sha256"]
