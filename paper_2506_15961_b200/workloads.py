@@ -75,6 +75,9 @@ GENERATED = {
                                                    "8 routed experts + 1 shared) TP=EP=4 PP=4 DP=2 "
                                                    "nm=2 SP, shape-reduced", family="deepseek-v3"),
     # small members of the same families (tests)
+    "deepseek-6l-tp4pp2dp2-ep": LlamaPlanSpec(6, tp=4, pp=2, dp=2, nm=2, sp=True,
+                                              desc="6-layer DeepSeek-style decoder (3 dense + 3 MoE), "
+                                                   "TP=EP=4 PP=2 DP=2 nm=2 SP", family="deepseek-v3"),
     "deepseek-2l-tp2dp2-sp": LlamaPlanSpec(2, tp=2, pp=1, dp=2, nm=1, sp=True,
                                            desc="2-layer DeepSeek-style decoder (1 dense + 1 MoE), "
                                                 "TP=EP=2 DP=2 SP", family="deepseek-v3"),
