@@ -59,3 +59,46 @@ def test_malformed_program_is_rejected(lib):
         e.add_stage(np.array([1, 2, 3], dtype=np.int32), np.zeros((0, 3), np.int64),
                     np.zeros(0, np.uint64))
     e.close()
+
+
+def test_compilation_is_deferred_and_status_resolves(lib):
+    """pqw_stage_add only queues the program (status PENDING); the first
+    status query compiles every pending stage; identical texts share one
+    compiled program."""
+    import ctypes as C
+    import numpy as np
+    from paper_2506_15961_b200.stages import IR_MAGIC, OPCODE, T_CHECK, T_VARS
+    consts = np.array([[2, 2, 1]], dtype=np.int64)
+    ir = np.array([IR_MAGIC, 3, 4, 2, 1, 2, 1, 2, 1, 2,
+                   T_VARS, 0, 1, 1, 0, 0,
+                   OPCODE["add"], 2, 1, 0, 0, 0, 1,
+                   OPCODE["scale"], 1, 1, 1, 0, 2, 0,
+                   T_CHECK, 2, 0, 1, 1, 2, 0], dtype=np.int32)
+    e = engine.Engine(0, 1, (1, 2, 3))
+    raw = np.zeros(16, dtype=np.int64)
+    keys = np.array([5, 6], dtype=np.uint64)
+    idx = e.lib.pqw_stage_add(e._h, ir.ctypes.data_as(C.POINTER(C.c_int32)), ir.size,
+                              consts.ctypes.data_as(C.POINTER(C.c_int64)), 1,
+                              keys.ctypes.data_as(C.POINTER(C.c_uint64)), 2,
+                              raw.ctypes.data_as(C.POINTER(C.c_int64)))
+    assert idx == 0 and raw[0] == engine.STAGE_PENDING and raw[13] == 2
+    e.n_stages += 1
+    dup = e.add_stage(ir, consts, keys)              # same text: a cache hit
+    a, b = e.stage_status(0), dup
+    assert a.status == b.status and a.obligations == b.obligations == 2
+    assert e.image_stats()["cache_hits"] == 1
+    e.close()
+
+
+def test_front_end_errors_surface_at_status(lib):
+    import numpy as np
+    import pytest
+    from paper_2506_15961_b200.errors import EngineError
+    from paper_2506_15961_b200.stages import IR_MAGIC
+    e = engine.Engine(0, 1, (1, 2, 3))
+    # a valid header followed by a truncated op stream
+    c = e.add_stage(np.array([IR_MAGIC, 1, 1, 0, 1, 2, 99], dtype=np.int32),
+                    np.zeros((0, 3), np.int64), np.zeros(0, np.uint64))
+    with pytest.raises(EngineError):
+        _ = c.status
+    e.close()
