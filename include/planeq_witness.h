@@ -17,7 +17,9 @@
  * failing witness is an exact integer counterexample.
  *
  * All entry points return 0 on success and a negative PQW_E* code on failure;
- * pqw_last_error() describes the last failure on the calling thread.
+ * pqw_last_error() describes the last failure on the calling thread. An engine
+ * is not thread-safe: call it from one thread at a time (it parallelises its
+ * own compilation internally). Engines on different devices are independent.
  * No torch types cross this boundary: plain pointers and sizes only.
  */
 #ifndef PLANEQ_WITNESS_H
