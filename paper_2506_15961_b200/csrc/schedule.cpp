@@ -329,29 +329,102 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
 
     // ---- 2. allocation: choose spills, then colour exactly -------------------
     const uint32_t K = o.smem_slots;
-    // the reserve for FILL/SPILL temporaries grows by what the last colouring
-    // overshot (each extra spilled value frees about one slot)
-    uint32_t overshoot = 0;
-    for (uint32_t reserve = 0;;) {
+    // the distinct bundles reading each value (CSR)
+    std::vector<uint32_t> rdb_off(N + 1, 0), rdb;
+    {
+      std::vector<uint32_t> rd;
+      for (uint32_t u = 0; u < N; ++u) {
+        rd.clear();
+        for (uint32_t i = cons_off[u]; i < cons_off[u + 1]; ++i) rd.push_back(bundle_of[cons[i]]);
+        std::sort(rd.begin(), rd.end());
+        rd.erase(std::unique(rd.begin(), rd.end()), rd.end());
+        rdb.insert(rdb.end(), rd.begin(), rd.end());
+        rdb_off[u + 1] = (uint32_t)rdb.size();
+      }
+    }
+    // slots the exact colouring below will need for a spill choice: the most
+    // shared-memory intervals alive at once (a slot frees strictly after its
+    // interval's end), without building the intervals themselves
+    std::vector<uint64_t> events;
+    auto slots_needed = [&](const std::vector<uint8_t>& spilled) -> uint32_t {
+      events.clear();
+      auto add = [&](uint64_t a, uint64_t b) {  // [a, b]; a start sorts before an end at the same time
+        events.push_back(a << 1);
+        events.push_back((b << 1) | 1);
+      };
+      for (uint32_t v : values) {
+        const uint32_t bdef = bundle_of[v];
+        if (!spilled[v]) {
+          add(vdef[v], vend[v]);
+        } else {
+          add(vdef[v], rend(bdef) + 1);
+          for (uint32_t i = rdb_off[v]; i < rdb_off[v + 1]; ++i) add(bts[rdb[i]] - 1, rend(rdb[i]));
+        }
+      }
+      std::sort(events.begin(), events.end());
+      uint32_t live = 0, most = 0;
+      for (uint64_t e : events) {
+        if (e & 1) {
+          --live;
+        } else {
+          most = std::max(most, ++live);
+        }
+      }
+      return most;
+    };
+    // the reserve for FILL/SPILL temporaries grows until the spill choice for
+    // K - reserve resident values fits the value file with its temporaries
+    uint32_t overshoot = 0, tries = 0;
+    for (uint32_t reserve = 0;; ++tries) {
       std::vector<uint8_t> spilled(N, 0);
       {
+        // sweep in definition order keeping at most keff values resident;
+        // when full, the resident value (or the new one) that ends last is
+        // spilled. Two heaps over (end, value) with lazy deletion: the earliest
+        // end expires, the latest end is evicted.
         const uint32_t keff = K - reserve;
-        std::set<std::pair<uint64_t, uint32_t>> active;
+        using E = std::pair<uint64_t, uint32_t>;
+        std::priority_queue<E, std::vector<E>, std::greater<E>> by_first;
+        std::priority_queue<E> by_last;
+        std::vector<uint8_t> gone(N, 0);  // expired or evicted
+        uint32_t n_active = 0;
         for (uint32_t v : values) {
-          while (!active.empty() && active.begin()->first < vdef[v]) active.erase(active.begin());
-          if (active.size() < keff) {
-            active.insert({vend[v], v});
-          } else {
-            auto last = std::prev(active.end());
-            if (last->first > vend[v]) {
-              spilled[last->second] = 1;
-              active.erase(last);
-              active.insert({vend[v], v});
-            } else {
-              spilled[v] = 1;
+          while (!by_first.empty() && by_first.top().first < vdef[v]) {
+            const uint32_t x = by_first.top().second;
+            by_first.pop();
+            if (!gone[x]) {
+              gone[x] = 1;
+              n_active--;
             }
           }
+          while (!by_last.empty() && gone[by_last.top().second]) by_last.pop();
+          if (n_active < keff) {
+            by_first.push({vend[v], v});
+            by_last.push({vend[v], v});
+            n_active++;
+          } else if (by_last.top().first > vend[v]) {
+            const uint32_t x = by_last.top().second;
+            by_last.pop();
+            gone[x] = 1;
+            spilled[x] = 1;
+            by_first.push({vend[v], v});
+            by_last.push({vend[v], v});
+          } else {
+            spilled[v] = 1;
+          }
         }
+      }
+      uint32_t n_sm = slots_needed(spilled);
+      if (n_sm > K) {  // more temporaries than the reserve: spill more
+        overshoot = n_sm - K;
+        if (reserve + 1 >= K) break;  // give up on this schedule: re-schedule narrower
+        // step by the overshoot (each step spills about what the last one
+        // overshot; the slot count is not monotone in the reserve, so small
+        // steps land closer to the least reserve that fits); double after a
+        // few steps to bound the search
+        const uint32_t step = 2 * overshoot + 16;
+        reserve = std::min(K - 1, tries < 4 ? reserve + step : std::max(reserve * 2, reserve + step));
+        continue;
       }
       // exec bundles: [FILL] main [SPILL] per main bundle
       std::vector<Exec> ex;
@@ -378,16 +451,13 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
       std::vector<Interval> sm, gm;
       std::vector<uint32_t> v_iv(N, ~0u), v_giv(N, ~0u);
       std::unordered_map<uint64_t, uint32_t> fill_iv;  // (bundle << 32 | value) -> interval
-      std::vector<uint32_t> rd;
       for (uint32_t v : values) {
         const uint32_t bdef = bundle_of[v];
-        rd.clear();
-        for (uint32_t i = cons_off[v]; i < cons_off[v + 1]; ++i) rd.push_back(bundle_of[cons[i]]);
-        std::sort(rd.begin(), rd.end());
-        rd.erase(std::unique(rd.begin(), rd.end()), rd.end());
+        const uint32_t* rd0 = rdb.data() + rdb_off[v];
+        const uint32_t* rd1 = rdb.data() + rdb_off[v + 1];
         if (!spilled[v]) {
           Interval I{vdef[v], vend[v], (uint32_t)main_exec[bdef], {}};
-          for (uint32_t b : rd) I.readers.push_back((uint32_t)main_exec[b]);
+          for (const uint32_t* b = rd0; b != rd1; ++b) I.readers.push_back((uint32_t)main_exec[*b]);
           v_iv[v] = (uint32_t)sm.size();
           sm.push_back(std::move(I));
         } else {
@@ -395,7 +465,8 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
           v_iv[v] = (uint32_t)sm.size();
           sm.push_back(std::move(T1));
           Interval G{vdef[v] + 1, rend(bdef) + 1, (uint32_t)spill_of[bdef], {}};
-          for (uint32_t b : rd) {
+          for (const uint32_t* pb = rd0; pb != rd1; ++pb) {
+            const uint32_t b = *pb;
             G.end = std::max(G.end, bts[b]);
             G.readers.push_back((uint32_t)fill_of[b]);
             Interval Fi{bts[b] - 1, rend(b), (uint32_t)fill_of[b], {(uint32_t)main_exec[b]}};
@@ -425,13 +496,8 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
       std::vector<int32_t> s_own, g_own;
       std::vector<uint32_t> s_wr, g_wr;
       owners(sm, s_own, s_wr);
-      const uint32_t n_sm = colour(sm, sprev, s_own, s_wr, NW);
-      if (n_sm > K) {  // more temporaries than the reserve: spill more
-        overshoot = n_sm - K;
-        if (reserve + 1 >= K) break;  // give up on this schedule: re-schedule narrower
-        reserve = std::min(K - 1, std::max(reserve * 2, reserve + 2 * overshoot + 16));
-        continue;
-      }
+      n_sm = colour(sm, sprev, s_own, s_wr, NW);
+      if (n_sm > K) fail("internal: colouring needs more slots than the interval count");
       owners(gm, g_own, g_wr);
       const uint32_t n_gm = colour(gm, gprev, g_own, g_wr, NW);
 
