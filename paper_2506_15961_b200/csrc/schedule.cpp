@@ -372,48 +372,49 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
       }
       return most;
     };
-    // the reserve for FILL/SPILL temporaries grows until the spill choice for
-    // K - reserve resident values fits the value file with its temporaries
-    uint32_t overshoot = 0, tries = 0;
-    for (uint32_t reserve = 0;; ++tries) {
-      std::vector<uint8_t> spilled(N, 0);
-      {
-        // sweep in definition order keeping at most keff values resident;
-        // when full, the resident value (or the new one) that ends last is
-        // spilled. Two heaps over (end, value) with lazy deletion: the earliest
-        // end expires, the latest end is evicted.
-        const uint32_t keff = K - reserve;
-        using E = std::pair<uint64_t, uint32_t>;
-        std::priority_queue<E, std::vector<E>, std::greater<E>> by_first;
-        std::priority_queue<E> by_last;
-        std::vector<uint8_t> gone(N, 0);  // expired or evicted
-        uint32_t n_active = 0;
-        for (uint32_t v : values) {
-          while (!by_first.empty() && by_first.top().first < vdef[v]) {
-            const uint32_t x = by_first.top().second;
-            by_first.pop();
-            if (!gone[x]) {
-              gone[x] = 1;
-              n_active--;
-            }
-          }
-          while (!by_last.empty() && gone[by_last.top().second]) by_last.pop();
-          if (n_active < keff) {
-            by_first.push({vend[v], v});
-            by_last.push({vend[v], v});
-            n_active++;
-          } else if (by_last.top().first > vend[v]) {
-            const uint32_t x = by_last.top().second;
-            by_last.pop();
+    // spill choice for `keff` resident values: sweep in definition order
+    // keeping at most keff values resident; when full, the resident value (or
+    // the new one) that ends last is spilled. Two heaps over (end, value) with
+    // lazy deletion: the earliest end expires, the latest end is evicted.
+    auto select = [&](uint32_t keff, std::vector<uint8_t>& spilled) {
+      spilled.assign(N, 0);
+      using E = std::pair<uint64_t, uint32_t>;
+      std::priority_queue<E, std::vector<E>, std::greater<E>> by_first;
+      std::priority_queue<E> by_last;
+      std::vector<uint8_t> gone(N, 0);  // expired or evicted
+      uint32_t n_active = 0;
+      for (uint32_t v : values) {
+        while (!by_first.empty() && by_first.top().first < vdef[v]) {
+          const uint32_t x = by_first.top().second;
+          by_first.pop();
+          if (!gone[x]) {
             gone[x] = 1;
-            spilled[x] = 1;
-            by_first.push({vend[v], v});
-            by_last.push({vend[v], v});
-          } else {
-            spilled[v] = 1;
+            n_active--;
           }
         }
+        while (!by_last.empty() && gone[by_last.top().second]) by_last.pop();
+        if (n_active < keff) {
+          by_first.push({vend[v], v});
+          by_last.push({vend[v], v});
+          n_active++;
+        } else if (by_last.top().first > vend[v]) {
+          const uint32_t x = by_last.top().second;
+          by_last.pop();
+          gone[x] = 1;
+          spilled[x] = 1;
+          by_first.push({vend[v], v});
+          by_last.push({vend[v], v});
+        } else {
+          spilled[v] = 1;
+        }
       }
+    };
+    // the reserve for FILL/SPILL temporaries grows until the spill choice for
+    // K - reserve resident values fits the value file with its temporaries
+    uint32_t overshoot = 0, tries = 0, last_fail = 0;
+    for (uint32_t reserve = 0;; ++tries) {
+      std::vector<uint8_t> spilled;
+      select(K - reserve, spilled);
       uint32_t n_sm = slots_needed(spilled);
       if (n_sm > K) {  // more temporaries than the reserve: spill more
         overshoot = n_sm - K;
@@ -423,8 +424,27 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
         // steps land closer to the least reserve that fits); double after a
         // few steps to bound the search
         const uint32_t step = 2 * overshoot + 16;
+        last_fail = reserve;
         reserve = std::min(K - 1, tries < 4 ? reserve + step : std::max(reserve * 2, reserve + step));
         continue;
+      }
+      // a step can overshoot the least reserve that fits by far (every
+      // reserved slot is a value spilled); bisect back towards the last
+      // failing reserve while the value file is left well under-used
+      if (tries > 0) {
+        std::vector<uint8_t> cand;
+        for (int r = 0; r < 2 && reserve - last_fail > 32 && K - n_sm > 32; ++r) {
+          const uint32_t mid = last_fail + (reserve - last_fail) / 2;
+          select(K - mid, cand);
+          const uint32_t n = slots_needed(cand);
+          if (n <= K) {
+            reserve = mid;
+            n_sm = n;
+            spilled.swap(cand);
+          } else {
+            last_fail = mid;
+          }
+        }
       }
       // exec bundles: [FILL] main [SPILL] per main bundle
       std::vector<Exec> ex;
