@@ -59,6 +59,27 @@ uint64_t bundle_cost(const DagUnit& h, size_t n) {
   return g_bundle_base + n * op_cost(h) + (h.op == I_INV && h.guarded ? 250 : 0);
 }
 
+// Set of unit ids in [0, n) as a bit vector: ordered iteration from any id
+// by word scans (the list scheduler walks its ready sets in priority order).
+struct IdSet {
+  std::vector<uint64_t> w;
+  uint32_t n = 0;
+  explicit IdSet(uint32_t n_ = 0) : w((n_ + 63) / 64, 0), n(n_) {}
+  void insert(uint32_t i) { w[i >> 6] |= 1ull << (i & 63); }
+  void erase(uint32_t i) { w[i >> 6] &= ~(1ull << (i & 63)); }
+  // first member >= i, or n
+  uint32_t next(uint32_t i) const {
+    if (i >= n) return n;
+    size_t k = i >> 6;
+    uint64_t m = w[k] & (~0ull << (i & 63));
+    while (!m) {
+      if (++k == w.size()) return n;
+      m = w[k];
+    }
+    return (uint32_t)(k * 64 + __builtin_ctzll(m));
+  }
+};
+
 struct Exec {             // one instruction bundle of a warp stream
   uint32_t warp;
   uint64_t ts;
@@ -203,8 +224,8 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
     std::vector<uint8_t> has2(N, 0), done(N, 0);
     std::vector<uint32_t> npred(N), bundle_of(N, 0);
     for (uint32_t u = 0; u < N; ++u) npred[u] = pred_off[u + 1] - pred_off[u];
-    std::set<uint32_t> ready;
-    std::vector<std::set<uint32_t>> ready_cls(n_cls);  // the ready units of each class
+    IdSet ready(N);
+    std::vector<IdSet> ready_cls(n_cls, IdSet(N));  // the ready units of each class
     auto make_ready = [&](uint32_t u) {
       uint64_t f1 = 0;
       int32_t w1 = -1;
@@ -254,35 +275,36 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
       for (uint32_t i = 1; i < std::min(NW, o.active_warps); ++i)
         if (T[i] < T[w]) w = i;
       const uint64_t t = T[w];
-      const uint64_t lim = (uint64_t)frontier + o.window;
-      auto it = ready.begin();
+      // unit ids below lim are in the window (every ready unit is >= frontier)
+      const uint32_t lim = (uint32_t)std::min<uint64_t>((uint64_t)frontier + o.window, N);
+      uint32_t head = ready.next(frontier);
       uint64_t tnext = INF;
-      for (; it != ready.end() && *it < lim; ++it) {
-        const uint64_t e = est(*it, w);
+      for (; head < lim; head = ready.next(head + 1)) {
+        const uint64_t e = est(head, w);
         if (e <= t) break;
         tnext = std::min(tnext, e);
       }
-      if (it == ready.end() || *it >= lim) {
+      if (head >= lim) {
         T[w] = tnext == INF ? t + 1 : std::max(t + 1, tnext);
         continue;
       }
-      uint32_t head = *it;
       if (o.pick_scan) {
         // among the next few eligible units, the one on the longest remaining path
         uint32_t seen = 0;
-        for (auto j = std::next(it); j != ready.end() && *j < lim && seen < o.pick_scan; ++j)
-          if (est(*j, w) <= t) {
+        const uint32_t first = head;
+        for (uint32_t j = ready.next(first + 1); j < lim && seen < o.pick_scan; j = ready.next(j + 1))
+          if (est(j, w) <= t) {
             ++seen;
-            if (blevel[*j] > blevel[head]) head = *j;
+            if (blevel[j] > blevel[head]) head = j;
           }
       }
       const DagUnit& H = U[head];
       cand.clear();
       cand.push_back(head);
       if (!(H.op == I_INV && !H.guarded)) {
-        const auto& rc = ready_cls[cls[head]];
-        for (auto j = rc.begin(); j != rc.end() && *j < lim && cand.size() < o.bmax; ++j)
-          if (*j != head && est(*j, w) <= t) cand.push_back(*j);
+        const IdSet& rc = ready_cls[cls[head]];
+        for (uint32_t j = rc.next(frontier); j < lim && cand.size() < o.bmax; j = rc.next(j + 1))
+          if (j != head && est(j, w) <= t) cand.push_back(j);
       }
       const uint64_t cost = bundle_cost(H, cand.size());
       const uint32_t bid = (uint32_t)bundles.size();
