@@ -167,15 +167,21 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
   std::vector<uint32_t> pred_off(N + 1, 0), preds;
   std::vector<uint32_t> ncons(N, 0);
   {
-    std::vector<uint32_t> tmp;
+    std::vector<uint32_t> tmp, stamp(N, UINT32_MAX);
     for (uint32_t u = 0; u < N; ++u) {
       const DagUnit& d = U[u];
       if ((uint64_t)d.arg0 + d.nargs > dag.pool.size()) fail("operand list out of range");
-      tmp.assign(dag.pool.begin() + d.arg0, dag.pool.begin() + d.arg0 + d.nargs);
-      std::sort(tmp.begin(), tmp.end());
-      tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
-      for (uint32_t p : tmp) {
+      tmp.clear();  // distinct operands (dedup by stamp, then sort the few left)
+      for (uint32_t i = 0; i < d.nargs; ++i) {
+        const uint32_t p = dag.pool[d.arg0 + i];
         if (p >= u) fail("operand defined after its use");
+        if (stamp[p] != u) {
+          stamp[p] = u;
+          tmp.push_back(p);
+        }
+      }
+      std::sort(tmp.begin(), tmp.end());
+      for (uint32_t p : tmp) {
         if (!U[p].defines()) fail("operand is not a value");
         preds.push_back(p);
         ncons[p]++;
@@ -354,12 +360,17 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
     // the distinct bundles reading each value (CSR)
     std::vector<uint32_t> rdb_off(N + 1, 0), rdb;
     {
-      std::vector<uint32_t> rd;
+      std::vector<uint32_t> rd, seen(bundles.size(), UINT32_MAX);
       for (uint32_t u = 0; u < N; ++u) {
         rd.clear();
-        for (uint32_t i = cons_off[u]; i < cons_off[u + 1]; ++i) rd.push_back(bundle_of[cons[i]]);
+        for (uint32_t i = cons_off[u]; i < cons_off[u + 1]; ++i) {
+          const uint32_t b = bundle_of[cons[i]];
+          if (seen[b] != u) {
+            seen[b] = u;
+            rd.push_back(b);
+          }
+        }
         std::sort(rd.begin(), rd.end());
-        rd.erase(std::unique(rd.begin(), rd.end()), rd.end());
         rdb.insert(rdb.end(), rd.begin(), rd.end());
         rdb_off[u + 1] = (uint32_t)rdb.size();
       }
@@ -433,7 +444,7 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
     };
     // the reserve for FILL/SPILL temporaries grows until the spill choice for
     // K - reserve resident values fits the value file with its temporaries
-    uint32_t overshoot = 0, tries = 0, last_fail = 0;
+    uint32_t overshoot = 0, tries = 0, last_fail = 0, prev_n = 0;
     for (uint32_t reserve = 0;; ++tries) {
       std::vector<uint8_t> spilled;
       select(K - reserve, spilled);
@@ -441,6 +452,11 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
       if (n_sm > K) {  // more temporaries than the reserve: spill more
         overshoot = n_sm - K;
         if (reserve + 1 >= K) break;  // give up on this schedule: re-schedule narrower
+        // past half the value file, a step that won back less than the
+        // remaining overshoot means the temporaries of this schedule's bundles
+        // alone nearly fill it: give up early as well
+        if (tries >= 2 && reserve > K / 2 && (uint64_t)n_sm + overshoot > prev_n) break;
+        prev_n = n_sm;
         // step by the overshoot (each step spills about what the last one
         // overshot; the slot count is not monotone in the reserve, so small
         // steps land closer to the least reserve that fits); double after a
