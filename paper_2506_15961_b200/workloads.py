@@ -83,7 +83,20 @@ GENERATED = {
                                                 "TP=EP=2 DP=2 SP", family="deepseek-v3"),
     "llama-4l-tp2pp2dp2-sp": LlamaPlanSpec(4, tp=2, pp=2, dp=2, nm=2, sp=True,
                                            desc="4-layer Llama-style decoder, TP=2 PP=2 DP=2 nm=2 SP"),
+    # configs[3]'s parallel shape (TP=8 PP=16 DP=2 nm=2, one layer per pipeline
+    # stage) at 16 layers: the same stage programs as the 126-layer sweep,
+    # small enough for the reference to verify every stage
+    "llama3-405b-16l-tp8pp16dp2": LlamaPlanSpec(16, tp=8, pp=16, dp=2, nm=2, sp=False,
+                                                desc="Llama3-405B-shaped (16 layers, GQA) TP=8 PP=16 "
+                                                     "DP=2 nm=2, shape-reduced"),
+    # mid-size MoE member the reference can finish: 3 dense + 1 MoE layer
+    "deepseek-4l-tp4pp2dp2-ep": LlamaPlanSpec(4, tp=4, pp=2, dp=2, nm=2, sp=True,
+                                              desc="4-layer DeepSeek-style decoder (3 dense + 1 MoE), "
+                                                   "TP=EP=4 PP=2 DP=2 nm=2 SP", family="deepseek-v3"),
 }
+# bug-injected variants: "<workload>~<fault category>" picks one site of that
+# category with a name-seeded RNG (BASELINE configs[2] on the full Llama3-8B)
+FAULT_SEP = "~"
 DEFAULT = "llama3-8b-tp4pp2dp2-sp"
 
 
@@ -121,9 +134,26 @@ def _fixture(fname: str) -> Plan:
         return loads(f.read())
 
 
+def fault_site(plan: Plan, name: str, category: str):
+    """The fault site a "<workload>~<category>" name denotes (deterministic)."""
+    import random
+    from .faults import list_sites
+    sites = list_sites(plan, category)
+    if not sites:
+        raise KeyError(f"workload {name!r} has no {category!r} fault site")
+    return random.Random(f"{name}{FAULT_SEP}{category}").choice(sites)
+
+
 def get_workload(name: str = "default") -> tuple[str, Plan]:
     if name == "default":
         name = DEFAULT
+    if FAULT_SEP in name:
+        from .faults import inject
+        base, category = name.split(FAULT_SEP, 1)
+        desc, plan = get_workload(base)
+        site = fault_site(plan, base, category)
+        return (f"{name}: {desc.split(': ', 1)[-1]}; injected {category} at {site.site}",
+                inject(plan, site))
     if name in FIXTURES:
         fname, desc = FIXTURES[name]
         return f"{name}: {desc}", _fixture(fname)
