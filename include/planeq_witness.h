@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define PQW_ABI_VERSION 3
+#define PQW_ABI_VERSION 4
 #define PQW_PRIME 2147483647u /* 2^31 - 1 */
 
 /* error codes */
@@ -41,6 +41,8 @@ extern "C" {
 #define PQW_ENODEV (-2)   /* no CUDA device or driver */
 #define PQW_ECUDA (-3)    /* CUDA runtime failure */
 #define PQW_ESTATE (-4)   /* call out of order (e.g. run before compile) */
+#define PQW_EPLAN (-5)    /* plan not well formed: the host's own checks raise the
+                             reference's exception for it (pqw_plan_* only) */
 
 /* per-stage compile status (pqw_stage_add out_status[0]) */
 #define PQW_STAGE_OK 0            /* residual obligations go to the GPU            */
@@ -101,7 +103,7 @@ typedef struct pqw_ins {
 } pqw_ins;
 
 /* entries of pqw_image_stats */
-#define PQW_IMAGE_STATS_LEN (14 + PQW_B_NUM_OPS)
+#define PQW_IMAGE_STATS_LEN (16 + PQW_B_NUM_OPS)
 
 typedef struct pqw_engine pqw_engine;
 
@@ -153,6 +155,16 @@ int pqw_stage_add(pqw_engine* e, const int32_t* ir, size_t ir_len,
  */
 int pqw_stage_status(pqw_engine* e, int stage, int64_t out_status[16]);
 
+/* Restrict scheduling and upload to the stages flagged in `active` (one flag
+ * per queued stage; default: all). Front ends still run for every stage, so a
+ * multi-GPU host can cost every stage once and schedule only its share. */
+int pqw_stage_select(pqw_engine* e, const uint8_t* active, size_t n);
+
+/* Device cost of a stage after the compiler front end (compiles every pending
+ * front end first): scheduling units of its residual cones, 0 for a stage
+ * decided at compile time. Negative on error. */
+int64_t pqw_stage_cost(pqw_engine* e, int stage);
+
 /* Drop every compiled stage (device image included). */
 int pqw_reset(pqw_engine* e);
 
@@ -203,8 +215,10 @@ int pqw_last_launch_ms(pqw_engine* e, float* ms);
  * image after sharing identical programs, out[5 + N] = compile-cache hits,
  * out[6 + N .. 10 + N] = field ops per witness by class (multiplies, adds,
  * keyed hashes, inversions, compares), out[11 + N] = max global spill slots
- * of a stage, out[12 + N] = bundles, out[13 + N] = cross-warp waits
- * (N = PQW_B_NUM_OPS). */
+ * of a stage, out[12 + N] = bundles, out[13 + N] = cross-warp waits,
+ * out[14 + N] = bytes the last pqw_upload copied to the device, out[15 + N] =
+ * bytes pqw_results reads back (N = PQW_B_NUM_OPS). Only stages selected by
+ * pqw_stage_select count. */
 int pqw_image_stats(pqw_engine* e, uint64_t* out, size_t cap);
 
 /* Measured integer-pipe ceiling of this device: field ops per second of
@@ -212,6 +226,105 @@ int pqw_image_stats(pqw_engine* e, uint64_t* out, size_t cap);
  * F_p adds, out[2] = keyed-hash evaluations, out[3] = inversions. The
  * roofline denominator of the interpreter (bench.py). */
 int pqw_peak_fieldops(int device, double out[4]);
+
+
+/* ---------------------------------------------------------------------------
+ * Native plan core: stage construction and lowering behind the C-ABI.
+ *
+ * Replaces, for the verify pipeline, the host-side work the reference does
+ * per plan and per stage before any decision is taken:
+ *   pkg/src/planeq/shapes.py:35-45   validate_concrete (shape rule per node)
+ *   pkg/src/planeq/stages.py:79-88   entry_order
+ *   pkg/src/planeq/stages.py:91-138  build_stages (lineage-cut backward slices)
+ *   pkg/src/planeq/graph.py:96-150   topo_sort (tie-break: device, seq, id)
+ *   pkg/src/planeq/stages.py:144-176 + :267-340  interface construction and
+ *                                    obligations of run_stage
+ * A plan is handed over once as flat arrays (names as NUL-terminated UTF-8
+ * strings, resolved here); stages are lowered into the same tensor-op
+ * programs pqw_stage_add takes (paper_2506_15961_b200/stages.py lower_stage
+ * emits the identical stream) on host threads and queued into an engine.
+ * Anything not well formed returns PQW_EPLAN: the caller's own host checks
+ * then raise the reference's exception with the reference's message.
+ * ------------------------------------------------------------------------- */
+
+/* One dataflow graph. Strings are concatenations of NUL-terminated names. */
+typedef struct pqw_graph_desc {
+  int64_t n_tensors;
+  const char* tensor_names;    /* n_tensors names (graph.tensors order)            */
+  const int32_t* tensor_ndim;  /* rank per tensor                                  */
+  const int64_t* tensor_dims;  /* concatenated shapes                              */
+  const uint8_t* tensor_flags; /* bit 0: dtype "int"; bit 1: meta.enum == "position" */
+  int64_t n_nodes;
+  const char* node_ids;        /* n_nodes ids (graph.nodes order)                  */
+  const int32_t* node_kind;    /* pqw_top opcode of the kind, -1 = unknown kind    */
+  const int32_t* node_nin;     /* inputs per node                                  */
+  const int32_t* node_nout;    /* outputs per node                                 */
+  const char* node_inputs;     /* all input names, node-major                      */
+  const char* node_outputs;    /* all output names, node-major                     */
+  const int32_t* node_nattr;   /* encoded attribute words per node (see stages.py) */
+  const int64_t* node_attrs;   /* concatenated                                     */
+  const int32_t* node_device;  /* -1 = None                                        */
+  const int64_t* node_seq;
+  int64_t n_inputs;
+  const char* input_names;     /* graph.inputs                                     */
+} pqw_graph_desc;
+
+/* Lineage: checkpoint entries (dict order) and their shards. */
+typedef struct pqw_lineage_desc {
+  int64_t n_entries;
+  const char* logical_names;   /* logical tensor id per entry                      */
+  const uint8_t* mode;         /* 0 = full, 1 = partial, 2 = anything else         */
+  const int32_t* n_shards;     /* shards per entry                                 */
+  const char* shard_names;     /* parallel tensor per shard, entry-major           */
+  const int32_t* shard_ndim;   /* ranges per shard                                 */
+  const int64_t* ranges;       /* (lo, hi) pairs, concatenated                     */
+} pqw_lineage_desc;
+
+typedef struct pqw_plan pqw_plan;
+
+/* Copy a plan in. consts: n_consts triples (residue, exact_num, exact_den) --
+ * the plan's distinct rational attributes (scale factor, shift addend, full
+ * value), referenced from node_attrs by index. */
+int pqw_plan_create(const pqw_graph_desc* logical, const pqw_graph_desc* parallel,
+                    const pqw_lineage_desc* lineage, const int64_t* consts, size_t n_consts,
+                    pqw_plan** out);
+void pqw_plan_destroy(pqw_plan* p);
+
+/* Structural checks and the concrete shape rule of every node of both graphs
+ * (validate_concrete). PQW_EPLAN when anything is off. */
+int pqw_plan_validate(pqw_plan* p);
+
+/* build_stages: out[0] = stages, out[1] = uncovered logical nodes, out[2] =
+ * uncovered parallel nodes. PQW_EPLAN when stage construction would raise
+ * (it does not require pqw_plan_validate: the reference builds the stages of
+ * a reduced plan without re-validating it). */
+int pqw_plan_build_stages(pqw_plan* p, int64_t out[3]);
+
+/* Stage `stage`: target (logical tensor index, graph.tensors order). */
+int pqw_plan_stage_target(pqw_plan* p, int stage);
+
+/* Node indices of a stage's logical (side 0) or parallel (side 1) slice in
+ * the stage's topological order; side 2 / 3: its logical / parallel boundary
+ * tensors (Stage.l_inputs / p_inputs, sorted by name). Returns the count,
+ * copies at most cap. */
+long pqw_plan_stage_nodes(pqw_plan* p, int stage, int side, int32_t* out, size_t cap);
+
+/* Nodes owned by no stage (side 0 logical, 1 parallel), sorted by id. */
+long pqw_plan_uncovered(pqw_plan* p, int side, int32_t* out, size_t cap);
+
+/* Lower the stages listed in `stages` (n of them; NULL = all, in order) with
+ * variables keyed by `seed` and queue them into `e` (pqw_stage_add). out_index
+ * (length n) receives each stage's engine index, or PQW_EPLAN for a stage whose
+ * lowering raises in the reference (the host re-lowers it to raise). Lowering
+ * runs on host threads (PQW_THREADS caps them). */
+int pqw_plan_add_stages(pqw_plan* p, pqw_engine* e, uint64_t seed, const int32_t* stages,
+                        size_t n, int32_t* out_index);
+
+/* The tensor-op program of one stage (what pqw_plan_add_stages queues): lens[0]
+ * = ir words, lens[1] = const triples, lens[2] = variables; copies what fits. */
+int pqw_plan_stage_program(pqw_plan* p, int stage, uint64_t seed, int32_t* ir, size_t ir_cap,
+                           int64_t* consts, size_t consts_cap, uint64_t* var_keys,
+                           size_t vk_cap, int64_t lens[3]);
 
 #ifdef __cplusplus
 }

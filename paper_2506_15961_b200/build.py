@@ -9,7 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libplaneq_witness.so")
-SOURCES = ["compiler.cpp", "schedule.cpp", "witness_kernel.cu"]
+SOURCES = ["compiler.cpp", "schedule.cpp", "plan.cpp", "witness_kernel.cu"]
 HEADERS = ["compiler.hpp", "field.hpp", "isa.hpp", "schedule.hpp", "interp.cuh"]
 
 

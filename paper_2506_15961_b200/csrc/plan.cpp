@@ -1,0 +1,1299 @@
+// plan.cpp -- native plan core: stage construction and lowering (pqw_plan_* C-ABI).
+//
+// What the reference does on the host before deciding anything, per plan and
+// per stage, done once here over flat arrays:
+//   validate_concrete  pkg/src/planeq/shapes.py:35-45 (shape rule of every node,
+//                      rules of ops.py:100-909 as restated in opshape.py)
+//   entry_order        pkg/src/planeq/stages.py:79-88
+//   build_stages       pkg/src/planeq/stages.py:91-138 (backward slices cut at
+//                      checkpoints, graph.py:303-328; topo order graph.py:96-150)
+//   stage lowering     pkg/src/planeq/stages.py:144-176 + :267-340 (interface,
+//                      both sub-DFGs, obligations) -- emits, word for word, the
+//                      tensor-op program paper_2506_15961_b200/stages.py
+//                      lower_stage emits, so pqw_stage_add cannot tell them apart.
+// Any input the reference would reject yields PQW_EPLAN; the Python host then
+// runs its own checks, which raise the reference's exception and message.
+#include <sched.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <queue>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/planeq_witness.h"
+#include "field.hpp"
+
+namespace pqw {
+int set_last_error(int code, const std::string& msg);  // witness_kernel.cu (pqw_last_error)
+namespace {
+
+int pfail(int code, const std::string& msg) { return set_last_error(code, msg); }
+
+struct PlanError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+constexpr int32_t IR_MAGIC = 0x50515701;
+
+// encoded attribute layouts (paper_2506_15961_b200/native.py pack_attrs)
+bool is_elementwise2(int k) {
+  return k == PQW_T_ADD || k == PQW_T_SUB || k == PQW_T_MUL || k == PQW_T_DIV ||
+         k == PQW_T_DROPOUT || k == PQW_T_SILU_GRAD;
+}
+bool is_unary(int k) {
+  return k == PQW_T_IDENTITY || k == PQW_T_SCALE || k == PQW_T_SHIFT || k == PQW_T_POW ||
+         k == PQW_T_RSQRT || k == PQW_T_SILU || k == PQW_T_MOVE;
+}
+bool is_comm(int k) {
+  return k == PQW_T_ALL_REDUCE || k == PQW_T_ALL_GATHER || k == PQW_T_REDUCE_SCATTER ||
+         k == PQW_T_ALL_TO_ALL;
+}
+
+int64_t pymod(int64_t a, int64_t m) {
+  int64_t r = a % m;
+  return r < 0 ? r + m : r;
+}
+
+void split_names(const char* s, int64_t n, std::string& store, std::vector<std::string_view>& out) {
+  // copy the NUL-separated names once, then view into the copy
+  size_t len = 0;
+  for (int64_t i = 0; i < n; ++i) len += std::strlen(s + len) + 1;
+  store.assign(s, len);
+  out.resize((size_t)n);
+  size_t off = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    size_t l = std::strlen(store.data() + off);
+    out[(size_t)i] = std::string_view(store.data() + off, l);
+    off += l + 1;
+  }
+}
+
+unsigned host_threads(size_t work) {
+  unsigned nt = std::max(1u, std::thread::hardware_concurrency());
+  cpu_set_t cs;
+  if (sched_getaffinity(0, sizeof(cs), &cs) == 0) nt = std::max(1, CPU_COUNT(&cs));
+  if (const char* s = getenv("PQW_THREADS")) nt = std::max(1, atoi(s));
+  return (unsigned)std::max<size_t>(1, std::min<size_t>(nt, work));
+}
+
+template <class F>
+void parallel_for(size_t n, F&& f) {
+  const unsigned nt = host_threads(n);
+  std::atomic<size_t> next{0};
+  auto work = [&](unsigned tid) {
+    for (;;) {
+      const size_t i = next.fetch_add(1);
+      if (i >= n) return;
+      f(i, tid);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < nt; ++t) pool.emplace_back(work, t);
+  work(0);
+  for (auto& t : pool) t.join();
+}
+
+// Open-addressing name -> index table (built once, then read from many threads).
+struct NameTable {
+  std::vector<uint64_t> hash;
+  std::vector<int32_t> slot;  // -1 empty
+  const std::vector<std::string_view>* names = nullptr;
+  uint64_t mask = 0;
+
+  static uint64_t h(std::string_view s) {
+    uint64_t x = 0xCBF29CE484222325ull;
+    size_t i = 0;
+    for (; i + 8 <= s.size(); i += 8) {
+      uint64_t w;
+      std::memcpy(&w, s.data() + i, 8);
+      x = (x ^ w) * 0x100000001B3ull;
+      x ^= x >> 29;
+    }
+    for (; i < s.size(); ++i) x = (x ^ (unsigned char)s[i]) * 0x100000001B3ull;
+    return mix64(x ^ s.size());
+  }
+  // returns false on a duplicate name
+  bool build(const std::vector<std::string_view>& ns) {
+    names = &ns;
+    size_t cap = 16;
+    while (cap < ns.size() * 2) cap <<= 1;
+    mask = cap - 1;
+    hash.assign(cap, 0);
+    slot.assign(cap, -1);
+    std::vector<uint64_t> hs(ns.size());
+    parallel_for((ns.size() + 65535) / 65536, [&](size_t c, unsigned) {
+      for (size_t i = c * 65536; i < std::min(ns.size(), (c + 1) * 65536); ++i) hs[i] = h(ns[i]);
+    });
+    bool unique = true;
+    for (size_t i = 0; i < ns.size(); ++i) {
+      uint64_t k = hs[i] & mask;
+      for (;; k = (k + 1) & mask) {
+        if (slot[k] < 0) {
+          slot[k] = (int32_t)i;
+          hash[k] = hs[i];
+          break;
+        }
+        if (hash[k] == hs[i] && ns[slot[k]] == ns[i]) {
+          unique = false;
+          break;
+        }
+      }
+    }
+    return unique;
+  }
+  int32_t find(std::string_view s) const {
+    const uint64_t hv = h(s);
+    for (uint64_t k = hv & mask;; k = (k + 1) & mask) {
+      if (slot[k] < 0) return -1;
+      if (hash[k] == hv && (*names)[slot[k]] == s) return slot[k];
+    }
+  }
+};
+
+struct GraphData {
+  std::string tstore, nstore, istore, ostore, gstore;
+  std::vector<std::string_view> tname, nid;
+  std::vector<int64_t> dim_off, dims;
+  std::vector<uint8_t> tflags;
+  std::vector<int32_t> kind;
+  std::vector<int64_t> in_off, out_off, attr_off;
+  std::vector<int32_t> ins, outs;  // tensor indices, -1 unresolved
+  std::vector<int64_t> attrs;
+  std::vector<int32_t> device;
+  std::vector<int64_t> seq;
+  std::vector<uint8_t> is_input;
+  std::vector<int32_t> producer;   // tensor -> node, -1 none
+  NameTable index;
+  bool resolved = true;            // every node input/output names a tensor
+  bool unique_producers = true;
+  std::string problem;
+
+  size_t nt() const { return tname.size(); }
+  size_t nn() const { return kind.size(); }
+  std::vector<int64_t> shape_vec(int32_t t) const {
+    return std::vector<int64_t>(dims.begin() + dim_off[t], dims.begin() + dim_off[t + 1]);
+  }
+  int32_t find(std::string_view s) const { return index.find(s); }
+  // topological key (graph.py:136 rank: device or -1, seq, id)
+  bool before(int32_t a, int32_t b) const {
+    if (device[a] != device[b]) return device[a] < device[b];
+    if (seq[a] != seq[b]) return seq[a] < seq[b];
+    return nid[a] < nid[b];
+  }
+
+  void resolve(const char* names, int64_t n, std::string& store, std::vector<int32_t>& out) {
+    std::vector<std::string_view> tmp;
+    split_names(names, n, store, tmp);
+    out.resize(tmp.size());
+    std::atomic<bool> all{true};
+    parallel_for((tmp.size() + 65535) / 65536, [&](size_t c, unsigned) {
+      for (size_t i = c * 65536; i < std::min(tmp.size(), (c + 1) * 65536); ++i) {
+        out[i] = find(tmp[i]);
+        if (out[i] < 0) all = false;
+      }
+    });
+    if (!all) resolved = false;
+  }
+
+  void load(const pqw_graph_desc& d) {
+    split_names(d.tensor_names, d.n_tensors, tstore, tname);
+    if (!index.build(tname)) {
+      resolved = false;
+      problem = "duplicate tensor id";
+    }
+    dim_off.assign((size_t)d.n_tensors + 1, 0);
+    for (int64_t i = 0; i < d.n_tensors; ++i) dim_off[i + 1] = dim_off[i] + d.tensor_ndim[i];
+    dims.assign(d.tensor_dims, d.tensor_dims + dim_off.back());
+    tflags.assign(d.tensor_flags, d.tensor_flags + d.n_tensors);
+    const size_t n = (size_t)d.n_nodes;
+    split_names(d.node_ids, d.n_nodes, nstore, nid);
+    kind.assign(d.node_kind, d.node_kind + n);
+    device.assign(d.node_device, d.node_device + n);
+    seq.assign(d.node_seq, d.node_seq + n);
+    in_off.assign(n + 1, 0);
+    out_off.assign(n + 1, 0);
+    attr_off.assign(n + 1, 0);
+    for (size_t i = 0; i < n; ++i) {
+      in_off[i + 1] = in_off[i] + d.node_nin[i];
+      out_off[i + 1] = out_off[i] + d.node_nout[i];
+      attr_off[i + 1] = attr_off[i] + d.node_nattr[i];
+    }
+    attrs.assign(d.node_attrs, d.node_attrs + attr_off[n]);
+    resolve(d.node_inputs, in_off[n], istore, ins);
+    resolve(d.node_outputs, out_off[n], ostore, outs);
+    {
+      std::vector<int32_t> gin;
+      std::string gs;
+      const bool keep = resolved;
+      resolve(d.input_names, d.n_inputs, gs, gin);
+      resolved = keep;  // graph.inputs may name anything (it is only a set of ids)
+      is_input.assign(nt(), 0);
+      for (int32_t t : gin)
+        if (t >= 0) is_input[t] = 1;
+    }
+    producer.assign(nt(), -1);
+    for (size_t v = 0; v < n; ++v)
+      for (int64_t j = out_off[v]; j < out_off[v + 1]; ++j) {
+        int32_t t = outs[j];
+        if (t < 0) continue;
+        if (producer[t] >= 0) unique_producers = false;
+        producer[t] = (int32_t)v;
+      }
+    // node ids must be unique for the (device, seq, id) order to be total
+    NameTable ids;
+    if (!ids.build(nid)) {
+      resolved = false;
+      problem = "duplicate node id";
+    }
+  }
+};
+
+struct Entry {
+  int32_t logical = -1;  // logical tensor
+  uint8_t mode = 0;
+  std::vector<int32_t> shards;                      // parallel tensors
+  std::vector<std::vector<std::pair<int64_t, int64_t>>> ranges;
+};
+
+struct StageRec {
+  int32_t target = -1;   // logical tensor
+  int32_t entry = -1;
+  std::vector<int32_t> lnodes, pnodes;  // topo order
+  std::vector<int32_t> l_inputs, p_inputs;  // sorted by name
+};
+
+// Per-thread scratch: generation-stamped marks over tensors and nodes.
+struct Marks {
+  std::vector<uint32_t> stamp;
+  uint32_t gen = 0;
+  void reset(size_t n) {
+    if (stamp.size() != n) {
+      stamp.assign(n, 0);
+      gen = 0;
+    }
+    if (++gen == 0) {
+      std::fill(stamp.begin(), stamp.end(), 0);
+      gen = 1;
+    }
+  }
+  bool test(size_t i) const { return stamp[i] == gen; }
+  bool set(size_t i) {  // true if newly set
+    if (stamp[i] == gen) return false;
+    stamp[i] = gen;
+    return true;
+  }
+};
+
+}  // namespace
+}  // namespace pqw
+
+struct pqw_plan {
+  pqw::GraphData L, P;
+  std::vector<pqw::Entry> entries;
+  std::vector<int32_t> entry_of_logical;  // logical tensor -> entry, -1
+  std::vector<int64_t> consts;             // triples
+  bool lineage_ok = true;
+  bool validated = false;
+  bool built = false;
+  std::vector<int32_t> order;              // entry_order (entry indices)
+  std::vector<int32_t> owner;              // parallel tensor -> earliest claiming entry
+  std::vector<pqw::StageRec> stages;
+  std::vector<int32_t> uncovered[2];
+};
+
+namespace pqw {
+namespace {
+
+// ---- validate_concrete -------------------------------------------------------
+
+using Shape = std::vector<int64_t>;
+
+int64_t volume(const Shape& s) {
+  int64_t v = 1;
+  for (auto d : s) v *= d;
+  return v;
+}
+
+struct ShapeFail {};
+
+void want(bool c) {
+  if (!c) throw ShapeFail{};
+}
+
+// einsum spec (code points) -> subscripts, rhs; as opshape.einsum_parse
+void einsum_split(const int64_t* a, int64_t n, size_t n_in, std::vector<std::vector<int64_t>>& subs,
+                  std::vector<int64_t>& rhs) {
+  std::vector<int64_t> sp;
+  for (int64_t i = 0; i < n; ++i)
+    if (a[i] != ' ') sp.push_back(a[i]);
+  int arrows = 0;
+  size_t at = 0;
+  for (size_t i = 0; i + 1 < sp.size(); ++i)
+    if (sp[i] == '-' && sp[i + 1] == '>') {
+      arrows++;
+      at = i;
+    }
+  if (arrows != 1) throw PlanError("einsum spec");
+  subs.assign(1, {});
+  for (size_t i = 0; i < at; ++i) {
+    if (sp[i] == ',') subs.emplace_back();
+    else subs.back().push_back(sp[i]);
+  }
+  rhs.assign(sp.begin() + at + 2, sp.end());
+  if (subs.size() != n_in) throw ShapeFail{};
+}
+
+std::vector<Shape> infer(int k, const int64_t* a, int64_t na, const std::vector<Shape>& ins) {
+  auto at = [&](int64_t i) -> int64_t {
+    if (i >= na) throw PlanError("attribute words");
+    return a[i];
+  };
+  if (k < PQW_T_ADD || k > PQW_T_ALL_TO_ALL) throw PlanError("unknown operator");
+  if (is_elementwise2(k)) {
+    want(ins.size() == 2);
+    want(ins[1] == ins[0]);
+    return {ins[0]};
+  }
+  if (is_unary(k)) {
+    want(ins.size() == 1);
+    if (k == PQW_T_POW) want(at(0) >= 1);
+    return {ins[0]};
+  }
+  switch (k) {
+    case PQW_T_SOFTMAX: {
+      want(ins.size() == 1);
+      const int64_t ax = at(0);
+      want(ax == -1 || ax == (int64_t)ins[0].size() - 1);
+      want(!ins[0].empty() && ins[0].back() >= 2);
+      return {ins[0]};
+    }
+    case PQW_T_CREATE_MASK: {
+      want(ins.empty());
+      const int64_t s = at(0);
+      want(s >= 2);
+      return {Shape{s, s}};
+    }
+    case PQW_T_APPLY_MASK: {
+      want(ins.size() == 2);
+      const Shape &x = ins[0], &m = ins[1];
+      want(m.size() == 2 && m[0] == m[1]);
+      want(x.size() >= 2 && x[x.size() - 2] == m[0] && x[x.size() - 1] == m[1]);
+      return {x};
+    }
+    case PQW_T_VIEW: {
+      want(ins.size() == 1);
+      Shape t(a + 1, a + 1 + at(0));
+      want(volume(ins[0]) == volume(t));
+      return {t};
+    }
+    case PQW_T_TRANSPOSE: {
+      want(ins.size() == 1);
+      Shape perm(a, a + na), sorted = perm;
+      std::sort(sorted.begin(), sorted.end());
+      want(sorted.size() == ins[0].size());
+      for (size_t i = 0; i < sorted.size(); ++i) want(sorted[i] == (int64_t)i);
+      Shape out;
+      for (auto p : perm) out.push_back(ins[0][p]);
+      return {out};
+    }
+    case PQW_T_EXPAND: {
+      if (ins.empty()) throw PlanError("expand without input");
+      Shape t(a + 1, a + 1 + at(0));
+      const Shape& s = ins[0];
+      want(t.size() == s.size());
+      for (size_t i = 0; i < s.size(); ++i) want(s[i] == t[i] || s[i] == 1);
+      return {t};
+    }
+    case PQW_T_SUM:
+    case PQW_T_MEAN: {
+      want(ins.size() == 1);
+      const int64_t r = (int64_t)ins[0].size();
+      const bool keep = at(0) != 0;
+      std::vector<char> red((size_t)r, 0);
+      if (at(1) == 0) {
+        std::fill(red.begin(), red.end(), 1);
+      } else {
+        if (r == 0) throw PlanError("reduce of rank 0");
+        for (int64_t i = 0; i < at(2); ++i) red[(size_t)pymod(at(3 + i), r)] = 1;
+      }
+      Shape out;
+      for (int64_t ax = 0; ax < r; ++ax) {
+        if (red[ax]) {
+          if (keep) out.push_back(1);
+        } else {
+          out.push_back(ins[0][ax]);
+        }
+      }
+      if (out.empty()) out.push_back(1);
+      return {out};
+    }
+    case PQW_T_MATMUL: {
+      want(ins.size() == 2);
+      const Shape &x = ins[0], &y = ins[1];
+      want(x.size() >= 2 && y.size() >= 2);
+      want(y.size() == x.size() || y.size() == 2);
+      if (y.size() == x.size())
+        want(std::equal(x.begin(), x.end() - 2, y.begin()));
+      want(x[x.size() - 1] == y[y.size() - 2]);
+      Shape out(x.begin(), x.end() - 1);
+      out.push_back(y.back());
+      return {out};
+    }
+    case PQW_T_EINSUM: {
+      std::vector<std::vector<int64_t>> subs;
+      std::vector<int64_t> rhs;
+      einsum_split(a + 1, at(0), ins.size(), subs, rhs);
+      std::vector<std::pair<int64_t, int64_t>> extent;  // (char, extent) in first-seen order
+      auto find = [&](int64_t ch) -> int64_t* {
+        for (auto& e : extent)
+          if (e.first == ch) return &e.second;
+        return nullptr;
+      };
+      for (size_t i = 0; i < subs.size(); ++i) {
+        want(subs[i].size() == ins[i].size());
+        for (size_t j = 0; j < subs[i].size(); ++j) {
+          int64_t* e = find(subs[i][j]);
+          if (e) want(*e == ins[i][j]);
+          else extent.push_back({subs[i][j], ins[i][j]});
+        }
+      }
+      int64_t vol = 1;
+      bool any = false;
+      for (auto& e : extent)
+        if (std::find(rhs.begin(), rhs.end(), e.first) == rhs.end()) {
+          any = true;
+          vol *= e.second;
+        }
+      if (any) want(vol >= 2);
+      Shape out;
+      for (auto ch : rhs) {
+        int64_t* e = find(ch);
+        if (!e) throw PlanError("einsum output index not in inputs");
+        out.push_back(*e);
+      }
+      return {out};
+    }
+    case PQW_T_FULL: {
+      want(ins.empty());
+      return {Shape(a + 2, a + 2 + at(1))};
+    }
+    case PQW_T_CHUNK: {
+      if (ins.empty()) throw PlanError("chunk without input");
+      const int64_t r = (int64_t)ins[0].size();
+      int64_t ax = at(0);
+      if (ax < -r || ax >= r) throw PlanError("chunk axis");
+      ax = pymod(ax, r);
+      const int64_t parts = at(1), idx = at(2), d = ins[0][ax];
+      want(parts >= 1 && idx >= 0 && idx < parts);
+      want(d % parts == 0);
+      Shape out = ins[0];
+      out[ax] = d / parts;
+      return {out};
+    }
+    case PQW_T_EMBEDDING: {
+      want(ins.size() == 2);
+      want(ins[0].size() == 2);
+      want(ins[0][0] >= volume(ins[1]));
+      Shape out = ins[1];
+      out.push_back(ins[0][1]);
+      return {out};
+    }
+    case PQW_T_EMBEDDING_GRAD: {
+      if (ins.size() != 2) throw PlanError("embedding_grad arity");
+      const Shape &g = ins[0], &ids = ins[1];
+      want(!g.empty() && g.size() - 1 == ids.size() && std::equal(ids.begin(), ids.end(), g.begin()));
+      const int64_t v = at(0);
+      want(v >= volume(ids));
+      return {Shape{v, g.back()}};
+    }
+    case PQW_T_GNORM_SQ:
+      want(!ins.empty());
+      return {Shape{1}};
+    default:
+      break;
+  }
+  // communication: group of n, n inputs, n outputs
+  const int64_t n = at(0);
+  want((int64_t)ins.size() == n);
+  if (n == 0) throw PlanError("empty group");
+  const int64_t r = (int64_t)ins[0].size();
+  auto axis = [&](int64_t ax) {
+    if (ax < -r || ax >= r) throw PlanError("axis out of range");
+    return pymod(ax, r);
+  };
+  if (k == PQW_T_ALL_REDUCE) {
+    for (auto& s : ins) want(s == ins[0]);
+    return std::vector<Shape>((size_t)n, ins[0]);
+  }
+  if (k == PQW_T_ALL_GATHER) {
+    // opshape.py compares s[:ax] + s[ax+1:] with Python slicing on the raw
+    // axis (a negative axis -1 keeps the whole shape in the second slice)
+    const int64_t ax = at(1);
+    auto clamp = [](int64_t i, int64_t len) {
+      if (i < 0) i += len;
+      return std::min(std::max<int64_t>(i, 0), len);
+    };
+    auto off_axis = [&](const Shape& s) {
+      const int64_t len = (int64_t)s.size();
+      Shape o(s.begin(), s.begin() + clamp(ax, len));
+      o.insert(o.end(), s.begin() + clamp(ax + 1, len), s.end());
+      return o;
+    };
+    Shape base = ins[0];
+    const Shape want_off = off_axis(base);
+    int64_t total = 0;
+    for (auto& s : ins) {
+      want(off_axis(s) == want_off);
+      const int64_t len = (int64_t)s.size();
+      if (ax < -len || ax >= len) throw PlanError("axis out of range");
+      total += s[(size_t)pymod(ax, len)];
+    }
+    base[(size_t)axis(ax)] = total;
+    return std::vector<Shape>((size_t)n, base);
+  }
+  if (k == PQW_T_REDUCE_SCATTER) {
+    const int64_t ax = axis(at(1));
+    for (auto& s : ins) want(s == ins[0]);
+    want(ins[0][ax] % n == 0);
+    Shape out = ins[0];
+    out[ax] /= n;
+    return std::vector<Shape>((size_t)n, out);
+  }
+  const int64_t sa = axis(at(1)), ca = axis(at(2));
+  for (auto& s : ins) want(s == ins[0]);
+  want(ins[0][sa] % n == 0);
+  Shape out = ins[0];
+  out[sa] /= n;
+  out[ca] *= n;
+  return std::vector<Shape>((size_t)n, out);
+}
+
+// Python negative-index semantics are applied by the packer only where the
+// reference normalises (softmax axis is compared raw); nothing else to do.
+
+bool validate_graph(const GraphData& g, std::string& why) {
+  if (!g.resolved) {
+    why = g.problem.empty() ? "unresolved tensor name" : g.problem;
+    return false;
+  }
+  // dangling inputs (graph.py topo_sort) and cycles
+  const size_t n = g.nn();
+  std::vector<int32_t> indeg(n, 0);
+  std::vector<std::vector<int32_t>> succ(n);
+  for (size_t v = 0; v < n; ++v)
+    for (int64_t j = g.in_off[v]; j < g.in_off[v + 1]; ++j) {
+      const int32_t t = g.ins[j];
+      if (g.is_input[t]) continue;
+      const int32_t src = g.producer[t];
+      if (src < 0) {
+        why = "dangling tensor";
+        return false;
+      }
+      indeg[v]++;
+      succ[src].push_back((int32_t)v);
+    }
+  {
+    std::vector<int32_t> q;
+    for (size_t v = 0; v < n; ++v)
+      if (!indeg[v]) q.push_back((int32_t)v);
+    size_t seen = 0;
+    while (!q.empty()) {
+      int32_t v = q.back();
+      q.pop_back();
+      seen++;
+      for (int32_t s : succ[v])
+        if (--indeg[s] == 0) q.push_back(s);
+    }
+    if (seen != n) {
+      why = "cycle";
+      return false;
+    }
+  }
+  std::atomic<bool> ok{true};
+  std::mutex mu;
+  const size_t chunk = 4096;
+  parallel_for((n + chunk - 1) / chunk, [&](size_t c, unsigned) {
+    std::vector<Shape> ins;
+    for (size_t v = c * chunk; v < std::min(n, (c + 1) * chunk) && ok.load(std::memory_order_relaxed); ++v) {
+      const int k = g.kind[v];
+      ins.clear();
+      for (int64_t j = g.in_off[v]; j < g.in_off[v + 1]; ++j) ins.push_back(g.shape_vec(g.ins[j]));
+      bool good = true;
+      try {
+        auto got = infer(k, g.attrs.data() + g.attr_off[v], g.attr_off[v + 1] - g.attr_off[v], ins);
+        // zip(outputs, got): only the common prefix is compared (opshape.py)
+        const int64_t no = g.out_off[v + 1] - g.out_off[v];
+        for (int64_t j = 0; j < no && (size_t)j < got.size(); ++j)
+          if (g.shape_vec(g.outs[g.out_off[v] + j]) != got[(size_t)j]) good = false;
+      } catch (...) {
+        good = false;
+      }
+      if (!good) {
+        ok = false;
+        std::lock_guard<std::mutex> l(mu);
+        why = std::string("node ") + std::string(g.nid[v]);
+      }
+    }
+  });
+  return ok.load();
+}
+
+// ---- stage construction -------------------------------------------------------
+
+// Deterministic Kahn order of `nodes` (graph.py topo_sort with the (device,
+// seq, id) tie-break); `picked` marks exactly `nodes`. Throws PlanError on a
+// dangling input or a cycle.
+std::vector<int32_t> topo_order(const GraphData& g, const std::vector<int32_t>& nodes,
+                                const Marks& picked) {
+  std::unordered_map<int32_t, int32_t> local;  // node -> position in `nodes`
+  local.reserve(nodes.size() * 2);
+  for (size_t i = 0; i < nodes.size(); ++i) local.emplace(nodes[i], (int32_t)i);
+  std::vector<int32_t> indeg(nodes.size(), 0);
+  std::vector<std::vector<int32_t>> succ(nodes.size());
+  for (size_t i = 0; i < nodes.size(); ++i) {
+    const int32_t v = nodes[i];
+    for (int64_t j = g.in_off[v]; j < g.in_off[v + 1]; ++j) {
+      const int32_t t = g.ins[j];
+      if (g.is_input[t]) continue;
+      const int32_t src = g.producer[t];
+      if (src >= 0 && picked.test((size_t)src)) {
+        indeg[i]++;
+        succ[(size_t)local[src]].push_back((int32_t)i);
+      } else if (src < 0) {
+        throw PlanError("dangling tensor");
+      }
+    }
+  }
+  auto cmp = [&](int32_t a, int32_t b) { return g.before(nodes[b], nodes[a]); };  // min-heap
+  std::priority_queue<int32_t, std::vector<int32_t>, decltype(cmp)> ready(cmp);
+  for (size_t i = 0; i < nodes.size(); ++i)
+    if (!indeg[i]) ready.push((int32_t)i);
+  std::vector<int32_t> out;
+  out.reserve(nodes.size());
+  while (!ready.empty()) {
+    const int32_t i = ready.top();
+    ready.pop();
+    out.push_back(nodes[i]);
+    for (int32_t s : succ[i])
+      if (--indeg[s] == 0) ready.push(s);
+  }
+  if (out.size() != nodes.size()) throw PlanError("cycle");
+  return out;
+}
+
+// graph.py backward_slice: nodes reached from roots without passing stop
+// tensors; returns picked nodes (marked in `picked`) and the boundary.
+void backward_slice(const GraphData& g, const std::vector<int32_t>& roots,
+                    const std::function<bool(int32_t)>& stop, Marks& seen, Marks& picked,
+                    std::vector<int32_t>& nodes, std::vector<int32_t>& boundary) {
+  seen.reset(g.nt());
+  picked.reset(g.nn());
+  nodes.clear();
+  boundary.clear();
+  std::vector<int32_t> stack(roots.rbegin(), roots.rend());
+  // (the reference pops from the end; order does not change the result sets)
+  while (!stack.empty()) {
+    const int32_t t = stack.back();
+    stack.pop_back();
+    if (!seen.set((size_t)t)) continue;
+    const int32_t v = g.producer[t];
+    const bool st = stop(t);
+    if (st || v < 0) {
+      if (st || g.is_input[t]) boundary.push_back(t);
+      continue;
+    }
+    if (picked.set((size_t)v)) {
+      nodes.push_back(v);
+      for (int64_t j = g.in_off[v]; j < g.in_off[v + 1]; ++j) stack.push_back(g.ins[j]);
+    }
+  }
+}
+
+void sort_by_name(const GraphData& g, std::vector<int32_t>& ts) {
+  std::sort(ts.begin(), ts.end(), [&](int32_t a, int32_t b) { return g.tname[a] < g.tname[b]; });
+}
+
+void build(pqw_plan* p) {
+  const GraphData &L = p->L, &P = p->P;
+  // entry_order: logical topological position of the producer, inputs first
+  std::vector<int32_t> all(L.nn());
+  for (size_t i = 0; i < all.size(); ++i) all[i] = (int32_t)i;
+  Marks everything;
+  everything.reset(L.nn());
+  for (size_t i = 0; i < all.size(); ++i) everything.set(i);
+  const auto lorder = topo_order(L, all, everything);
+  std::vector<int64_t> pos(L.nn(), -1);
+  for (size_t i = 0; i < lorder.size(); ++i) pos[lorder[i]] = (int64_t)i;
+  const size_t ne = p->entries.size();
+  p->order.resize(ne);
+  for (size_t i = 0; i < ne; ++i) p->order[i] = (int32_t)i;
+  auto epos = [&](int32_t e) {
+    const int32_t v = L.producer[p->entries[e].logical];
+    return v < 0 ? (int64_t)-1 : pos[v];
+  };
+  std::sort(p->order.begin(), p->order.end(), [&](int32_t a, int32_t b) {
+    const int64_t pa = epos(a), pb = epos(b);
+    if (pa != pb) return pa < pb;
+    return L.tname[p->entries[a].logical] < L.tname[p->entries[b].logical];
+  });
+  std::vector<int32_t> rank(ne);
+  for (size_t r = 0; r < ne; ++r) rank[p->order[r]] = (int32_t)r;
+  // earliest checkpoint claiming each shard tensor
+  p->owner.assign(P.nt(), -1);
+  for (size_t r = ne; r-- > 0;)
+    for (int32_t s : p->entries[p->order[r]].shards) p->owner[s] = p->order[r];
+  // a shard is an "earlier shard" of stage r iff some entry of rank < r lists it:
+  // first_rank[s] = smallest rank of an entry listing s
+  std::vector<int32_t> first_rank(P.nt(), INT32_MAX);
+  for (size_t r = 0; r < ne; ++r)
+    for (int32_t s : p->entries[p->order[r]].shards)
+      first_rank[s] = std::min(first_rank[s], (int32_t)r);
+  std::vector<int32_t> produced;  // ranks of produced checkpoints
+  for (size_t r = 0; r < ne; ++r)
+    if (L.producer[p->entries[p->order[r]].logical] >= 0) produced.push_back((int32_t)r);
+  p->stages.assign(produced.size(), StageRec{});
+  std::mutex err_mu;
+  std::string err;
+  const unsigned nt = host_threads(produced.size());
+  std::vector<Marks> seen_l(nt), picked_l(nt), seen_p(nt), picked_p(nt);
+  parallel_for(produced.size(), [&](size_t si, unsigned tid) {
+    try {
+      const int32_t r = produced[si];
+      const Entry& e = p->entries[p->order[r]];
+      StageRec& st = p->stages[si];
+      st.target = e.logical;
+      st.entry = p->order[r];
+      std::vector<int32_t> nodes, bound;
+      backward_slice(L, {e.logical},
+                     [&](int32_t t) { return t != e.logical && p->entry_of_logical[t] >= 0; },
+                     seen_l[tid], picked_l[tid], nodes, bound);
+      std::sort(nodes.begin(), nodes.end());
+      st.lnodes = topo_order(L, nodes, picked_l[tid]);
+      for (int32_t b : bound)
+        if (p->entry_of_logical[b] < 0) throw PlanError("logical input has no checkpoint entry");
+      sort_by_name(L, bound);
+      st.l_inputs = bound;
+      backward_slice(P, e.shards, [&](int32_t t) { return first_rank[t] < r; }, seen_p[tid],
+                     picked_p[tid], nodes, bound);
+      std::sort(nodes.begin(), nodes.end());
+      st.pnodes = topo_order(P, nodes, picked_p[tid]);
+      for (int32_t b : bound)
+        if (!(first_rank[b] < r)) throw PlanError("parallel input is not a checkpoint shard");
+      sort_by_name(P, bound);
+      st.p_inputs = bound;
+    } catch (const std::exception& ex) {
+      std::lock_guard<std::mutex> l(err_mu);
+      if (err.empty()) err = ex.what();
+    }
+  });
+  if (!err.empty()) throw PlanError(err);
+  // ownership in stage order: a node belongs to the first stage whose slice has it
+  for (int side = 0; side < 2; ++side) {
+    const GraphData& g = side ? P : L;
+    std::vector<char> claimed(g.nn(), 0);
+    for (auto& st : p->stages)
+      for (int32_t v : side ? st.pnodes : st.lnodes) claimed[v] = 1;
+    auto& u = p->uncovered[side];
+    u.clear();
+    for (size_t v = 0; v < g.nn(); ++v)
+      if (!claimed[v]) u.push_back((int32_t)v);
+    std::sort(u.begin(), u.end(), [&](int32_t a, int32_t b) { return g.nid[a] < g.nid[b]; });
+  }
+}
+
+// ---- lowering ---------------------------------------------------------------------
+
+uint64_t fnv1a64(std::string_view a, std::string_view b) {
+  uint64_t h = 0xCBF29CE484222325ull;
+  for (unsigned char c : a) h = (h ^ c) * 0x100000001B3ull;
+  for (unsigned char c : b) h = (h ^ c) * 0x100000001B3ull;
+  return h;
+}
+
+struct Program {
+  std::vector<int32_t> ir;
+  std::vector<int64_t> consts;
+  std::vector<uint64_t> var_keys;
+};
+
+struct Lowerer {
+  const pqw_plan* p = nullptr;
+  uint64_t seed = 0;
+  std::vector<Shape> shapes;
+  std::vector<int32_t> ops;
+  int32_t n_ops = 0;
+  std::vector<int64_t> consts;
+  std::unordered_map<int64_t, int32_t> const_idx;  // plan const id -> stage const index
+  std::vector<uint64_t> var_keys;
+  int64_t n_vars = 0;
+  std::unordered_map<int32_t, int32_t> lt, pt;      // "L:"/"P:" keys -> local tensor
+  std::unordered_map<int32_t, int32_t> boxes;       // logical tensor -> local tensor
+
+  int32_t temp(const Shape& s) {
+    shapes.push_back(s);
+    return (int32_t)shapes.size() - 1;
+  }
+  int32_t tensor(std::unordered_map<int32_t, int32_t>& m, int32_t key, const Shape& s) {
+    auto it = m.find(key);
+    if (it != m.end()) return it->second;
+    const int32_t idx = temp(s);
+    m.emplace(key, idx);
+    return idx;
+  }
+  int32_t cst(int64_t cid) {
+    auto it = const_idx.find(cid);
+    if (it != const_idx.end()) return it->second;
+    if (cid < 0 || (size_t)(3 * cid + 2) >= p->consts.size()) throw PlanError("const id");
+    const int32_t idx = (int32_t)(consts.size() / 3);
+    consts.insert(consts.end(), p->consts.begin() + 3 * cid, p->consts.begin() + 3 * cid + 3);
+    const_idx.emplace(cid, idx);
+    return idx;
+  }
+  void emit(int32_t op, const std::vector<int32_t>& ins, const std::vector<int32_t>& outs,
+            const std::vector<int32_t>& attrs) {
+    ops.push_back(op);
+    ops.push_back((int32_t)ins.size());
+    ops.push_back((int32_t)outs.size());
+    ops.push_back((int32_t)attrs.size());
+    ops.insert(ops.end(), ins.begin(), ins.end());
+    ops.insert(ops.end(), outs.begin(), outs.end());
+    ops.insert(ops.end(), attrs.begin(), attrs.end());
+    n_ops++;
+  }
+  int32_t vars_for(std::string_view pre, std::string_view name, const Shape& s) {
+    const int64_t n = volume(s);
+    const int32_t out = temp(s);
+    emit(PQW_T_VARS, {}, {out}, {(int32_t)n_vars});
+    // stages.py tensor_var_keys: mix64(base + (i+1) * VAR_STEP)
+    const uint64_t base = seed ^ fnv1a64(std::string("var:") + std::string(pre), name);
+    for (int64_t i = 0; i < n; ++i)
+      var_keys.push_back(mix64(base + (uint64_t)(i + 1) * 0xD1B54A32D192ED03ull));
+    n_vars += n;
+    return out;
+  }
+  int32_t box_of(int32_t tid) {
+    auto it = boxes.find(tid);
+    if (it != boxes.end()) return it->second;
+    const GraphData& L = p->L;
+    const Shape s = L.shape_vec(tid);
+    int32_t idx;
+    if (L.tflags[tid] & 1) {
+      if (!(L.tflags[tid] & 2)) throw PlanError("integer checkpoint has no enumerated values");
+      idx = temp(s);
+      const int32_t base = (int32_t)(consts.size() / 3);
+      const int64_t n = volume(s);
+      for (int64_t v = 0; v < n; ++v) {
+        consts.push_back(v % (int64_t)PQW_PRIME);
+        consts.push_back(v);
+        consts.push_back(1);
+      }
+      emit(PQW_T_INTS, {}, {idx}, {base});
+    } else {
+      idx = vars_for("v.", L.tname[tid], s);
+    }
+    boxes.emplace(tid, idx);
+    return idx;
+  }
+
+  std::vector<int32_t> node_attrs(const GraphData& g, int32_t v, const std::vector<int32_t>& in) {
+    const int k = g.kind[v];
+    const int64_t* a = g.attrs.data() + g.attr_off[v];
+    const int64_t na = g.attr_off[v + 1] - g.attr_off[v];
+    auto at = [&](int64_t i) -> int64_t {
+      if (i >= na) throw PlanError("attribute words");
+      return a[i];
+    };
+    auto rank0 = [&]() -> int64_t {
+      if (in.empty()) throw PlanError("no input");
+      return (int64_t)shapes[in[0]].size();
+    };
+    switch (k) {
+      case PQW_T_SCALE:
+      case PQW_T_SHIFT:
+      case PQW_T_FULL:
+        return {cst(at(0))};
+      case PQW_T_POW:
+        return {(int32_t)at(0)};
+      case PQW_T_DIV:
+        return {(int32_t)(at(0) != 0)};
+      case PQW_T_TRANSPOSE: {
+        std::vector<int32_t> out;
+        for (int64_t i = 0; i < na; ++i) out.push_back((int32_t)a[i]);
+        return out;
+      }
+      case PQW_T_SUM:
+      case PQW_T_MEAN: {
+        const int64_t r = rank0();
+        std::vector<int32_t> out{(int32_t)(at(0) != 0)};
+        std::vector<int64_t> axes;
+        if (at(1) == 0) {
+          for (int64_t i = 0; i < r; ++i) axes.push_back(i);
+        } else {
+          if (r == 0) throw PlanError("reduce of rank 0");
+          for (int64_t i = 0; i < at(2); ++i) axes.push_back(pymod(at(3 + i), r));
+          std::sort(axes.begin(), axes.end());
+        }
+        for (auto x : axes) out.push_back((int32_t)x);
+        return out;
+      }
+      case PQW_T_EINSUM: {
+        std::vector<std::vector<int64_t>> subs;
+        std::vector<int64_t> rhs;
+        try {
+          einsum_split(a + 1, at(0), in.size(), subs, rhs);
+        } catch (const ShapeFail&) {
+          throw PlanError("einsum arity");
+        }
+        std::vector<int32_t> out{(int32_t)subs.size()};
+        for (auto& s : subs) {
+          out.push_back((int32_t)s.size());
+          for (auto c : s) out.push_back((int32_t)c);
+        }
+        out.push_back((int32_t)rhs.size());
+        for (auto c : rhs) out.push_back((int32_t)c);
+        return out;
+      }
+      case PQW_T_CHUNK: {
+        const int64_t r = rank0();
+        if (r == 0) throw PlanError("chunk of rank 0");
+        return {(int32_t)pymod(at(0), r), (int32_t)at(1), (int32_t)at(2)};
+      }
+      case PQW_T_ALL_GATHER:
+      case PQW_T_REDUCE_SCATTER: {
+        const int64_t r = rank0();
+        if (r == 0) throw PlanError("rank 0");
+        return {(int32_t)pymod(at(1), r)};
+      }
+      case PQW_T_ALL_TO_ALL: {
+        const int64_t r = rank0();
+        if (r == 0) throw PlanError("rank 0");
+        return {(int32_t)pymod(at(1), r), (int32_t)pymod(at(2), r)};
+      }
+      default:
+        return {};
+    }
+  }
+
+  void run_nodes(const GraphData& g, const std::vector<int32_t>& nodes,
+                 std::unordered_map<int32_t, int32_t>& m, int side) {
+    emit(PQW_T_SIDE, {}, {}, {side});
+    std::vector<int32_t> in, out;
+    for (int32_t v : nodes) {
+      if (g.kind[v] < PQW_T_ADD || g.kind[v] > PQW_T_ALL_TO_ALL) throw PlanError("unknown operator");
+      in.clear();
+      out.clear();
+      for (int64_t j = g.in_off[v]; j < g.in_off[v + 1]; ++j) {
+        auto it = m.find(g.ins[j]);
+        if (it == m.end()) throw PlanError("unbound input");
+        in.push_back(it->second);
+      }
+      for (int64_t j = g.out_off[v]; j < g.out_off[v + 1]; ++j)
+        out.push_back(tensor(m, g.outs[j], g.shape_vec(g.outs[j])));
+      emit(g.kind[v], in, out, node_attrs(g, v, in));
+    }
+  }
+
+  static std::vector<int32_t> lows(const std::vector<std::pair<int64_t, int64_t>>& rs) {
+    std::vector<int32_t> out;
+    for (auto& r : rs) out.push_back((int32_t)r.first);
+    return out;
+  }
+  static Shape extents(const std::vector<std::pair<int64_t, int64_t>>& rs) {
+    Shape out;
+    for (auto& r : rs) out.push_back(r.second - r.first);
+    return out;
+  }
+
+  // entry.groups() sorted by ranges; members sorted by tensor name
+  std::vector<std::pair<std::vector<std::pair<int64_t, int64_t>>, std::vector<int32_t>>> groups(
+      const Entry& e) const {
+    std::vector<std::pair<std::vector<std::pair<int64_t, int64_t>>, std::vector<int32_t>>> gs;
+    for (size_t i = 0; i < e.shards.size(); ++i) {
+      auto it = std::find_if(gs.begin(), gs.end(), [&](auto& g) { return g.first == e.ranges[i]; });
+      if (it == gs.end()) gs.push_back({e.ranges[i], {e.shards[i]}});
+      else it->second.push_back(e.shards[i]);
+    }
+    std::sort(gs.begin(), gs.end(), [](auto& a, auto& b) { return a.first < b.first; });
+    for (auto& g : gs)
+      std::stable_sort(g.second.begin(), g.second.end(),
+                       [&](int32_t a, int32_t b) { return p->P.tname[a] < p->P.tname[b]; });
+    return gs;
+  }
+
+  Program lower(const StageRec& st) {
+    const GraphData &L = p->L, &P = p->P;
+    {
+      std::vector<char> produced;
+      std::unordered_map<int32_t, char> prod_l;
+      for (int32_t v : st.lnodes)
+        for (int64_t j = L.out_off[v]; j < L.out_off[v + 1]; ++j) prod_l[L.outs[j]] = 1;
+      for (int32_t t : st.l_inputs)
+        if (!prod_l.count(t)) lt[t] = box_of(t);
+    }
+    run_nodes(L, st.lnodes, lt, 0);
+    std::unordered_map<int32_t, char> prod_p;
+    for (int32_t v : st.pnodes)
+      for (int64_t j = P.out_off[v]; j < P.out_off[v + 1]; ++j) prod_p[P.outs[j]] = 1;
+    std::vector<int32_t> done;
+    for (int32_t s : st.p_inputs) {
+      if (prod_p.count(s)) continue;
+      const int32_t ei = p->owner[s];
+      if (ei < 0) throw PlanError("shard without owner");
+      if (std::find(done.begin(), done.end(), ei) != done.end()) continue;
+      done.push_back(ei);
+      const Entry& e = p->entries[ei];
+      const int32_t box = box_of(e.logical);
+      if (e.mode == 0) {
+        for (size_t i = 0; i < e.shards.size(); ++i) {
+          const int32_t out = tensor(pt, e.shards[i], extents(e.ranges[i]));
+          emit(PQW_T_SLICE, {box}, {out}, lows(e.ranges[i]));
+        }
+        continue;
+      }
+      if (L.tflags[e.logical] & 1) throw PlanError("partial checkpoint over integer tensor");
+      for (auto& g : groups(e)) {
+        const Shape ext = extents(g.first);
+        std::vector<int32_t> frees;
+        for (size_t i = 0; i + 1 < g.second.size(); ++i) {
+          const int32_t v = vars_for("ps.", P.tname[g.second[i]], ext);
+          pt[g.second[i]] = v;
+          frees.push_back(v);
+        }
+        const int32_t sl = temp(ext);
+        emit(PQW_T_SLICE, {box}, {sl}, lows(g.first));
+        if (!frees.empty()) {
+          const int32_t last = tensor(pt, g.second.back(), ext);
+          std::vector<int32_t> ins{sl};
+          ins.insert(ins.end(), frees.begin(), frees.end());
+          emit(PQW_T_RESID, ins, {last}, {});
+        } else {
+          pt[g.second.back()] = sl;
+        }
+      }
+    }
+    run_nodes(P, st.pnodes, pt, 1);
+    // obligations (stages.py:316-340 order)
+    const Entry& e = p->entries[st.entry];
+    auto tit = lt.find(st.target);
+    if (tit == lt.end()) throw PlanError("target not computed");
+    const int32_t tgt = tit->second;
+    int32_t n_obl = 0;
+    auto shard_tensor = [&](int32_t s) {
+      auto it = pt.find(s);
+      if (it == pt.end()) throw PlanError("shard never computed");
+      return it->second;
+    };
+    if (e.mode == 0) {
+      for (size_t i = 0; i < e.shards.size(); ++i) {
+        const int32_t rhs = shard_tensor(e.shards[i]);
+        const Shape ext = extents(e.ranges[i]);
+        const int32_t lhs = temp(ext);
+        emit(PQW_T_SLICE, {tgt}, {lhs}, lows(e.ranges[i]));
+        emit(PQW_T_CHECK, {lhs, rhs}, {}, {n_obl});
+        n_obl += (int32_t)volume(ext);
+      }
+    } else {
+      for (auto& g : groups(e)) {
+        std::vector<int32_t> rhs;
+        for (int32_t s : g.second) rhs.push_back(shard_tensor(s));
+        const Shape ext = extents(g.first);
+        const int32_t lhs = temp(ext);
+        emit(PQW_T_SLICE, {tgt}, {lhs}, lows(g.first));
+        std::vector<int32_t> ins{lhs};
+        ins.insert(ins.end(), rhs.begin(), rhs.end());
+        emit(PQW_T_CHECKSUM, ins, {}, {n_obl});
+        n_obl += (int32_t)volume(ext);
+      }
+    }
+    Program out;
+    out.ir = {IR_MAGIC, (int32_t)shapes.size(), n_ops, n_obl};
+    for (auto& s : shapes) {
+      out.ir.push_back((int32_t)s.size());
+      for (auto d : s) out.ir.push_back((int32_t)d);
+    }
+    out.ir.insert(out.ir.end(), ops.begin(), ops.end());
+    out.consts = std::move(consts);
+    out.var_keys = std::move(var_keys);
+    return out;
+  }
+};
+
+Program lower_stage(const pqw_plan* p, int stage, uint64_t seed) {
+  Lowerer lw;
+  lw.p = p;
+  lw.seed = seed;
+  return lw.lower(p->stages[(size_t)stage]);
+}
+
+}  // namespace
+}  // namespace pqw
+
+using pqw::pfail;
+
+extern "C" {
+
+int pqw_plan_create(const pqw_graph_desc* logical, const pqw_graph_desc* parallel,
+                    const pqw_lineage_desc* lineage, const int64_t* consts, size_t n_consts,
+                    pqw_plan** out) {
+  if (!logical || !parallel || !lineage || !out || (n_consts && !consts))
+    return pfail(PQW_EINVAL, "null argument");
+  auto* p = new pqw_plan();
+  try {
+    p->L.load(*logical);
+    p->P.load(*parallel);
+    p->consts.assign(consts, consts + 3 * n_consts);
+    std::vector<std::string_view> lnames, snames;
+    std::string ls, ss;
+    pqw::split_names(lineage->logical_names, lineage->n_entries, ls, lnames);
+    int64_t n_sh = 0;
+    for (int64_t i = 0; i < lineage->n_entries; ++i) n_sh += lineage->n_shards[i];
+    pqw::split_names(lineage->shard_names, n_sh, ss, snames);
+    p->entry_of_logical.assign(p->L.nt(), -1);
+    p->entries.resize((size_t)lineage->n_entries);
+    int64_t k = 0, r = 0;
+    for (int64_t i = 0; i < lineage->n_entries; ++i) {
+      auto& e = p->entries[(size_t)i];
+      e.logical = p->L.find(lnames[(size_t)i]);
+      e.mode = lineage->mode[i];
+      if (e.logical < 0 || e.mode > 1) p->lineage_ok = false;
+      else p->entry_of_logical[e.logical] = (int32_t)i;
+      for (int32_t j = 0; j < lineage->n_shards[i]; ++j, ++k) {
+        const int32_t s = p->P.find(snames[(size_t)k]);
+        if (s < 0) p->lineage_ok = false;
+        e.shards.push_back(s);
+        std::vector<std::pair<int64_t, int64_t>> rs;
+        for (int32_t a = 0; a < lineage->shard_ndim[k]; ++a, ++r)
+          rs.push_back({lineage->ranges[2 * r], lineage->ranges[2 * r + 1]});
+        e.ranges.push_back(std::move(rs));
+      }
+    }
+  } catch (const std::exception& ex) {
+    delete p;
+    return pfail(PQW_EINVAL, std::string("plan load: ") + ex.what());
+  }
+  *out = p;
+  return PQW_OK;
+}
+
+void pqw_plan_destroy(pqw_plan* p) { delete p; }
+
+int pqw_plan_validate(pqw_plan* p) {
+  if (!p) return pfail(PQW_EINVAL, "null plan");
+  std::string why;
+  if (!pqw::validate_graph(p->L, why)) return pfail(PQW_EPLAN, "logical graph: " + why);
+  if (!pqw::validate_graph(p->P, why)) return pfail(PQW_EPLAN, "parallel graph: " + why);
+  p->validated = true;
+  return PQW_OK;
+}
+
+int pqw_plan_build_stages(pqw_plan* p, int64_t out[3]) {
+  if (!p || !out) return pfail(PQW_EINVAL, "null argument");
+  if (!p->L.resolved || !p->P.resolved || !p->lineage_ok || !p->L.unique_producers ||
+      !p->P.unique_producers)
+    return pfail(PQW_EPLAN, "lineage or producers not well formed");
+  try {
+    pqw::build(p);
+  } catch (const std::exception& ex) {
+    p->stages.clear();
+    return pfail(PQW_EPLAN, std::string("build_stages: ") + ex.what());
+  }
+  p->built = true;
+  out[0] = (int64_t)p->stages.size();
+  out[1] = (int64_t)p->uncovered[0].size();
+  out[2] = (int64_t)p->uncovered[1].size();
+  return PQW_OK;
+}
+
+int pqw_plan_stage_target(pqw_plan* p, int stage) {
+  if (!p || !p->built || stage < 0 || (size_t)stage >= p->stages.size())
+    return pfail(PQW_EINVAL, "bad stage");
+  return p->stages[(size_t)stage].target;
+}
+
+long pqw_plan_stage_nodes(pqw_plan* p, int stage, int side, int32_t* out, size_t cap) {
+  if (!p || !p->built || stage < 0 || (size_t)stage >= p->stages.size())
+    return pfail(PQW_EINVAL, "bad stage");
+  const auto& st = p->stages[(size_t)stage];
+  const auto& v = side == 0 ? st.lnodes : side == 1 ? st.pnodes : side == 2 ? st.l_inputs
+                                                                              : st.p_inputs;
+  if (out) std::memcpy(out, v.data(), std::min(cap, v.size()) * sizeof(int32_t));
+  return (long)v.size();
+}
+
+long pqw_plan_uncovered(pqw_plan* p, int side, int32_t* out, size_t cap) {
+  if (!p || !p->built) return pfail(PQW_ESTATE, "stages not built");
+  const auto& v = p->uncovered[side ? 1 : 0];
+  if (out) std::memcpy(out, v.data(), std::min(cap, v.size()) * sizeof(int32_t));
+  return (long)v.size();
+}
+
+int pqw_plan_add_stages(pqw_plan* p, pqw_engine* e, uint64_t seed, const int32_t* stages, size_t n,
+                        int32_t* out_index) {
+  if (!p || !e || !out_index) return pfail(PQW_EINVAL, "null argument");
+  if (!p->built) return pfail(PQW_ESTATE, "stages not built");
+  std::vector<int32_t> list;
+  if (stages) list.assign(stages, stages + n);
+  else {
+    n = p->stages.size();
+    for (size_t i = 0; i < n; ++i) list.push_back((int32_t)i);
+  }
+  for (int32_t s : list)
+    if (s < 0 || (size_t)s >= p->stages.size()) return pfail(PQW_EINVAL, "bad stage index");
+  std::vector<pqw::Program> progs(n);
+  std::vector<char> bad(n, 0);
+  pqw::parallel_for(n, [&](size_t i, unsigned) {
+    try {
+      progs[i] = pqw::lower_stage(p, list[i], seed);
+    } catch (const std::exception&) {
+      bad[i] = 1;
+    }
+  });
+  int64_t status[16];
+  for (size_t i = 0; i < n; ++i) {
+    if (bad[i]) {
+      out_index[i] = PQW_EPLAN;
+      continue;
+    }
+    auto& pg = progs[i];
+    const int idx = pqw_stage_add(e, pg.ir.data(), pg.ir.size(), pg.consts.data(),
+                                  pg.consts.size() / 3, pg.var_keys.data(), pg.var_keys.size(),
+                                  status);
+    if (idx < 0) return idx;
+    out_index[i] = idx;
+    pqw::Program().ir.swap(pg.ir);
+  }
+  return PQW_OK;
+}
+
+int pqw_plan_stage_program(pqw_plan* p, int stage, uint64_t seed, int32_t* ir, size_t ir_cap,
+                           int64_t* consts, size_t consts_cap, uint64_t* var_keys, size_t vk_cap,
+                           int64_t lens[3]) {
+  if (!p || !lens) return pfail(PQW_EINVAL, "null argument");
+  if (!p->built || stage < 0 || (size_t)stage >= p->stages.size())
+    return pfail(PQW_EINVAL, "bad stage");
+  pqw::Program pg;
+  try {
+    pg = pqw::lower_stage(p, stage, seed);
+  } catch (const std::exception& ex) {
+    return pfail(PQW_EPLAN, std::string("lower: ") + ex.what());
+  }
+  lens[0] = (int64_t)pg.ir.size();
+  lens[1] = (int64_t)pg.consts.size() / 3;
+  lens[2] = (int64_t)pg.var_keys.size();
+  if (ir) std::memcpy(ir, pg.ir.data(), std::min(ir_cap, pg.ir.size()) * 4);
+  if (consts) std::memcpy(consts, pg.consts.data(), std::min(consts_cap * 3, pg.consts.size()) * 8);
+  if (var_keys)
+    std::memcpy(var_keys, pg.var_keys.data(), std::min(vk_cap, pg.var_keys.size()) * 8);
+  return PQW_OK;
+}
+
+}  // extern "C"

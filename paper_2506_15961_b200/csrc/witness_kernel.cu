@@ -40,6 +40,8 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 }  // namespace
+
+int set_last_error(int code, const std::string& msg) { return fail(code, msg); }
 }  // namespace pqw
 
 struct pqw_engine {
@@ -50,6 +52,7 @@ struct pqw_engine {
   // deferred front ends: per stage, the stage it duplicates (-1: compile its
   // own text, kept in cache_src) and its var base; front_done once compiled
   std::vector<int> alias;
+  std::vector<uint8_t> active;   // pqw_stage_select: only active stages are scheduled/uploaded
   std::vector<uint32_t> pend_nvars, pend_base;
   std::vector<char> front_done;
   size_t n_front_pending = 0;
@@ -74,6 +77,7 @@ struct pqw_engine {
   uint32_t* d_n_bad = nullptr;
   uint32_t* d_probe = nullptr;
   size_t scratch_bytes = 0;
+  uint64_t h2d_bytes = 0;  // bytes the last pqw_upload copied host -> device
   uint32_t n_gpu_stages = 0;
   uint32_t max_slots = 0;
   uint32_t smem_slots = 0;
@@ -136,9 +140,12 @@ static int finalize_all(pqw_engine* e) {
   }
   std::vector<pqw::CompiledStage*> todo;
   std::unordered_map<const pqw::StageBackend*, int> seen;
-  for (auto& st : e->stages)
-    if (st.status == PQW_STAGE_OK && !st.be->ready && seen.emplace(st.be.get(), 1).second)
+  for (size_t i = 0; i < e->stages.size(); ++i) {
+    auto& st = e->stages[i];
+    if (e->active[i] && st.status == PQW_STAGE_OK && !st.be->ready &&
+        seen.emplace(st.be.get(), 1).second)
       todo.push_back(&st);
+  }
   if (todo.empty()) return PQW_OK;
   // largest first, handed out through a shared counter
   std::sort(todo.begin(), todo.end(), [](const pqw::CompiledStage* a, const pqw::CompiledStage* b) {
@@ -289,6 +296,7 @@ int pqw_stage_add(pqw_engine* e, const int32_t* ir, size_t ir_len, const int64_t
   }
   e->stages.emplace_back();
   e->alias.push_back(alias);
+  e->active.push_back(1);
   e->pend_nvars.push_back((uint32_t)n_vars);
   e->pend_base.push_back(base);
   e->front_done.push_back(0);
@@ -350,6 +358,26 @@ static int finalize_front(pqw_engine* e) {
   return PQW_OK;
 }
 
+int pqw_stage_select(pqw_engine* e, const uint8_t* active, size_t n) {
+  if (!e || !active) return fail(PQW_EINVAL, "null argument");
+  if (n != e->stages.size()) return fail(PQW_EINVAL, "select: one flag per stage");
+  e->active.assign(active, active + n);
+  e->uploaded = false;
+  return PQW_OK;
+}
+
+int64_t pqw_stage_cost(pqw_engine* e, int stage) {
+  if (!e) return fail(PQW_EINVAL, "null engine");
+  if (stage < 0 || (size_t)stage >= e->stages.size()) return fail(PQW_EINVAL, "bad stage");
+  {
+    int rc = finalize_front(e);
+    if (rc != PQW_OK) return rc;
+  }
+  const auto& st = e->stages[stage];
+  if (st.status != PQW_STAGE_OK || !st.dag) return 0;
+  return (int64_t)st.dag->units.size();
+}
+
 int pqw_stage_status(pqw_engine* e, int stage, int64_t out_status[16]) {
   if (!e || !out_status) return fail(PQW_EINVAL, "null argument");
   if (stage < 0 || (size_t)stage >= e->stages.size()) return fail(PQW_EINVAL, "bad stage");
@@ -389,6 +417,7 @@ int pqw_reset(pqw_engine* e) {
   }
   e->stages.clear();
   e->alias.clear();
+  e->active.clear();
   e->pend_nvars.clear();
   e->pend_base.clear();
   e->front_done.clear();
@@ -449,7 +478,7 @@ int pqw_upload(pqw_engine* e) {
   // stages that need the GPU, longest first (LPT order for the work queue)
   std::vector<int> ids;
   for (size_t i = 0; i < e->stages.size(); ++i)
-    if (e->stages[i].status == PQW_STAGE_OK) ids.push_back((int)i);
+    if (e->active[i] && e->stages[i].status == PQW_STAGE_OK) ids.push_back((int)i);
   std::stable_sort(ids.begin(), ids.end(), [&](int a, int b) {
     return e->stages[a].prog().code.size() > e->stages[b].prog().code.size();
   });
@@ -543,6 +572,9 @@ int pqw_upload(pqw_engine* e) {
   CU(cudaMalloc(&e->d_n_valid, nr * sizeof(uint32_t)));
   CU(cudaMalloc(&e->d_n_bad, nr * sizeof(uint32_t)));
   CU(cudaMalloc(&e->d_probe, 2 * sizeof(uint32_t)));
+  e->h2d_bytes = code.size() * sizeof(pqw_ins) + descs.size() * sizeof(pqw::StageDesc) +
+                 work.size() * sizeof(uint32_t) + e->var_keys.size() * sizeof(uint64_t) +
+                 3 * sizeof(uint64_t);
   if (!e->ev0) CU(cudaEventCreate(&e->ev0));
   if (!e->ev1) CU(cudaEventCreate(&e->ev1));
   e->uploaded = true;
@@ -739,8 +771,9 @@ int pqw_image_stats(pqw_engine* e, uint64_t* out, size_t cap) {
     if (rc != PQW_OK) return rc;
   }
   uint64_t n_gpu = 0, n_code = 0, max_slots = 0, max_spill = 0, bundles = 0, waits = 0;
-  for (const auto& st : e->stages) {
-    if (st.status != PQW_STAGE_OK) continue;
+  for (size_t si = 0; si < e->stages.size(); ++si) {
+    const auto& st = e->stages[si];
+    if (st.status != PQW_STAGE_OK || !e->active[si]) continue;
     n_gpu++;
     const auto& pr = st.prog();
     n_code += pr.code.size();
@@ -760,6 +793,8 @@ int pqw_image_stats(pqw_engine* e, uint64_t* out, size_t cap) {
   buf[11 + N] = max_spill;
   buf[12 + N] = bundles;
   buf[13 + N] = waits;
+  buf[14 + N] = e->h2d_bytes;
+  buf[15 + N] = (uint64_t)e->n_gpu_stages * (sizeof(unsigned long long) + 2 * sizeof(uint32_t));
   std::memcpy(out, buf, std::min(cap, (size_t)PQW_IMAGE_STATS_LEN) * sizeof(uint64_t));
   return PQW_OK;
 }

@@ -18,7 +18,7 @@ from .errors import EngineError, EngineUnavailable
 
 LIB_NAME = "libplaneq_witness.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 # PQW_STAGE_* codes
 STAGE_OK = 0
@@ -33,13 +33,18 @@ STAGE_PENDING = 6
 BOP_NAMES = ("END", "DOT", "SUM", "SUB", "NEG", "HASH", "INV", "VAR", "CONST", "CHK", "DEN",
              "FILL", "SPILL", "WAIT", "SIGNAL")
 N_BOPS = len(BOP_NAMES)
-IMAGE_STATS_LEN = 14 + N_BOPS
+IMAGE_STATS_LEN = 16 + N_BOPS
 FIELD_CLASSES = ("mul", "add", "hash", "inv", "cmp")
 
 EXPORTS = ("pqw_abi_version", "pqw_last_error", "pqw_device_count", "pqw_engine_create",
            "pqw_engine_destroy", "pqw_stage_add", "pqw_stage_status", "pqw_reset", "pqw_stage_bytecode",
            "pqw_obligation_support", "pqw_upload", "pqw_launch", "pqw_results", "pqw_probe",
-           "pqw_last_launch_ms", "pqw_image_stats", "pqw_peak_fieldops")
+           "pqw_last_launch_ms", "pqw_image_stats", "pqw_peak_fieldops", "pqw_stage_select",
+           "pqw_stage_cost",
+           # native plan core (native.py)
+           "pqw_plan_create", "pqw_plan_destroy", "pqw_plan_validate", "pqw_plan_build_stages",
+           "pqw_plan_stage_target", "pqw_plan_stage_nodes", "pqw_plan_uncovered",
+           "pqw_plan_add_stages", "pqw_plan_stage_program")
 
 
 class _Ins(C.Structure):
@@ -97,6 +102,10 @@ def load_library(path: str | None = None):
     lib.pqw_last_launch_ms.restype = C.c_int
     lib.pqw_image_stats.argtypes = [C.c_void_p, u64p, C.c_size_t]
     lib.pqw_image_stats.restype = C.c_int
+    lib.pqw_stage_select.argtypes = [C.c_void_p, C.POINTER(C.c_uint8), C.c_size_t]
+    lib.pqw_stage_select.restype = C.c_int
+    lib.pqw_stage_cost.argtypes = [C.c_void_p, C.c_int]
+    lib.pqw_stage_cost.restype = C.c_int64
     lib.pqw_peak_fieldops.argtypes = [C.c_int, C.POINTER(C.c_double)]
     lib.pqw_peak_fieldops.restype = C.c_int
     if lib.pqw_abi_version() != ABI_VERSION:
@@ -217,6 +226,10 @@ class Engine:
         self.n_stages += 1
         return _LazyStage(self, idx)
 
+    def stage_lazy(self, idx: int) -> "StageCompile":
+        """Compile handle of an already queued stage (resolved on first use)."""
+        return _LazyStage(self, idx)
+
     def stage_status(self, idx: int) -> StageCompile:
         st = np.zeros(16, dtype=np.int64)
         self._check(self.lib.pqw_stage_status(self._h, idx, _ptr(st, C.c_int64)))
@@ -229,6 +242,15 @@ class Engine:
                             exact_rhs=None if st[11] == imin else int(st[11]),
                             field_ops=int(st[12]), n_vars=int(st[13]),
                             spill_slots=int(st[14]), bundles=int(st[15]))
+
+    def select(self, active) -> None:
+        """Schedule and upload only the stages whose flag is set."""
+        a = np.ascontiguousarray(np.asarray(active, dtype=np.uint8))
+        self._check(self.lib.pqw_stage_select(self._h, _ptr(a, C.c_uint8), a.size))
+
+    def cost(self, idx: int) -> int:
+        """Front-end device cost of a queued stage (0: decided at compile time)."""
+        return int(self._check(self.lib.pqw_stage_cost(self._h, idx)))
 
     def reset(self):
         self._check(self.lib.pqw_reset(self._h))
@@ -287,4 +309,5 @@ class Engine:
                 "unique_instructions": int(out[4 + n]), "cache_hits": int(out[5 + n]),
                 "field_ops": {FIELD_CLASSES[i]: int(out[6 + n + i]) for i in range(5)},
                 "max_spill_slots": int(out[11 + n]), "bundles": int(out[12 + n]),
-                "waits": int(out[13 + n])}
+                "waits": int(out[13 + n]), "h2d_bytes": int(out[14 + n]),
+                "d2h_bytes": int(out[15 + n])}

@@ -18,10 +18,12 @@ import time
 from dataclasses import asdict, dataclass
 from typing import Any
 
+import numpy as np
+
 from . import field as F
 from .engine import (STAGE_BAD_INDEX, STAGE_LOG_DIV0, STAGE_OK, STAGE_PAR_DIV0, STAGE_PROVEN,
                      STAGE_REFUTED_CONST, Engine)
-from .errors import GraphError, PlanEqError, UncoveredNode
+from .errors import EngineError, GraphError, PlanEqError, UncoveredNode
 from .graph import validate_lineage
 from .opshape import validate_concrete
 from .plan import Plan
@@ -43,7 +45,7 @@ class VerifyOptions:
     # witness engine
     witnesses: int = DEFAULT_WITNESSES
     seed: int = 0
-    device: int = 0
+    device: int | None = None  # None: LOCAL_RANK under torchrun, else 0
     shard: bool = True  # under torch.distributed (world > 1): split stages over the ranks
 
 
@@ -54,30 +56,6 @@ def _aggregate(results: list[StageResult], cancelled: int) -> str:
     if "unknown" in statuses or cancelled or not results:
         return "unknown"
     return "proven"
-
-
-class _Deferred:
-    """An exception raised while lowering a stage, re-raised in stage order."""
-
-    def __init__(self, exc: BaseException):
-        self.exc = exc
-
-
-def compile_stages(plan: Plan, stages: list[Stage], engine: Engine, seed: int):
-    """Lower and compile every stage into `engine`. Returns per-stage
-    (LoweredStage | _Deferred, StageCompile | None, compile seconds)."""
-    owner = shard_owner(plan, entry_order(plan))
-    out = []
-    for st in stages:
-        t0 = time.perf_counter()
-        try:
-            lw = lower_stage(plan, st, owner, seed)
-        except PlanEqError as e:
-            out.append((_Deferred(e), None, time.perf_counter() - t0))
-            continue
-        comp = engine.add_stage(lw.ir, lw.consts, lw.var_keys)
-        out.append((lw, comp, time.perf_counter() - t0))
-    return out
 
 
 def _const_detail(lw: LoweredStage, comp) -> dict[str, Any]:
@@ -114,82 +92,203 @@ def _witness_detail(engine: Engine, lw: LoweredStage, comp, first_bad: int,
     }
 
 
+class _StageRef:
+    """One stage of a discharge: its target, how to lower it on the host (for
+    counterexample reports and to raise deferred lowering errors), and its
+    engine compile handle (None when the host lowering raises)."""
+
+    __slots__ = ("target", "lower", "comp", "lw")
+
+    def __init__(self, target: str, lower, comp, lw=None):
+        self.target, self.lower, self.comp, self.lw = target, lower, comp, lw
+
+    def lowered(self) -> LoweredStage:
+        if self.lw is None:
+            self.lw = self.lower()
+        return self.lw
+
+
+def _run(refs: list[_StageRef], eng: Engine, opts: VerifyOptions, host_s: float,
+         stats: dict, errors: str = "raise") -> tuple[list, int, dict]:
+    """Compile (pending front/back ends), launch once, and turn the engine's
+    per-stage outcome into StageResults in stage order with the reference's
+    cancellation (verify.py:119-122). errors="collect": a stage whose
+    discharge raises yields a distributed.StageFailure in its place."""
+    t0 = time.perf_counter()
+    comps = [r.comp for r in refs]
+    needs_gpu = any(c is not None and c.status == STAGE_OK for c in comps)
+    gpu_ms = 0.0
+    fb = nv = nb = None
+    if needs_gpu:
+        eng.upload()
+        eng.launch(opts.witnesses)
+        fb, nv, nb = eng.results()
+        gpu_ms = eng.last_launch_ms()
+    t_dev = time.perf_counter() - t0
+    n_gpu = sum(1 for c in comps if c is not None and c.status == STAGE_OK)
+    per_stage = (host_s + t_dev) / max(len(refs), 1)
+    results: list[StageResult] = []
+    cancelled = 0
+    for ref in refs:
+        try:
+            r = _one(ref, eng, opts, fb, nv, nb, per_stage)
+        except PlanEqError as e:
+            if errors != "collect":
+                raise
+            from .distributed import StageFailure
+            results.append(StageFailure(e))
+            continue
+        results.append(r)
+        if r.status == "refuted" and not opts.no_cancel:
+            cancelled = len(refs) - len(results)
+            break
+    stats.update({"gpu_ms": round(gpu_ms, 4), "gpu_stages": n_gpu, "witnesses": opts.witnesses,
+                  "device_s": round(t_dev, 6)})
+    if needs_gpu:
+        stats.update(eng.image_stats())
+    return results, cancelled, stats
+
+
+def _device(opts: VerifyOptions) -> int:
+    if opts.device is not None:
+        return opts.device
+    from .distributed import local_device
+    return local_device()
+
+
+def _one(ref: _StageRef, eng: Engine, opts: VerifyOptions, fb, nv, nb,
+         per_stage: float) -> StageResult:
+    comp = ref.comp
+    if comp is None:
+        ref.lowered()  # the host lowering raises the reference's exception
+        raise EngineError(f"stage {ref.target}: the native lowering declined a stage "
+                          "the host lowers")
+    r = StageResult(ref.target, "proven", comp.obligations, comp.fast, comp.residual,
+                    per_stage, degree_bound=comp.degree)
+    if comp.status == STAGE_PROVEN:
+        r.note = "closed by value numbering"
+    elif comp.status == STAGE_REFUTED_CONST:
+        r.status = "refuted"
+        r.detail = _const_detail(ref.lowered(), comp)
+    elif comp.status == STAGE_PAR_DIV0:
+        r = StageResult(ref.target, "refuted", 0, 0, 0, per_stage,
+                        {"reason": "parallel side divides by zero: "
+                                   "constant denominator violates side condition"})
+    elif comp.status == STAGE_LOG_DIV0:
+        raise GraphError(f"stage {ref.target}: logical side divides by zero: "
+                         "constant denominator violates side condition")
+    elif comp.status == STAGE_BAD_INDEX:
+        raise GraphError(f"stage {ref.target}: token id outside its embedding table")
+    else:
+        i = comp.index
+        r.witnesses = opts.witnesses
+        r.valid_witnesses = int(nv[i])
+        r.failing_witnesses = int(nb[i])
+        r.false_equiv_log2 = bound_log2(comp.degree, int(nv[i]))
+        if int(fb[i]) != 0xFFFFFFFFFFFFFFFF:
+            r.status = "refuted"
+            r.detail = _witness_detail(eng, ref.lowered(), comp, int(fb[i]), opts.seed)
+        elif int(nv[i]) == 0:
+            r.status = "unknown"
+            r.note = "no witness kept every denominator nonzero"
+    return r
+
+
 def discharge(plan: Plan, stages: list[Stage], opts: VerifyOptions,
-              engine: Engine | None = None) -> tuple[list[StageResult], int, dict]:
-    """Run every stage through the witness engine; returns (results, cancelled, stats)."""
+              engine: Engine | None = None, errors: str = "raise") -> tuple[list, int, dict]:
+    """Run every stage (host Stage records, lowered by stages.lower_stage)
+    through the witness engine; returns (results, cancelled, stats)."""
     own = engine is None
-    eng = engine or Engine(opts.device, opts.seed, F.fn_keys(opts.seed))
+    eng = engine or Engine(_device(opts), opts.seed, F.fn_keys(opts.seed))
     try:
         t0 = time.perf_counter()
-        compiled = compile_stages(plan, stages, eng, opts.seed)
+        owner = shard_owner(plan, entry_order(plan))
+        refs = []
+        for st in stages:
+            try:
+                lw = lower_stage(plan, st, owner, opts.seed)
+            except PlanEqError as e:
+                refs.append(_StageRef(st.target, _raiser(e), None))
+                continue
+            refs.append(_StageRef(st.target, None, eng.add_stage(lw.ir, lw.consts, lw.var_keys), lw))
         t_compile = time.perf_counter() - t0
-        needs_gpu = any(c is not None and c.status == STAGE_OK for _, c, _ in compiled)
-        gpu_ms = 0.0
-        fb = nv = nb = None
-        if needs_gpu:
-            eng.upload()
-            eng.launch(opts.witnesses)
-            fb, nv, nb = eng.results()
-            gpu_ms = eng.last_launch_ms()
-        n_gpu = sum(1 for _, c, _ in compiled if c is not None and c.status == STAGE_OK)
-        share = (gpu_ms / 1e3) / n_gpu if n_gpu else 0.0
-        results: list[StageResult] = []
-        cancelled = 0
-        for st, (lw, comp, t_c) in zip(stages, compiled):
-            if isinstance(lw, _Deferred):
-                raise lw.exc
-            r = StageResult(st.target, "proven", comp.obligations, comp.fast, comp.residual,
-                            t_c, degree_bound=comp.degree)
-            if comp.status == STAGE_PROVEN:
-                r.note = "closed by value numbering"
-            elif comp.status == STAGE_REFUTED_CONST:
-                r.status = "refuted"
-                r.detail = _const_detail(lw, comp)
-            elif comp.status == STAGE_PAR_DIV0:
-                r = StageResult(st.target, "refuted", 0, 0, 0, t_c,
-                                {"reason": "parallel side divides by zero: "
-                                           "constant denominator violates side condition"})
-            elif comp.status == STAGE_LOG_DIV0:
-                raise GraphError(f"stage {st.target}: logical side divides by zero: "
-                                 "constant denominator violates side condition")
-            elif comp.status == STAGE_BAD_INDEX:
-                raise GraphError(f"stage {st.target}: token id outside its embedding table")
-            else:
-                i = comp.index
-                r.witnesses = opts.witnesses
-                r.valid_witnesses = int(nv[i])
-                r.failing_witnesses = int(nb[i])
-                r.wall_s = t_c + share
-                r.false_equiv_log2 = bound_log2(comp.degree, int(nv[i]))
-                if int(fb[i]) != 0xFFFFFFFFFFFFFFFF:
-                    r.status = "refuted"
-                    r.detail = _witness_detail(eng, lw, comp, int(fb[i]), opts.seed)
-                elif int(nv[i]) == 0:
-                    r.status = "unknown"
-                    r.note = "no witness kept every denominator nonzero"
-            results.append(r)
-            if r.status == "refuted" and not opts.no_cancel:
-                cancelled = len(stages) - len(results)
-                break
-        stats = {"compile_s": round(t_compile, 6), "gpu_ms": round(gpu_ms, 4),
-                 "gpu_stages": n_gpu, "witnesses": opts.witnesses}
-        if needs_gpu:
-            stats.update(eng.image_stats())
-        return results, cancelled, stats
+        stats = {"host_path": "python", "compile_s": round(t_compile, 6)}
+        return _run(refs, eng, opts, t_compile, stats, errors)
     finally:
         if own:
             eng.close()
 
 
+def _raiser(exc: BaseException):
+    def f():
+        raise exc
+    return f
+
+
+def discharge_native(nplan, opts: VerifyOptions, engine: Engine | None = None,
+                     which: list[int] | None = None, indices=None,
+                     errors: str = "raise") -> tuple[list, int, dict]:
+    """Run the stages of a NativePlan (all, or the listed indices) through the
+    witness engine: lowering and compilation in C++ on host threads.
+    `indices`: engine indices of every plan stage already queued into
+    `engine` (NativePlan.add_stages), so nothing is lowered twice."""
+    plan = nplan.plan
+    own = engine is None
+    eng = engine or Engine(_device(opts), opts.seed, F.fn_keys(opts.seed))
+    try:
+        t0 = time.perf_counter()
+        sel = list(range(nplan.n_stages)) if which is None else list(which)
+        if indices is None:
+            idx = nplan.add_stages(eng, opts.seed, which)
+        else:
+            idx = np.asarray([indices[i] for i in sel], dtype=np.int32)
+        targets = nplan.targets()
+        owner = None
+        refs = []
+        for k, i in zip(idx.tolist(), sel):
+            def lower(i=i):
+                nonlocal owner
+                if owner is None:
+                    owner = shard_owner(plan, entry_order(plan))
+                return lower_stage(plan, nplan.stage(i), owner, opts.seed)
+            refs.append(_StageRef(targets[i], lower, eng.stage_lazy(k) if k >= 0 else None))
+        t_add = time.perf_counter() - t0
+        stats = {"host_path": "native", "lower_s": round(t_add, 6)}
+        return _run(refs, eng, opts, t_add, stats, errors)
+    finally:
+        if own:
+            eng.close()
+
+
+def _native(plan: Plan):
+    """NativePlan of `plan`, or None when the native core declines it."""
+    from .native import NativePlan, PlanDeclined
+    try:
+        return NativePlan(plan)
+    except PlanDeclined:
+        return None
+
+
 def verify_plan(plan: Plan, opts: VerifyOptions | None = None) -> dict[str, Any]:
+    """The reference's verify_plan (verify.py:62-145): validation, optional
+    shape reduction, stage construction, discharge, one verdict. Stage
+    construction and lowering run in the native core; the host's own checks
+    run only when it declines a plan (they raise the reference's errors)."""
     opts = opts or VerifyOptions()
     t0 = time.perf_counter()
+    times: dict[str, float] = {}
     report: dict[str, Any] = {"verdict": "unknown", "stages": [], "jobs": opts.jobs}
     if plan.parallel is None or plan.lineage is None:
         raise GraphError("plan has no parallel graph or no lineage")
-    validate_concrete(plan.logical)
-    validate_concrete(plan.parallel)
+    nat = _native(plan)
+    times["pack_s"] = time.perf_counter() - t0
+    t = time.perf_counter()
+    if nat is None or not nat.validate():
+        validate_concrete(plan.logical)
+        validate_concrete(plan.parallel)
+        nat = None  # well formed after all: the host path takes it from here
     problems = validate_lineage(plan.logical, plan.parallel, plan.lineage)
+    times["validate_s"] = time.perf_counter() - t
     tiling = [p for p in problems if "do not tile" in p]
     hard = [p for p in problems if "do not tile" not in p]
     if hard:
@@ -206,8 +305,17 @@ def verify_plan(plan: Plan, opts: VerifyOptions | None = None) -> dict[str, Any]
                           timeout_s=opts.timeout_s)
         work = red.plan
         report["reduction"] = red.report
+        if work is not plan:
+            nat = _native(work)
 
-    stages, uncovered = build_stages(work)
+    t = time.perf_counter()
+    if nat is not None and nat.build_stages():
+        stages = None
+        uncovered = nat.uncovered()
+    else:
+        nat = None
+        stages, uncovered = build_stages(work)
+    times["build_stages_s"] = time.perf_counter() - t
     report["uncovered"] = uncovered
     loose = uncovered["parallel"] + uncovered["logical"]
     if loose:
@@ -217,13 +325,21 @@ def verify_plan(plan: Plan, opts: VerifyOptions | None = None) -> dict[str, Any]
                              f"not checked: {loose[:8]}")
 
     from .distributed import discharge_sharded, world_info
+    t = time.perf_counter()
     if opts.shard and world_info()[1] > 1:
-        results, cancelled, stats = discharge_sharded(work, stages, opts)
+        results, cancelled, stats = discharge_sharded(work, stages, opts, nplan=nat)
+    elif nat is not None:
+        results, cancelled, stats = discharge_native(nat, opts)
     else:
         results, cancelled, stats = discharge(work, stages, opts)
+    times["discharge_s"] = time.perf_counter() - t
+    n_stages = nat.n_stages if nat is not None else len(stages)
+    if nat is not None:
+        nat.close()
     verdict = _aggregate(results, cancelled)
     total_ob = sum(r.obligations for r in results)
     total_fast = sum(r.fastpath for r in results)
+    stats["times"] = {k: round(v, 6) for k, v in times.items()}
     report.update(
         verdict=verdict,
         stages=[asdict(r) for r in results],
@@ -233,7 +349,7 @@ def verify_plan(plan: Plan, opts: VerifyOptions | None = None) -> dict[str, Any]
         engine=stats,
         wall_s=round(time.perf_counter() - t0, 6),
     )
-    if not stages:
+    if not n_stages:
         report["note"] = "lineage has no produced checkpoints; nothing was proven"
     for r in results:
         if r.status == "refuted":

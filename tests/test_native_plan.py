@@ -1,0 +1,162 @@
+"""The native plan core (csrc/plan.cpp behind pqw_plan_*) against the host code it
+replaces on the verify path: opshape.validate_concrete, stages.build_stages and
+stages.lower_stage (which restate the reference's shapes.py:35-45,
+stages.py:79-176 and :267-340).
+
+On every golden plan (the reference's toy/fault/random corpus, the Llama and
+DeepSeek families): the same stages (targets, slices in topological order,
+boundaries, assumed checkpoints, owned nodes, uncovered nodes) and, word for
+word, the same tensor-op program, constant table and variable keys per stage.
+On malformed plans: the native core declines, and verify_plan raises the
+reference's exception (the host checks run on the declined plan).
+"""
+
+import copy
+import json
+import os
+
+import numpy as np
+import pytest
+
+from golden_io import GOLDEN, load_plan, verdicts
+from paper_2506_15961_b200.errors import (CycleError, DanglingTensorError, GraphError,
+                                          PlanFormatError, ShapeError, UnknownOperator)
+from paper_2506_15961_b200.graph import Node, Tensor
+from paper_2506_15961_b200.native import NativePlan
+from paper_2506_15961_b200.opshape import validate_concrete
+from paper_2506_15961_b200.stages import build_stages, entry_order, lower_stage, shard_owner
+from paper_2506_15961_b200.verify import VerifyOptions, verify_plan
+
+
+def _golden_plans():
+    out = [(r["name"], r["work_plan"]) for r in verdicts() if r.get("work_plan")]
+    for fname in ("verdicts_llama.json", "verdicts_deepseek.json"):
+        p = os.path.join(GOLDEN, fname)
+        if os.path.exists(p):
+            out += [(r["name"], r["plan"]) for r in json.load(open(p))["plans"]]
+    return out
+
+
+PLANS = _golden_plans()
+
+
+def _python_ok(fn, *a):
+    try:
+        return True, fn(*a)
+    except Exception as e:  # noqa: BLE001
+        return False, e
+
+
+@pytest.mark.parametrize("name,rel", PLANS, ids=[n for n, _ in PLANS])
+def test_native_stages_and_programs_match_host(lib, name, rel):
+    plan = load_plan(rel)
+    nat = NativePlan(plan)
+    ok_py = all(_python_ok(validate_concrete, g)[0] for g in (plan.logical, plan.parallel))
+    assert nat.validate() == ok_py, name
+    ok, got = _python_ok(build_stages, plan)
+    assert nat.build_stages() == ok, (name, got)
+    if not ok:
+        return
+    stages, unc = got
+    nst = nat.stages()
+    assert [s.target for s in nst] == [s.target for s in stages]
+    for a, b in zip(stages, nst):
+        assert [n.id for n in a.logical_nodes] == [n.id for n in b.logical_nodes], a.target
+        assert [n.id for n in a.parallel_nodes] == [n.id for n in b.parallel_nodes], a.target
+        assert (a.l_inputs, a.p_inputs, a.assumed) == (b.l_inputs, b.p_inputs, b.assumed)
+        assert (a.owned_logical, a.owned_parallel) == (b.owned_logical, b.owned_parallel)
+    assert nat.uncovered() == unc
+    owner = shard_owner(plan, entry_order(plan))
+    for i, st in enumerate(stages):
+        seed = 11 + i
+        ok, lw = _python_ok(lower_stage, plan, st, owner, seed)
+        if not ok:
+            with pytest.raises(Exception):
+                nat.stage_program(i, seed)
+            continue
+        ir, cs, vk = nat.stage_program(i, seed)
+        assert np.array_equal(ir, lw.ir), st.target
+        assert np.array_equal(cs, lw.consts.reshape(-1, 3)), st.target
+        assert np.array_equal(vk, lw.var_keys), st.target
+    nat.close()
+
+
+def _base():
+    rec = next(r for r in verdicts() if r["name"] == "tp2")
+    return load_plan(rec["work_plan"])
+
+
+def _first(g, kind):
+    return next(i for i, n in enumerate(g.nodes) if n.kind == kind)
+
+
+def _mutations():
+    def shape(plan):
+        g = plan.parallel
+        n = g.nodes[_first(g, "matmul")]
+        t = g.tensors[n.outputs[0]]
+        g.tensors[t.id] = Tensor(t.id, tuple(t.shape[:-1]) + (t.shape[-1] + 1,), t.role, t.dtype,
+                                 t.device, t.microbatch, dict(t.meta))
+        return ShapeError
+
+    def unknown(plan):
+        g = plan.logical
+        i = _first(g, "add")
+        g.nodes[i] = copy.replace(g.nodes[i], kind="frobnicate") if hasattr(copy, "replace") \
+            else Node(g.nodes[i].id, "frobnicate", g.nodes[i].inputs, g.nodes[i].outputs,
+                      dict(g.nodes[i].attrs), g.nodes[i].device, g.nodes[i].seq)
+        return UnknownOperator
+
+    def dangling(plan):
+        g = plan.parallel
+        i = _first(g, "mul")
+        n = g.nodes[i]
+        g.tensors["ghost"] = Tensor("ghost", g.tensors[n.inputs[0]].shape)
+        g.nodes[i] = Node(n.id, n.kind, ("ghost",) + tuple(n.inputs[1:]), n.outputs,
+                          dict(n.attrs), n.device, n.seq)
+        return DanglingTensorError
+
+    def cycle(plan):
+        g = plan.logical
+        i = _first(g, "add")
+        n = g.nodes[i]
+        later = next(m for m in g.nodes[i + 1:] if m.kind in ("add", "mul")
+                     and g.tensors[m.outputs[0]].shape == g.tensors[n.inputs[0]].shape)
+        g.nodes[i] = Node(n.id, n.kind, (later.outputs[0],) + tuple(n.inputs[1:]), n.outputs,
+                          dict(n.attrs), n.device, n.seq)
+        return (CycleError, GraphError)
+
+    def twice(plan):
+        g = plan.parallel
+        a = g.nodes[_first(g, "mul")]
+        b = next(m for m in g.nodes if m.kind == "add")
+        i = g.nodes.index(b)
+        g.nodes[i] = Node(b.id, b.kind, b.inputs, a.outputs, dict(b.attrs), b.device, b.seq)
+        return (PlanFormatError, GraphError, ShapeError)
+
+    return {"shape": shape, "unknown": unknown, "dangling": dangling, "cycle": cycle,
+            "twice": twice}
+
+
+@pytest.mark.parametrize("kind", sorted(_mutations()))
+def test_malformed_plans_are_declined_and_raise_the_host_error(lib, kind):
+    plan = _base()
+    want = _mutations()[kind](plan)
+    nat = NativePlan(plan)
+    declined = not nat.validate() or not nat.build_stages()
+    assert declined, kind
+    with pytest.raises(want):
+        verify_plan(plan, VerifyOptions(no_reduce=True))
+
+
+def test_verify_plan_reports_stage_errors_of_the_host(lib):
+    """A graph input without a checkpoint entry: the native build declines and
+    the host's build_stages raises its GraphError."""
+    plan = _base()
+    victim = next(t for t in plan.logical.inputs if t in plan.lineage)
+    del plan.lineage[victim]
+    nat = NativePlan(plan)
+    assert nat.validate()
+    assert not nat.build_stages()
+    with pytest.raises(GraphError):
+        build_stages(plan)

@@ -5,9 +5,10 @@ per stage of the *2-layer* plans), so at full size parity is checked against
 the oracle port -- itself pinned to the reference by tests/test_oracle_golden.py
 and the golden verdict corpora:
 
-* configs[1] (Llama3-8B TP4 PP2 DP2 SP) and configs[4] (DeepSeek-V3 MLA+MoE,
-  expert all_to_all): every distinct stage program, engine witness outcomes
-  (valid, failing, first failing witness/obligation) equal the oracle's;
+* configs[1] (Llama3-8B TP4 PP2 DP2 SP), configs[3] (Llama3-405B TP8 PP16 DP2)
+  and configs[4] (DeepSeek-V3 MLA+MoE, expert all_to_all): every distinct
+  stage program (exact program-text hash), engine witness outcomes (valid,
+  failing, first failing witness/obligation) equal the oracle's;
 * configs[2] (bug-injected Llama3-8B: wrong all-reduce scaling, misordered
   concat, dropped partial sum): verify_plan refutes each mutant, the refuted
   stage's counterexample is the oracle's first failing witness, and the clean
@@ -26,43 +27,68 @@ from paper_2506_15961_b200.workloads import get_workload
 W = 96  # three tiles, the last one ragged against the oracle's witness list
 
 
-def _distinct_gpu_stages(plan, stages, eng, seed, limit):
-    owner = shard_owner(plan, entry_order(plan))
+def distinct_programs(nat, seed):
+    """First stage index of every distinct stage program, keyed by the exact
+    program text (ir words + constant table): stages that differ only in their
+    variable keys share a program and a compiled image."""
+    import hashlib
     seen, picked = set(), []
-    for st in stages:
-        lw = lower_stage(plan, st, owner, seed)
-        key = (lw.ir.size, int(lw.ir[: min(64, lw.ir.size)].sum()), lw.consts.size)
-        c = eng.add_stage(lw.ir, lw.consts, lw.var_keys)
-        if key in seen:
-            continue
-        seen.add(key)
-        picked.append((st, c))
-    gpu = [(st, c) for st, c in picked if c.status == STAGE_OK]
-    return owner, gpu[:limit]
+    for i in range(nat.n_stages):
+        ir, cs, _vk = nat.stage_program(i, seed)
+        key = hashlib.sha256(ir.tobytes() + b"|" + cs.tobytes()).digest()
+        if key not in seen:
+            seen.add(key)
+            picked.append(i)
+    return picked
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["llama3-8b-tp4pp2dp2-sp", "deepseek-v3-tp4pp4dp2-ep"])
+@pytest.mark.parametrize("name", ["llama3-8b-tp4pp2dp2-sp", "llama3-405b-tp8pp16dp2",
+                                  "deepseek-v3-tp4pp4dp2-ep"])
 def test_full_size_workload_matches_oracle(gpu, name):
+    """configs[1], configs[3] (the metric's own config) and configs[4] at full
+    size: EVERY distinct GPU stage program -- engine witness outcomes (valid,
+    failing, first failing witness/obligation) equal the CPU oracle's."""
+    from paper_2506_15961_b200.native import NativePlan
     seed = 13
     _desc, plan = get_workload(name)
-    stages, _ = build_stages(plan)
+    nat = NativePlan(plan)
+    assert nat.validate() and nat.build_stages()
+    picked = distinct_programs(nat, seed)
     eng = Engine(0, seed, F.fn_keys(seed))
-    owner, picked = _distinct_gpu_stages(plan, stages, eng, seed, limit=10)
-    assert picked, "no GPU stage"
+    idx = nat.add_stages(eng, seed, picked)
+    gpu_stages = [(i, int(k)) for i, k in zip(picked, idx) if k >= 0 and
+                  eng.stage_status(int(k)).status == STAGE_OK]
+    assert gpu_stages, "no GPU stage"
     eng.upload()
     eng.launch(W - 7)
     fb, nv, nb = eng.results()
     wit = np.arange(W - 7, dtype=np.uint64)
-    for st, c in picked:
+    owner = shard_owner(plan, entry_order(plan))
+    for i, k in gpu_stages:
+        st = nat.stage(i)
         o = check_stage(plan, st, owner, seed, wit)
-        assert (int(nv[c.index]), int(nb[c.index])) == (o.valid, o.bad), st.target
+        assert (int(nv[k]), int(nb[k])) == (o.valid, o.bad), st.target
         if o.first_bad is None:
-            assert int(fb[c.index]) == 0xFFFFFFFFFFFFFFFF, st.target
+            assert int(fb[k]) == 0xFFFFFFFFFFFFFFFF, st.target
         else:
             w, obl = o.first_bad
-            assert int(fb[c.index]) == (w << 32) | obl, st.target
+            assert int(fb[k]) == (w << 32) | obl, st.target
     eng.close()
+    nat.close()
+
+
+@pytest.mark.parametrize("name", ["llama3-405b-tp8pp16dp2"])
+def test_full_size_programs_are_deduplicated_exactly(lib, name):
+    """CPU: the distinct-program count that the GPU test covers (no sampling:
+    every stage's program text is hashed)."""
+    from paper_2506_15961_b200.native import NativePlan
+    _desc, plan = get_workload(name)
+    nat = NativePlan(plan)
+    assert nat.validate() and nat.build_stages()
+    picked = distinct_programs(nat, 13)
+    assert 1 < len(picked) < nat.n_stages
+    nat.close()
 
 
 @pytest.mark.gpu
