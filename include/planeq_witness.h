@@ -52,6 +52,8 @@ extern "C" {
 #define PQW_STAGE_LOG_DIV0 4      /* logical side divides by a constant zero       */
 #define PQW_STAGE_BAD_INDEX 5     /* embedding id outside its table                 */
 #define PQW_STAGE_PENDING 6       /* pqw_stage_add: not compiled yet (pqw_stage_status) */
+#define PQW_STAGE_LOSSY 7         /* an exact constant is a nonzero multiple of p: the
+                                     field image loses it, the stage stays undecided */
 
 /* tensor-op program opcodes (pqw_stage_add ir stream) */
 enum pqw_top {
@@ -204,6 +206,29 @@ int pqw_results(pqw_engine* e, uint64_t* first_bad, uint32_t* n_valid,
  */
 int pqw_probe(pqw_engine* e, int stage, uint32_t witness, uint32_t obl,
               uint32_t* lhs, uint32_t* rhs, uint32_t* var_vals, size_t n_vars);
+
+/*
+ * Confirm a refutation on the host the way the reference does before it
+ * reports one (pkg/src/planeq/stages.py:221-264 _confirm). Re-runs the
+ * stage's front end, then:
+ *  1. out[0] = the first residual obligation whose cone holds no uninterpreted
+ *     function (EXP/RSQRT/SIGMOID or a constant folded from one) and whose
+ *     sides differ in F_p at `witness` (all definedness conditions holding
+ *     there): an exact rational counterexample, no replay needed; -1: none.
+ *  2. Otherwise the real-valued replay: for each of the n_env variable
+ *     assignments (env_vals: n_env rows of the stage's variables, in order),
+ *     every definedness condition must hold (|v| > 1e-12, v > 1e-12 where the
+ *     reference requires positivity), then each residual obligation with an
+ *     uninterpreted function in its cone is evaluated in double precision
+ *     with the genuine exp, 1/sqrt and logistic functions (a failed
+ *     evaluation skips the obligation, as a raised exception does there);
+ *     out[1] = the first environment in which some obligation's sides differ
+ *     by more than tol, out[2] = that obligation, sides[0..1] = its sides
+ *     (out[1] = out[2] = -1: not confirmed).
+ * out[3] = residual obligations with an uninterpreted function in their cone.
+ */
+int pqw_confirm(pqw_engine* e, int stage, uint32_t witness, const double* env_vals,
+                size_t n_env, double tol, int64_t out[4], double sides[2]);
 
 /* Device time of the last launch in milliseconds (CUDA events on the launch stream). */
 int pqw_last_launch_ms(pqw_engine* e, float* ms);

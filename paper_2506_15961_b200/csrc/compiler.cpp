@@ -15,6 +15,7 @@
 #include "compiler.hpp"
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -34,7 +35,10 @@ constexpr size_t CHUNK = 16;  // max operands of one n-ary sum / dot before chun
 
 enum VKind : uint8_t { K_CONST = 0, K_VAR = 1, K_OP = 2 };
 enum VOp : uint8_t { O_NONE = 0, O_ADD, O_SUB, O_MUL, O_NEG, O_DIV, O_HASH, O_SUMN, O_DOT, O_INV };
-enum : uint8_t { F_DEN = 1, F_INT = 2 };
+// F_UF: an uninterpreted function (or a constant folded from one) is in the
+// value's cone (the reference's Expr.has_uf); F_POS: a definedness condition
+// that also requires positivity (require_positive)
+enum : uint8_t { F_DEN = 1, F_INT = 2, F_UF = 4, F_POS = 8 };
 enum Fn : uint32_t { FN_EXP = 0, FN_RSQRT = 1, FN_SIGMOID = 2 };
 
 struct Val {
@@ -100,44 +104,73 @@ static uint32_t residue_of(int64_t num, int64_t den) {
   return fmul((uint32_t)n, finv((uint32_t)d));
 }
 
+// Constants are interned by their exact rational when the compiler knows it,
+// else by residue: two distinct rationals congruent mod p never share a value
+// id (so no obligation between them closes at compile time).
+struct ConstKey {
+  uint8_t exact;
+  int64_t a, b;  // (num, den) or (residue, 0)
+  bool operator==(const ConstKey& o) const { return exact == o.exact && a == o.a && b == o.b; }
+};
+struct ConstKeyHash {
+  size_t operator()(const ConstKey& k) const {
+    return (size_t)mix64((uint64_t)k.a * 0x9E3779B97F4A7C15ull ^ (uint64_t)k.b ^ ((uint64_t)k.exact << 62));
+  }
+};
+
+double real_fn(uint32_t fn, double x) {
+  if (fn == 0) return std::exp(x);                                  // EXP
+  if (fn == 1) return x > 0 ? 1.0 / std::sqrt(x) : std::nan("");   // RSQRT
+  return 1.0 / (1.0 + std::exp(-x));                                // SIGMOID
+}
+
 struct Builder {
   std::vector<Val> vals;
   std::vector<Exact> exact;  // per value, meaningful for consts
+  std::vector<double> realc; // per value: the real value of a constant (replay)
   std::vector<uint32_t> pool;
   std::unordered_map<uint64_t, uint32_t> head;
   std::vector<uint32_t> chain;
-  std::unordered_map<uint32_t, uint32_t> const_ids;
+  std::unordered_map<ConstKey, uint32_t, ConstKeyHash> const_ids;
+  bool lossy = false;        // an exact constant vanishes mod p (nonzero multiple of p)
   std::vector<uint32_t> dens;  // definedness conditions, creation order
   const uint64_t* fn_keys = nullptr;
   int side = 0;
   uint32_t zero_id = NONE, one_id = NONE;
 
-  uint32_t push(const Val& v, const Exact& ex) {
+  uint32_t push(const Val& v, const Exact& ex, double real = 0.0) {
     vals.push_back(v);
     exact.push_back(ex);
+    realc.push_back(real);
     chain.push_back(NONE);
     return (uint32_t)(vals.size() - 1);
   }
 
   // -- constants ---------------------------------------------------------
-  uint32_t cst(uint32_t r, Exact ex, bool is_int = false) {
-    auto it = const_ids.find(r);
+  // r: residue; ex: exact value when known; real: its real value (for the
+  // real-valued replay); uf: folded from an uninterpreted function
+  uint32_t cst(uint32_t r, Exact ex, double real, bool uf = false, bool is_int = false) {
+    const ConstKey key = ex.ok ? ConstKey{1, ex.num, ex.den} : ConstKey{0, (int64_t)r, 0};
+    auto it = const_ids.find(key);
     if (it != const_ids.end()) {
       if (is_int) vals[it->second].flags |= F_INT;
+      if (uf) vals[it->second].flags |= F_UF;
       return it->second;
     }
+    if (ex.ok && ex.num != 0 && ex.num % (int64_t)P == 0) lossy = true;
     Val v{};
     v.kind = K_CONST;
     v.aux = r;
-    v.flags = is_int ? F_INT : 0;
-    uint32_t id = push(v, ex);
-    const_ids.emplace(r, id);
+    v.flags = (uint8_t)((is_int ? F_INT : 0) | (uf ? F_UF : 0));
+    uint32_t id = push(v, ex, ex.ok ? (double)ex.num / (double)ex.den : real);
+    const_ids.emplace(key, id);
     return id;
   }
   uint32_t cst_int(int64_t n, bool is_int = false) {
-    return cst(residue_of(n, 1), Exact{true, n, 1}, is_int);
+    return cst(residue_of(n, 1), Exact{true, n, 1}, (double)n, false, is_int);
   }
-  uint32_t cst_exact(const Exact& ex, uint32_t r) { return cst(r, ex); }
+  bool ufc(uint32_t x) const { return (vals[x].flags & F_UF) != 0; }
+  uint32_t cst_exact(const Exact& ex, uint32_t r, double real) { return cst(r, ex, real); }
   bool is_const(uint32_t id) const { return vals[id].kind == K_CONST; }
   uint32_t res(uint32_t id) const { return (uint32_t)vals[id].aux; }
   uint32_t zero() { return zero_id == NONE ? (zero_id = cst_int(0)) : zero_id; }
@@ -189,6 +222,13 @@ struct Builder {
     v.aux = aux;
     v.dnum = dnum;
     v.dden = dden;
+    bool uf = op == O_HASH;
+    if (list) {
+      for (uint32_t i = 0; i < n && !uf; ++i) uf = ufc(list[i]);
+    } else {
+      uf = uf || ufc(a) || (op != O_NEG && op != O_INV && op != O_HASH && ufc(b));
+    }
+    v.flags = uf ? F_UF : 0;
     if (list) {
       v.a = (uint32_t)pool.size();
       v.b = n;
@@ -229,7 +269,7 @@ struct Builder {
                                       (__int128)exact[y].num * exact[x].den,
                                   (__int128)exact[x].den * exact[y].den)
                      : Exact{false, 0, 0};
-      return cst(fadd(res(x), res(y)), ex);
+      return cst(fadd(res(x), res(y)), ex, realc[x] + realc[y], ufc(x) || ufc(y));
     }
     if (x > y) std::swap(x, y);
     uint32_t n, d;
@@ -245,7 +285,7 @@ struct Builder {
                                       (__int128)exact[y].num * exact[x].den,
                                   (__int128)exact[x].den * exact[y].den)
                      : Exact{false, 0, 0};
-      return cst(fsub(res(x), res(y)), ex);
+      return cst(fsub(res(x), res(y)), ex, realc[x] - realc[y], ufc(x) || ufc(y));
     }
     uint32_t n, d;
     deg_add(x, y, n, d);
@@ -254,7 +294,7 @@ struct Builder {
   uint32_t neg(uint32_t x) {
     if (is_const(x)) {
       Exact ex = exact[x].ok ? Exact{true, -exact[x].num, exact[x].den} : Exact{false, 0, 0};
-      return cst(fneg(res(x)), ex);
+      return cst(fneg(res(x)), ex, -realc[x], ufc(x));
     }
     return intern(O_NEG, x, 0, 0, nullptr, 0, vals[x].dnum, vals[x].dden);
   }
@@ -268,14 +308,14 @@ struct Builder {
                      ? make_exact((__int128)exact[x].num * exact[y].num,
                                   (__int128)exact[x].den * exact[y].den)
                      : Exact{false, 0, 0};
-      return cst(fmul(res(x), res(y)), ex);
+      return cst(fmul(res(x), res(y)), ex, realc[x] * realc[y], ufc(x) || ufc(y));
     }
     if (x > y) std::swap(x, y);
     return intern(O_MUL, x, y, 0, nullptr, 0, sat_add(vals[x].dnum, vals[y].dnum),
                   sat_add(vals[x].dden, vals[y].dden));
   }
-  uint32_t scale_exact(uint32_t x, const Exact& ex, uint32_t r) {
-    return mul(x, cst_exact(ex, r));
+  uint32_t scale_exact(uint32_t x, const Exact& ex, uint32_t r, double real) {
+    return mul(x, cst_exact(ex, r, real));
   }
 
   // require_nonzero (reference sym.py:379-387): constants are decided now,
@@ -291,6 +331,7 @@ struct Builder {
       vals[e].flags |= F_DEN;
       dens.push_back(e);
     }
+    if (positive) vals[e].flags |= F_POS;
   }
   uint32_t div(uint32_t x, uint32_t y) {
     // caller has already called require(y, ...)
@@ -299,7 +340,7 @@ struct Builder {
       Exact ex = exact[y].ok && exact[y].num != 0
                      ? make_exact((__int128)exact[y].den, (__int128)exact[y].num)
                      : Exact{false, 0, 0};
-      return mul(x, cst(inv, ex));
+      return mul(x, cst(inv, ex, 1.0 / realc[y], ufc(y)));
     }
     if (is_const(x) && res(x) == 0) return zero();
     // x / y = x * y^-1 with the inverse value-numbered: rows that share a
@@ -308,7 +349,8 @@ struct Builder {
     return mul(x, iv);
   }
   uint32_t hash(uint32_t fn, uint32_t x) {
-    if (is_const(x)) return cst(uf_apply(fn_keys[fn], res(x)), Exact{false, 0, 0});
+    if (is_const(x))
+      return cst(uf_apply(fn_keys[fn], res(x)), Exact{false, 0, 0}, real_fn(fn, realc[x]), true);
     return intern(O_HASH, x, 0, fn, nullptr, 0, 1, 0);
   }
   uint32_t sumn(std::vector<uint32_t> xs) {
@@ -474,7 +516,7 @@ struct Compiler {
     if (ci < 0 || (size_t)ci >= n_consts) bad("const index out of range");
     const int64_t* c = consts + 3 * ci;
     Exact ex = c[2] != 0 ? Exact{true, c[1], c[2]} : Exact{false, 0, 0};
-    return B.cst((uint32_t)c[0], ex);
+    return B.cst((uint32_t)c[0], ex, std::nan(""));
   }
   void record(uint32_t obl, uint32_t l, uint32_t r) {
     if (obl >= obls.size()) bad("obligation id out of range");
@@ -769,7 +811,7 @@ void Compiler::run_op(int32_t op, const int32_t* ins, int n_in, const int32_t* o
         uint32_t s = B.sumn(acc[o]);
         if (op == PQW_T_MEAN) {
           need(count >= 1, "mean of nothing");
-          s = B.mul(s, B.cst(finv(residue_of(count, 1)), make_exact(1, count)));
+          s = B.mul(s, B.cst(finv(residue_of(count, 1)), make_exact(1, count), 1.0 / (double)count));
         }
         v[o] = s;
       }
@@ -1091,21 +1133,14 @@ struct Emitter {
 
 }  // namespace
 
-CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* consts,
-                            size_t n_consts, uint32_t n_vars, uint32_t var_base,
-                            const uint64_t fn_keys[3], uint32_t smem_slots,
-                            uint32_t n_warps, const SchedOptions& sched) {
-  CompiledStage st;
-  st.n_vars = n_vars;
-  st.n_warps = n_warps;
-  if (n_warps < 1 || n_warps > 32) bad("n_warps must be in [1, 32]");
-  st.var_base = var_base;
-  Compiler C;
+// Parse a tensor-op program and run it through the front end (symbolic
+// execution into the value graph). Throws Div0 / BadIndex / runtime_error.
+static void run_front(Compiler& C, const int32_t* ir, size_t ir_len, const int64_t* consts,
+                      size_t n_consts, uint32_t n_vars, const uint64_t fn_keys[3]) {
   C.B.fn_keys = fn_keys;
   C.consts = consts;
   C.n_consts = n_consts;
   C.n_vars = n_vars;
-
   size_t p = 0;
   auto rd = [&]() -> int32_t {
     if (p >= ir_len) bad("truncated program");
@@ -1128,16 +1163,31 @@ CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* con
   }
   C.obls.resize(n_obl);
   C.obl_set.assign(n_obl, 0);
+  for (int32_t o = 0; o < n_ops; ++o) {
+    int32_t op = rd(), ni = rd(), no = rd(), na = rd();
+    if (ni < 0 || no < 0 || na < 0 || p + ni + no + na > ir_len) bad("bad op header");
+    const int32_t* ins = ir + p;
+    const int32_t* outs = ins + ni;
+    const int32_t* at = outs + no;
+    p += ni + no + na;
+    C.run_op(op, ins, ni, outs, no, at, na);
+  }
+  for (int32_t o = 0; o < n_obl; ++o)
+    if (!C.obl_set[o]) bad("obligation never checked");
+}
+
+CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* consts,
+                            size_t n_consts, uint32_t n_vars, uint32_t var_base,
+                            const uint64_t fn_keys[3], uint32_t smem_slots,
+                            uint32_t n_warps, const SchedOptions& sched) {
+  CompiledStage st;
+  st.n_vars = n_vars;
+  st.n_warps = n_warps;
+  if (n_warps < 1 || n_warps > 32) bad("n_warps must be in [1, 32]");
+  st.var_base = var_base;
+  Compiler C;
   try {
-    for (int32_t o = 0; o < n_ops; ++o) {
-      int32_t op = rd(), ni = rd(), no = rd(), na = rd();
-      if (ni < 0 || no < 0 || na < 0 || p + ni + no + na > ir_len) bad("bad op header");
-      const int32_t* ins = ir + p;
-      const int32_t* outs = ins + ni;
-      const int32_t* at = outs + no;
-      p += ni + no + na;
-      C.run_op(op, ins, ni, outs, no, at, na);
-    }
+    run_front(C, ir, ir_len, consts, n_consts, n_vars, fn_keys);
   } catch (const Div0& d) {
     st.status = d.side ? PQW_STAGE_PAR_DIV0 : PQW_STAGE_LOG_DIV0;
     return st;
@@ -1145,8 +1195,8 @@ CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* con
     st.status = PQW_STAGE_BAD_INDEX;
     return st;
   }
-  for (int32_t o = 0; o < n_obl; ++o)
-    if (!C.obl_set[o]) bad("obligation never checked");
+  const int32_t n_obl = (int32_t)C.obls.size();
+
   st.n_obligations = n_obl;
 
   // classify obligations: fast (same value), constant mismatch, residual
@@ -1177,6 +1227,11 @@ CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* con
     st.const_rhs = B.res(r);
     st.exact_lhs = (B.exact[l].ok && B.exact[l].den == 1) ? B.exact[l].num : INT64_MIN;
     st.exact_rhs = (B.exact[r].ok && B.exact[r].den == 1) ? B.exact[r].num : INT64_MIN;
+    return st;
+  }
+  if (B.lossy) {
+    // an exact constant vanishes mod p: evaluation in F_p cannot decide the stage
+    st.status = PQW_STAGE_LOSSY;
     return st;
   }
   // the degree bound of the stage: numerator degree of lhs - rhs
@@ -1297,6 +1352,163 @@ std::vector<uint32_t> obligation_support(const CompiledStage& st, uint32_t obl) 
   std::sort(vars.begin(), vars.end());
   vars.erase(std::unique(vars.begin(), vars.end()), vars.end());
   return vars;
+}
+
+namespace {
+
+// Residual obligations of a front end (deduplicated (lhs, rhs) pairs in
+// obligation order: the reference's residual dict, stages.py:341-351).
+std::vector<uint32_t> residual_of(const Compiler& C) {
+  std::vector<uint32_t> out;
+  std::unordered_set<uint64_t> seen;
+  for (size_t o = 0; o < C.obls.size(); ++o) {
+    const uint32_t l = C.obls[o].l, r = C.obls[o].r;
+    if (l == r) continue;
+    if (seen.insert(((uint64_t)l << 32) | r).second) out.push_back((uint32_t)o);
+  }
+  return out;
+}
+
+// Evaluate every value of the graph in F_p (vars from their witness values).
+std::vector<uint32_t> eval_field(const Builder& B, const uint64_t* var_keys, uint32_t w) {
+  std::vector<uint32_t> v(B.vals.size(), 0);
+  for (size_t i = 0; i < B.vals.size(); ++i) {
+    const Val& x = B.vals[i];
+    if (x.kind == K_CONST) {
+      v[i] = (uint32_t)x.aux;
+      continue;
+    }
+    if (x.kind == K_VAR) {
+      v[i] = witness_value(var_keys[x.aux], w);
+      continue;
+    }
+    switch (x.op) {
+      case O_ADD: v[i] = fadd(v[x.a], v[x.b]); break;
+      case O_SUB: v[i] = fsub(v[x.a], v[x.b]); break;
+      case O_MUL: v[i] = fmul(v[x.a], v[x.b]); break;
+      case O_NEG: v[i] = fneg(v[x.a]); break;
+      case O_INV: v[i] = v[x.a] ? finv(v[x.a]) : 0u; break;
+      case O_HASH: v[i] = uf_apply(B.fn_keys[x.aux], v[x.a]); break;
+      case O_SUMN: {
+        uint32_t acc = 0;
+        for (uint32_t k = 0; k < x.b; ++k) acc = fadd(acc, v[B.pool[x.a + k]]);
+        v[i] = acc;
+        break;
+      }
+      case O_DOT: {
+        uint32_t acc = 0;
+        for (uint32_t k = 0; k + 1 < x.b; k += 2)
+          acc = fadd(acc, fmul(v[B.pool[x.a + k]], v[B.pool[x.a + k + 1]]));
+        v[i] = acc;
+        break;
+      }
+      default: bad("internal: bad value op");
+    }
+  }
+  return v;
+}
+
+// Evaluate every value in double precision with the genuine functions; a
+// failed evaluation (1/0, rsqrt of a non-positive value, overflow) is NaN.
+std::vector<double> eval_real(const Builder& B, const double* vars) {
+  std::vector<double> v(B.vals.size(), 0.0);
+  for (size_t i = 0; i < B.vals.size(); ++i) {
+    const Val& x = B.vals[i];
+    double r;
+    if (x.kind == K_CONST) {
+      r = B.realc[i];
+    } else if (x.kind == K_VAR) {
+      r = vars[x.aux];
+    } else {
+      switch (x.op) {
+        case O_ADD: r = v[x.a] + v[x.b]; break;
+        case O_SUB: r = v[x.a] - v[x.b]; break;
+        case O_MUL: r = v[x.a] * v[x.b]; break;
+        case O_NEG: r = -v[x.a]; break;
+        case O_INV: r = v[x.a] != 0.0 ? 1.0 / v[x.a] : std::nan(""); break;
+        case O_HASH: r = real_fn((uint32_t)x.aux, v[x.a]); break;
+        case O_SUMN: {
+          r = 0.0;
+          for (uint32_t k = 0; k < x.b; ++k) r += v[B.pool[x.a + k]];
+          break;
+        }
+        case O_DOT: {
+          r = 0.0;
+          for (uint32_t k = 0; k + 1 < x.b; k += 2) r += v[B.pool[x.a + k]] * v[B.pool[x.a + k + 1]];
+          break;
+        }
+        default: bad("internal: bad value op");
+      }
+    }
+    v[i] = std::isfinite(r) ? r : std::nan("");
+  }
+  return v;
+}
+
+}  // namespace
+
+int confirm_stage(const int32_t* ir, size_t ir_len, const int64_t* consts, size_t n_consts,
+                  uint32_t n_vars, const uint64_t fn_keys[3], const uint64_t* var_keys,
+                  uint32_t witness, const double* env_vals, size_t n_env, double tol,
+                  int64_t out[4], double sides[2]) {
+  out[0] = out[1] = out[2] = -1;
+  out[3] = 0;
+  sides[0] = sides[1] = 0.0;
+  Compiler C;
+  try {
+    run_front(C, ir, ir_len, consts, n_consts, n_vars, fn_keys);
+  } catch (const Div0&) {
+    return -1;
+  } catch (const BadIndex&) {
+    return -1;
+  }
+  const Builder& B = C.B;
+  const auto res = residual_of(C);
+  std::vector<uint32_t> uf;
+  for (uint32_t o : res)
+    if (B.ufc(C.obls[o].l) || B.ufc(C.obls[o].r)) uf.push_back(o);
+  out[3] = (int64_t)uf.size();
+  // 1. an obligation free of uninterpreted functions that fails in F_p at the
+  //    witness: an exact rational counterexample (no replay needed)
+  {
+    const auto v = eval_field(B, var_keys, witness);
+    bool valid = true;
+    for (uint32_t d : B.dens) valid = valid && v[d] != 0;
+    if (valid)
+      for (uint32_t o : res) {
+        const uint32_t l = C.obls[o].l, r = C.obls[o].r;
+        if (!B.ufc(l) && !B.ufc(r) && v[l] != v[r]) {
+          out[0] = o;
+          return 0;
+        }
+      }
+  }
+  // 2. the reference's replay with the genuine functions (stages.py:241-264)
+  for (size_t k = 0; k < n_env; ++k) {
+    const auto v = eval_real(B, env_vals + k * (size_t)n_vars);
+    bool hold = true;
+    for (uint32_t d : B.dens) {
+      const double x = v[d];
+      const bool pos = (B.vals[d].flags & F_POS) != 0;
+      if (std::isnan(x) || (pos ? x <= 1e-12 : std::fabs(x) <= 1e-12)) {
+        hold = false;
+        break;
+      }
+    }
+    if (!hold) continue;
+    for (uint32_t o : uf) {
+      const double l = v[C.obls[o].l], r = v[C.obls[o].r];
+      if (std::isnan(l) || std::isnan(r)) continue;
+      if (std::fabs(l - r) > tol) {
+        out[1] = (int64_t)k;
+        out[2] = o;
+        sides[0] = l;
+        sides[1] = r;
+        return 0;
+      }
+    }
+  }
+  return 0;
 }
 
 }  // namespace pqw

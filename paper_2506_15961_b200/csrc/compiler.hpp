@@ -53,6 +53,13 @@ CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* con
 constexpr uint32_t DEFAULT_FAST_SLOTS = 1680;
 constexpr uint32_t DEFAULT_WARPS = 16;
 
+// Host confirmation of a refutation (pqw_confirm in include/planeq_witness.h):
+// re-runs the front end; returns -1 when the program has no value graph.
+int confirm_stage(const int32_t* ir, size_t ir_len, const int64_t* consts, size_t n_consts,
+                  uint32_t n_vars, const uint64_t fn_keys[3], const uint64_t* var_keys,
+                  uint32_t witness, const double* env_vals, size_t n_env, double tol,
+                  int64_t out[4], double sides[2]);
+
 // Run the back end of a stage compiled with status OK (idempotent).
 void finalize_stage(CompiledStage& st);
 

@@ -750,6 +750,31 @@ int pqw_probe(pqw_engine* e, int stage, uint32_t witness, uint32_t obl, uint32_t
   return PQW_OK;
 }
 
+int pqw_confirm(pqw_engine* e, int stage, uint32_t witness, const double* env_vals, size_t n_env,
+                double tol, int64_t out[4], double sides[2]) {
+  if (!e || !out || !sides || (n_env && !env_vals)) return fail(PQW_EINVAL, "null argument");
+  if (stage < 0 || (size_t)stage >= e->stages.size()) return fail(PQW_EINVAL, "bad stage");
+  {
+    int rc = finalize_front(e);
+    if (rc != PQW_OK) return rc;
+  }
+  const size_t root = e->alias[stage] < 0 ? (size_t)stage : (size_t)e->alias[stage];
+  auto it = e->cache_src.find(root);
+  if (it == e->cache_src.end()) return fail(PQW_ESTATE, "stage program not retained");
+  const auto& src = it->second;
+  const uint32_t base = e->pend_base[stage], nv = e->pend_nvars[stage];
+  try {
+    int rc = pqw::confirm_stage(src.first.data(), src.first.size(), src.second.data(),
+                                src.second.size() / 3, nv, e->fn_keys,
+                                e->var_keys.data() + base, witness, env_vals, n_env, tol, out,
+                                sides);
+    if (rc < 0) return fail(PQW_ESTATE, "stage has no value graph");
+  } catch (const std::exception& ex) {
+    return fail(PQW_EINVAL, std::string("confirm: ") + ex.what());
+  }
+  return PQW_OK;
+}
+
 int pqw_last_launch_ms(pqw_engine* e, float* ms) {
   if (!e || !ms) return fail(PQW_EINVAL, "null argument");
   if (!e->timed) {

@@ -28,6 +28,7 @@ STAGE_PAR_DIV0 = 3
 STAGE_LOG_DIV0 = 4
 STAGE_BAD_INDEX = 5
 STAGE_PENDING = 6
+STAGE_LOSSY = 7
 
 # bytecode opcodes (pqw_bop)
 BOP_NAMES = ("END", "DOT", "SUM", "SUB", "NEG", "HASH", "INV", "VAR", "CONST", "CHK", "DEN",
@@ -40,7 +41,7 @@ EXPORTS = ("pqw_abi_version", "pqw_last_error", "pqw_device_count", "pqw_engine_
            "pqw_engine_destroy", "pqw_stage_add", "pqw_stage_status", "pqw_reset", "pqw_stage_bytecode",
            "pqw_obligation_support", "pqw_upload", "pqw_launch", "pqw_results", "pqw_probe",
            "pqw_last_launch_ms", "pqw_image_stats", "pqw_peak_fieldops", "pqw_stage_select",
-           "pqw_stage_cost",
+           "pqw_stage_cost", "pqw_confirm",
            # native plan core (native.py)
            "pqw_plan_create", "pqw_plan_destroy", "pqw_plan_validate", "pqw_plan_build_stages",
            "pqw_plan_stage_target", "pqw_plan_stage_nodes", "pqw_plan_uncovered",
@@ -106,6 +107,9 @@ def load_library(path: str | None = None):
     lib.pqw_stage_select.restype = C.c_int
     lib.pqw_stage_cost.argtypes = [C.c_void_p, C.c_int]
     lib.pqw_stage_cost.restype = C.c_int64
+    lib.pqw_confirm.argtypes = [C.c_void_p, C.c_int, C.c_uint32, C.POINTER(C.c_double),
+                                C.c_size_t, C.c_double, i64p, C.POINTER(C.c_double)]
+    lib.pqw_confirm.restype = C.c_int
     lib.pqw_peak_fieldops.argtypes = [C.c_int, C.POINTER(C.c_double)]
     lib.pqw_peak_fieldops.restype = C.c_int
     if lib.pqw_abi_version() != ABI_VERSION:
@@ -293,6 +297,17 @@ class Engine:
         self._check(self.lib.pqw_probe(self._h, stage, witness, obl, C.byref(lhs), C.byref(rhs),
                                        _ptr(vals, C.c_uint32), max(n_vars, 1)))
         return int(lhs.value), int(rhs.value), vals[:n_vars]
+
+    def confirm(self, stage: int, witness: int, envs: np.ndarray, tol: float = 1e-6):
+        """Host confirmation of a refutation (pqw_confirm): (exact obligation or
+        -1, env index or -1, replay obligation or -1, lhs, rhs, #uf obligations)."""
+        envs = np.ascontiguousarray(envs, dtype=np.float64)
+        out = np.zeros(4, dtype=np.int64)
+        sides = np.zeros(2, dtype=np.float64)
+        n_env = envs.shape[0] if envs.ndim == 2 else 0
+        self._check(self.lib.pqw_confirm(self._h, stage, witness, _ptr(envs, C.c_double), n_env,
+                                         tol, _ptr(out, C.c_int64), _ptr(sides, C.c_double)))
+        return int(out[0]), int(out[1]), int(out[2]), float(sides[0]), float(sides[1]), int(out[3])
 
     def last_launch_ms(self) -> float:
         ms = C.c_float()

@@ -30,6 +30,7 @@ distinct rational constants):
 from __future__ import annotations
 
 import ctypes as C
+import os
 from collections import defaultdict
 from fractions import Fraction
 from itertools import chain
@@ -161,24 +162,34 @@ def _joined(names) -> bytes:
     return ("\0".join(names) + "\0").encode()
 
 
-def _pack_graph(g: Graph, consts: _Consts, keep: list) -> _GraphDesc:
-    tv = list(g.tensors.values())
+def _zjoin(names, n: int) -> bytes:
+    """n names, each NUL-terminated (empty for n == 0, so slices concatenate)."""
+    return _joined(names) if n else b""
+
+
+_CONST_KINDS = (OPCODE["scale"], OPCODE["shift"], OPCODE["full"])
+
+
+def _pack_tensors(tv: list) -> dict:
     nt = len(tv)
     shapes = list(map(attrgetter("shape"), tv))
-    ndim = np.fromiter(map(len, shapes), np.int32, nt)
-    dims = np.fromiter(chain.from_iterable(shapes), np.int64)
-    flags = np.zeros(max(nt, 1), np.uint8)
+    flags = np.zeros(nt, np.uint8)
     is_int = np.fromiter(map("int".__eq__, map(attrgetter("dtype"), tv)), np.bool_, nt)
     for i in np.flatnonzero(is_int).tolist():
         flags[i] = 1 | (2 if tv[i].meta.get("enum") == "position" else 0)
-    nodes = g.nodes
+    return dict(ndim=np.fromiter(map(len, shapes), np.int32, nt),
+                dims=np.fromiter(chain.from_iterable(shapes), np.int64), flags=flags,
+                tn=_zjoin(map(attrgetter("id"), tv), nt))
+
+
+def _pack_nodes(nodes: list) -> dict:
+    """Columns of a node slice; rational attributes get slice-local constant ids
+    (the "consts" list of (num, den) keys), remapped to plan ids by the caller."""
     nn = len(nodes)
+    consts = _Consts()
     kinds = list(map(attrgetter("kind"), nodes))
-    kind = np.fromiter(map(_KIND.__getitem__, kinds), np.int32, nn)
     ins = list(map(attrgetter("inputs"), nodes))
     outs = list(map(attrgetter("outputs"), nodes))
-    nin = np.fromiter(map(len, ins), np.int32, nn)
-    nout = np.fromiter(map(len, outs), np.int32, nn)
     nattr = [0] * nn
     words: list[int] = []
     attrs = list(map(attrgetter("attrs"), nodes))
@@ -188,23 +199,114 @@ def _pack_graph(g: Graph, consts: _Consts, keep: list) -> _GraphDesc:
             nattr[i] = len(w)
             words.extend(w)
     devs = list(map(attrgetter("device"), nodes))
-    device = np.fromiter(map(_NONE_TO_M1.get, devs, devs), np.int32, nn)
-    seq = np.fromiter(map(attrgetter("seq"), nodes), np.int64, nn)
-    arrs = dict(ndim=ndim, dims=dims if dims.size else np.zeros(1, np.int64), flags=flags,
-                kind=kind, nin=nin, nout=nout, nattr=np.array(nattr, dtype=np.int32),
-                attrs=np.array(words or [0], dtype=np.int64), device=device, seq=seq)
-    strs = dict(tn=_joined(g.tensors), ids=_joined(map(attrgetter("id"), nodes)),
-                ins=_joined(chain.from_iterable(ins)), outs=_joined(chain.from_iterable(outs)),
+    nin = np.fromiter(map(len, ins), np.int32, nn)
+    nout = np.fromiter(map(len, outs), np.int32, nn)
+    return dict(kind=np.fromiter(map(_KIND.__getitem__, kinds), np.int32, nn), nin=nin,
+                nout=nout, nattr=np.array(nattr, dtype=np.int32),
+                attrs=np.array(words, dtype=np.int64),
+                device=np.fromiter(map(_NONE_TO_M1.get, devs, devs), np.int32, nn),
+                seq=np.fromiter(map(attrgetter("seq"), nodes), np.int64, nn),
+                ids=_zjoin(map(attrgetter("id"), nodes), nn),
+                ins=_zjoin(chain.from_iterable(ins), int(nin.sum())),
+                outs=_zjoin(chain.from_iterable(outs), int(nout.sum())),
+                consts=list(consts.idx))
+
+
+PARALLEL_PACK_MIN = 150_000  # nodes; smaller graphs pack in-process
+
+
+def _workers() -> int:
+    try:
+        n = len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        n = os.cpu_count() or 1
+    return max(1, min(16, n))
+
+
+def _forked(jobs: list) -> list:
+    """Run zero-argument callables in forked children (they inherit the plan
+    copy-on-write) and return their pickled results in order. Used for the
+    per-node Python work of packing a large plan; children touch no CUDA."""
+    import pickle
+    procs = []
+    for fn in jobs:
+        r, w = os.pipe()
+        pid = os.fork()
+        if pid == 0:  # child
+            os.close(r)
+            try:
+                out = pickle.dumps(("ok", fn()), protocol=pickle.HIGHEST_PROTOCOL)
+            except BaseException as e:  # noqa: BLE001 - reported to the parent
+                out = pickle.dumps(("err", f"{type(e).__name__}: {e}"))
+            with os.fdopen(w, "wb") as f:
+                f.write(out)
+            os._exit(0)
+        os.close(w)
+        procs.append((pid, r))
+    results = []
+    for pid, r in procs:
+        with os.fdopen(r, "rb") as f:
+            data = f.read()
+        os.waitpid(pid, 0)
+        results.append(pickle.loads(data) if data else ("err", "packer child died"))
+    return results
+
+
+def _pack_graph(g: Graph, consts: _Consts, keep: list) -> _GraphDesc:
+    tv = list(g.tensors.values())
+    nodes = g.nodes
+    nt, nn = len(tv), len(nodes)
+    k = _workers() if nn >= PARALLEL_PACK_MIN else 1
+    if k > 1:
+        import gc
+        bt = [(i * nt) // k for i in range(k + 1)]
+        bn = [(i * nn) // k for i in range(k + 1)]
+        gc.freeze()  # keep the children from dirtying every page with GC bookkeeping
+        try:
+            got = _forked([(lambda a=bt[i], b=bt[i + 1]: _pack_tensors(tv[a:b])) for i in range(k)] +
+                          [(lambda a=bn[i], b=bn[i + 1]: _pack_nodes(nodes[a:b]))
+                           for i in range(k)])
+        finally:
+            gc.unfreeze()
+        for st, val in got:
+            if st != "ok":
+                raise ValueError(val)
+        tparts = [v for _, v in got[:k]]
+        nparts = [v for _, v in got[k:]]
+    else:
+        tparts = [_pack_tensors(tv)]
+        nparts = [_pack_nodes(nodes)]
+    # slice-local constant ids -> plan ids (scale/shift/full carry one, first word)
+    for part in nparts:
+        if not part["consts"]:
+            continue
+        remap = np.array([consts(Fraction(n, d)) for n, d in part["consts"]], dtype=np.int64)
+        off = np.cumsum(part["nattr"], dtype=np.int64) - part["nattr"]
+        at = off[np.isin(part["kind"], _CONST_KINDS) & (part["nattr"] > 0)]
+        part["attrs"][at] = remap[part["attrs"][at]]
+
+    def cat(parts, key, dtype):
+        arr = np.concatenate([p[key] for p in parts]) if parts else np.zeros(0, dtype)
+        return np.ascontiguousarray(arr if arr.size else np.zeros(1, dtype), dtype=dtype)
+    arrs = dict(ndim=cat(tparts, "ndim", np.int32), dims=cat(tparts, "dims", np.int64),
+                flags=cat(tparts, "flags", np.uint8), kind=cat(nparts, "kind", np.int32),
+                nin=cat(nparts, "nin", np.int32), nout=cat(nparts, "nout", np.int32),
+                nattr=cat(nparts, "nattr", np.int32), attrs=cat(nparts, "attrs", np.int64),
+                device=cat(nparts, "device", np.int32), seq=cat(nparts, "seq", np.int64))
+    strs = dict(tn=b"".join(p["tn"] for p in tparts) or b"\0",
+                ids=b"".join(p["ids"] for p in nparts) or b"\0",
+                ins=b"".join(p["ins"] for p in nparts) or b"\0",
+                outs=b"".join(p["outs"] for p in nparts) or b"\0",
                 inputs=_joined(g.inputs))
     keep.append((arrs, strs))
 
     def p(a, t):
         return a.ctypes.data_as(t)
-    return _GraphDesc(nt, strs["tn"], p(ndim, _I32P), p(arrs["dims"], _I64P), p(flags, _U8P),
-                      nn, strs["ids"], p(kind, _I32P), p(nin, _I32P), p(nout, _I32P),
-                      strs["ins"], strs["outs"], p(arrs["nattr"], _I32P),
-                      p(arrs["attrs"], _I64P), p(device, _I32P), p(seq, _I64P),
-                      len(g.inputs), strs["inputs"])
+    return _GraphDesc(nt, strs["tn"], p(arrs["ndim"], _I32P), p(arrs["dims"], _I64P),
+                      p(arrs["flags"], _U8P), nn, strs["ids"], p(arrs["kind"], _I32P),
+                      p(arrs["nin"], _I32P), p(arrs["nout"], _I32P), strs["ins"], strs["outs"],
+                      p(arrs["nattr"], _I32P), p(arrs["attrs"], _I64P), p(arrs["device"], _I32P),
+                      p(arrs["seq"], _I64P), len(g.inputs), strs["inputs"])
 
 
 def _pack_lineage(lineage, keep: list) -> _LineageDesc:

@@ -14,6 +14,7 @@ interpretation of EXP/RSQRT/SIGMOID, replayable with exact rationals);
 
 from __future__ import annotations
 
+import hashlib
 import time
 from dataclasses import asdict, dataclass
 from typing import Any
@@ -21,8 +22,8 @@ from typing import Any
 import numpy as np
 
 from . import field as F
-from .engine import (STAGE_BAD_INDEX, STAGE_LOG_DIV0, STAGE_OK, STAGE_PAR_DIV0, STAGE_PROVEN,
-                     STAGE_REFUTED_CONST, Engine)
+from .engine import (STAGE_BAD_INDEX, STAGE_LOG_DIV0, STAGE_LOSSY, STAGE_OK, STAGE_PAR_DIV0,
+                     STAGE_PROVEN, STAGE_REFUTED_CONST, Engine)
 from .errors import EngineError, GraphError, PlanEqError, UncoveredNode
 from .graph import validate_lineage
 from .opshape import validate_concrete
@@ -69,6 +70,79 @@ def _const_detail(lw: LoweredStage, comp) -> dict[str, Any]:
     else:
         d["assignment"] = {}
     return d
+
+
+REPLAY_TOL = 1e-6   # reference stages.py:52
+REPLAY_ENVS = 8     # reference stages.py:247 (seeded candidate environments)
+# after the reference's own environments: a seeded search at decreasing
+# magnitudes, standing in for the reference's first candidate, the solver's
+# model (stages.py:246), which a witness engine does not have
+SEARCH_SCALES = (2.0, 1.0, 0.5, 0.25, 0.125)
+SEARCH_PER_SCALE = 32
+
+
+def replay_envs(tag: str, names: list[str], n_env: int = REPLAY_ENVS) -> np.ndarray:
+    """The reference's seeded replay environments (stages.py:247-252): value of
+    variable n in environment k = (sha256("tag:k:n")[:4] mod 1600 - 800) / 256."""
+    out = np.empty((n_env, len(names)), dtype=np.float64)
+    for k in range(n_env):
+        for j, n in enumerate(names):
+            h = hashlib.sha256(f"{tag}:{k}:{n}".encode()).digest()
+            out[k, j] = (int.from_bytes(h[:4], "big") % 1600 - 800) / 256.0
+    return out
+
+
+def search_envs(tag: str, n_vars: int) -> np.ndarray:
+    """Further candidate environments: uniform in [-s, s] for each search scale,
+    from a generator seeded by the stage target."""
+    seed = int.from_bytes(hashlib.sha256(f"{tag}:search".encode()).digest()[:8], "big")
+    rng = np.random.default_rng(seed)
+    return np.concatenate([rng.uniform(-s, s, size=(SEARCH_PER_SCALE, n_vars))
+                           for s in SEARCH_SCALES])
+
+
+def host_confirm(eng: Engine, index: int, target: str, names: list[str], witness: int):
+    """pqw_confirm over the reference's environments, then the search ones.
+    Returns (environments, (exact obligation, env index, replay obligation,
+    lhs, rhs, obligations with an uninterpreted function))."""
+    envs = np.concatenate([replay_envs(target, names), search_envs(target, len(names))])
+    return envs, eng.confirm(index, witness, envs, REPLAY_TOL)
+
+
+def _confirm(eng: Engine, ref, comp, first_bad: int, seed: int):
+    """A field witness broke an obligation; decide what the reference reports
+    (stages.py:221-264): an obligation free of uninterpreted functions that
+    fails at the witness is an exact rational counterexample ("refuted",
+    confirmation "exact"); otherwise the obligations with EXP/RSQRT/SIGMOID in
+    their cone are replayed with the genuine functions in the reference's
+    seeded environments -- a difference beyond REPLAY_TOL refutes
+    (confirmation "real"), none leaves the stage "unknown" with the
+    reference's reason. Returns (status, detail, note)."""
+    w, obl = first_bad >> 32, first_bad & 0xFFFFFFFF
+    lw = ref.lowered()
+    names = [lw.var_name(j) for j in range(comp.n_vars)]
+    envs, (exact, k, o2, lv, rv, n_uf) = host_confirm(eng, comp.index, ref.target, names, w)
+    if exact >= 0:
+        d = _witness_detail(eng, lw, comp, (w << 32) | exact, seed)
+        d["confirmation"] = "exact"
+        return "refuted", d, None
+    field = {"witness": w, "obligation": obl, "field": f"F_p, p={F.P}", "seed": seed,
+             "uf": "keyed-hash (field.py uf_apply)"}
+    if o2 >= 0:
+        label, idx = lw.locate(o2)
+        support = eng.support(comp.index, o2)
+        env = envs[k]
+        assign = sorted((names[j], float(env[j])) for j in support)
+        return "refuted", {"shard": label, "index": list(idx), "lhs_value": str(lv),
+                           "rhs_value": str(rv), "assignment": {n: str(v) for n, v in assign[:16]},
+                           "confirmation": "real",
+                           "replay_env": (f"reference seeded environment {k}" if k < REPLAY_ENVS
+                                          else f"search environment {k - REPLAY_ENVS}"),
+                           "obligation": o2, "field_witness": field}, None
+    return "unknown", {"reason": "countermodel failed replay confirmation",
+                       "uf_obligations": n_uf, "field_witness": field}, \
+        ("F_p witness differs only under the keyed-hash interpretation of "
+         "EXP/RSQRT/SIGMOID; the real-valued replay did not confirm it")
 
 
 def _witness_detail(engine: Engine, lw: LoweredStage, comp, first_bad: int,
@@ -179,6 +253,10 @@ def _one(ref: _StageRef, eng: Engine, opts: VerifyOptions, fb, nv, nb,
                          "constant denominator violates side condition")
     elif comp.status == STAGE_BAD_INDEX:
         raise GraphError(f"stage {ref.target}: token id outside its embedding table")
+    elif comp.status == STAGE_LOSSY:
+        r.status = "unknown"
+        r.note = ("a constant is a nonzero multiple of the field prime: evaluation in F_p "
+                  "cannot decide this stage")
     else:
         i = comp.index
         r.witnesses = opts.witnesses
@@ -186,8 +264,7 @@ def _one(ref: _StageRef, eng: Engine, opts: VerifyOptions, fb, nv, nb,
         r.failing_witnesses = int(nb[i])
         r.false_equiv_log2 = bound_log2(comp.degree, int(nv[i]))
         if int(fb[i]) != 0xFFFFFFFFFFFFFFFF:
-            r.status = "refuted"
-            r.detail = _witness_detail(eng, ref.lowered(), comp, int(fb[i]), opts.seed)
+            r.status, r.detail, r.note = _confirm(eng, ref, comp, int(fb[i]), opts.seed)
         elif int(nv[i]) == 0:
             r.status = "unknown"
             r.note = "no witness kept every denominator nonzero"

@@ -54,6 +54,7 @@ def test_gpu_stage_verdicts_match_reference(gpu, rec):
             # tests/test_replay_reference.py replays in the reference evaluator
             assert target in rec["stage_reason"]
             assert r.status == "refuted", target
+            assert r.detail["confirmation"] in ("exact", "real"), target
         else:
             assert r.status == status, target
     rep = verify_plan(plan, VerifyOptions(no_reduce=True, no_cancel=True))

@@ -42,14 +42,17 @@ def test_stage_verdicts_match_reference(gpu, rec):
     got = [(r.target, r.status) for r in results]
     want = [tuple(x) for x in ref["stage_status"]]
     assert [t for t, _ in got] == [t for t, _ in want]
-    for (t, g), (_, r) in zip(got, want):
+    for res, (t, g), (_, r) in zip(results, got, want):
         if r in ("proven", "refuted"):
             assert g == r, t
         else:
             # the reference's solver gave up (z3 timeout); the witness engine
-            # must decide -- refutations are replayed through the reference's
-            # evaluator in tests/test_replay_reference.py
+            # must decide -- a refutation carries an exact or real-valued
+            # counterexample (tests/test_confirmation.py replays the real ones
+            # through the reference's own evaluator)
             assert g in ("proven", "refuted"), t
+            if g == "refuted":
+                assert (res.detail or {}).get("confirmation") in ("exact", "real"), t
     bundled = BUNDLED.get(rec["name"])
     if bundled and "stage_status" in bundled:
         for (t, g), (_, r) in zip(got, bundled["stage_status"]):
@@ -58,7 +61,7 @@ def test_stage_verdicts_match_reference(gpu, rec):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("rec", RECS[:12], ids=[r["name"] for r in RECS[:12]])
+@pytest.mark.parametrize("rec", RECS, ids=[r["name"] for r in RECS])
 def test_witness_outcomes_bit_exact_with_oracle(gpu, rec):
     seed = 11
     plan = load_plan(rec["work_plan"])
@@ -107,7 +110,7 @@ def test_verify_plan_end_to_end_matches_reference(gpu):
             assert rep["verdict"] == ref["verdict"], rec["name"]
         else:
             assert rep["verdict"] in ("proven", "refuted"), rec["name"]
-        if rep["verdict"] == "refuted" and rep.get("counterexample", {}).get("witness") is not None:
+        if rep["verdict"] == "refuted" and rep.get("counterexample", {}).get("confirmation"):
             cx = rep["counterexample"]
             assert cx["lhs_value"] != cx["rhs_value"]
 

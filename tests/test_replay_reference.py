@@ -43,10 +43,17 @@ def _ref_modules():
     return rplan, rstages, rops, rsym, iter_box, range_extents
 
 
+_REF_CACHE: dict = {}
+
+
 def _ref_obligations(rplan, rstages, rops, rsym, iter_box, plan_text, target):
     """The reference's (lhs, rhs) expression list for one stage, in obligation order."""
-    plan = rplan.loads(plan_text)
-    stages, _ = rstages.build_stages(plan)
+    key = hash(plan_text)
+    if key not in _REF_CACHE:
+        plan = rplan.loads(plan_text)
+        _REF_CACHE.clear()
+        _REF_CACHE[key] = (plan, rstages.build_stages(plan)[0])
+    plan, stages = _REF_CACHE[key]
     stage = next(s for s in stages if s.target == target)
     alg = rsym.Algebra()
     ctx = rsym.ExecContext(alg)
@@ -92,7 +99,14 @@ def _ref_obligations(rplan, rstages, rops, rsym, iter_box, plan_text, target):
             vts = [env_p[s.tensor] for s in members]
             for li, g in enumerate(iter_box(ranges)):
                 out.append((box.at(g), alg.addn([vt.data[li] for vt in vts])))
+    _ref_obligations.last_conds = ctx.conds
     return out, alg
+
+
+def _ref_obligations_ctx(rplan, rstages, rops, rsym, iter_box, plan_text, target):
+    """(obligation expression pairs, definedness conditions) of one stage."""
+    pairs, _alg = _ref_obligations(rplan, rstages, rops, rsym, iter_box, plan_text, target)
+    return pairs, _ref_obligations.last_conds
 
 
 @pytest.mark.parametrize("rec", RECS, ids=[r["name"] for r in RECS])
