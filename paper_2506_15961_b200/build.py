@@ -22,7 +22,31 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _ext_path() -> str:
+    import sysconfig
+    return os.path.join(HERE, "_pqw_pack" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_pack(force: bool = False) -> str:
+    """The CPython host packer (csrc/pack.cpp -> _pqw_pack extension, g++)."""
+    import sysconfig
+    out = _ext_path()
+    src = os.path.join(CSRC, "pack.cpp")
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= os.path.getmtime(src):
+        return out
+    cxx = os.environ.get("CXX", "g++")
+    cmd = [cxx, "-O2", "-std=c++17", "-shared", "-fPIC", "-I", sysconfig.get_paths()["include"],
+           src, "-o", out + ".tmp"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("g++ failed building the _pqw_pack extension")
+    os.replace(out + ".tmp", out)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    build_pack(force)
     if not force and not _stale():
         return OUT
     nvcc = os.environ.get("NVCC", "nvcc")

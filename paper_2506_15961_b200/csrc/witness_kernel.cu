@@ -711,6 +711,9 @@ int pqw_probe(pqw_engine* e, int stage, uint32_t witness, uint32_t obl, uint32_t
     if (e->gpu_stage_of[r] == stage) break;
   uint32_t* d_vars = nullptr;
   CU(cudaMalloc(&d_vars, std::max<size_t>(st.n_vars, 1) * sizeof(uint32_t)));
+  // variables the program never reads (pruned by value numbering) keep this
+  // marker (not a field element) and get their value from the host below
+  CU(cudaMemset(d_vars, 0xFF, std::max<size_t>(st.n_vars, 1) * sizeof(uint32_t)));
   uint32_t* d_work1 = nullptr;
   CU(cudaMalloc(&d_work1, sizeof(uint32_t)));
   CU(cudaMemcpy(d_work1, &r, sizeof(uint32_t), cudaMemcpyHostToDevice));
@@ -743,8 +746,12 @@ int pqw_probe(pqw_engine* e, int stage, uint32_t witness, uint32_t obl, uint32_t
   CU(cudaMemcpy(got, e->d_probe, sizeof(got), cudaMemcpyDeviceToHost));
   if (lhs) *lhs = got[0];
   if (rhs) *rhs = got[1];
-  if (var_vals && st.n_vars)
+  if (var_vals && st.n_vars) {
     CU(cudaMemcpy(var_vals, d_vars, st.n_vars * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    for (uint32_t i = 0; i < st.n_vars; ++i)
+      if (var_vals[i] == 0xFFFFFFFFu)
+        var_vals[i] = pqw::witness_value(e->var_keys[st.var_base + i], witness);
+  }
   cudaFree(d_vars);
   cudaFree(d_work1);
   return PQW_OK;

@@ -30,7 +30,6 @@ distinct rational constants):
 from __future__ import annotations
 
 import ctypes as C
-import os
 from collections import defaultdict
 from fractions import Fraction
 from itertools import chain
@@ -212,92 +211,46 @@ def _pack_nodes(nodes: list) -> dict:
                 consts=list(consts.idx))
 
 
-PARALLEL_PACK_MIN = 150_000  # nodes; smaller graphs pack in-process
-
-
-def _workers() -> int:
+def _ext():
     try:
-        n = len(os.sched_getaffinity(0))
-    except (AttributeError, OSError):
-        n = os.cpu_count() or 1
-    return max(1, min(16, n))
+        from . import _pqw_pack
+        return _pqw_pack
+    except ImportError:
+        return None
 
 
-def _forked(jobs: list) -> list:
-    """Run zero-argument callables in forked children (they inherit the plan
-    copy-on-write) and return their pickled results in order. Used for the
-    per-node Python work of packing a large plan; children touch no CUDA."""
-    import pickle
-    procs = []
-    for fn in jobs:
-        r, w = os.pipe()
-        pid = os.fork()
-        if pid == 0:  # child
-            os.close(r)
-            try:
-                out = pickle.dumps(("ok", fn()), protocol=pickle.HIGHEST_PROTOCOL)
-            except BaseException as e:  # noqa: BLE001 - reported to the parent
-                out = pickle.dumps(("err", f"{type(e).__name__}: {e}"))
-            with os.fdopen(w, "wb") as f:
-                f.write(out)
-            os._exit(0)
-        os.close(w)
-        procs.append((pid, r))
-    results = []
-    for pid, r in procs:
-        with os.fdopen(r, "rb") as f:
-            data = f.read()
-        os.waitpid(pid, 0)
-        results.append(pickle.loads(data) if data else ("err", "packer child died"))
-    return results
+def _pack_columns(g: Graph, consts: _Consts) -> tuple[dict, tuple[int, int, int]]:
+    """Flat columns of a graph: through the C++ packer (csrc/pack.cpp) when it
+    is built, else the Python restatement above."""
+    ext = _ext()
+    if ext is not None:
+        d = ext.pack_graph(g, OPCODE, lambda v: consts(v))
+        cols = {k: d[k] for k in ("tn", "ids", "ins", "outs", "inputs")}
+        for k, dt in (("ndim", np.int32), ("dims", np.int64), ("flags", np.uint8),
+                      ("kind", np.int32), ("nin", np.int32), ("nout", np.int32),
+                      ("nattr", np.int32), ("attrs", np.int64), ("device", np.int32),
+                      ("seq", np.int64)):
+            cols[k] = np.frombuffer(d[k], dtype=dt)
+        return cols, d["counts"]
+    tv = list(g.tensors.values())
+    t = _pack_tensors(tv)
+    t["tn"] = _zjoin(g.tensors, len(tv))
+    n = _pack_nodes(g.nodes)
+    if n["consts"]:  # slice-local constant ids -> plan ids
+        remap = np.array([consts(Fraction(a, b)) for a, b in n["consts"]], dtype=np.int64)
+        off = np.cumsum(n["nattr"], dtype=np.int64) - n["nattr"]
+        at = off[np.isin(n["kind"], _CONST_KINDS) & (n["nattr"] > 0)]
+        n["attrs"][at] = remap[n["attrs"][at]]
+    cols = {**t, **n, "inputs": _zjoin(g.inputs, len(g.inputs))}
+    return cols, (len(tv), len(g.nodes), len(g.inputs))
 
 
 def _pack_graph(g: Graph, consts: _Consts, keep: list) -> _GraphDesc:
-    tv = list(g.tensors.values())
-    nodes = g.nodes
-    nt, nn = len(tv), len(nodes)
-    k = _workers() if nn >= PARALLEL_PACK_MIN else 1
-    if k > 1:
-        import gc
-        bt = [(i * nt) // k for i in range(k + 1)]
-        bn = [(i * nn) // k for i in range(k + 1)]
-        gc.freeze()  # keep the children from dirtying every page with GC bookkeeping
-        try:
-            got = _forked([(lambda a=bt[i], b=bt[i + 1]: _pack_tensors(tv[a:b])) for i in range(k)] +
-                          [(lambda a=bn[i], b=bn[i + 1]: _pack_nodes(nodes[a:b]))
-                           for i in range(k)])
-        finally:
-            gc.unfreeze()
-        for st, val in got:
-            if st != "ok":
-                raise ValueError(val)
-        tparts = [v for _, v in got[:k]]
-        nparts = [v for _, v in got[k:]]
-    else:
-        tparts = [_pack_tensors(tv)]
-        nparts = [_pack_nodes(nodes)]
-    # slice-local constant ids -> plan ids (scale/shift/full carry one, first word)
-    for part in nparts:
-        if not part["consts"]:
-            continue
-        remap = np.array([consts(Fraction(n, d)) for n, d in part["consts"]], dtype=np.int64)
-        off = np.cumsum(part["nattr"], dtype=np.int64) - part["nattr"]
-        at = off[np.isin(part["kind"], _CONST_KINDS) & (part["nattr"] > 0)]
-        part["attrs"][at] = remap[part["attrs"][at]]
-
-    def cat(parts, key, dtype):
-        arr = np.concatenate([p[key] for p in parts]) if parts else np.zeros(0, dtype)
-        return np.ascontiguousarray(arr if arr.size else np.zeros(1, dtype), dtype=dtype)
-    arrs = dict(ndim=cat(tparts, "ndim", np.int32), dims=cat(tparts, "dims", np.int64),
-                flags=cat(tparts, "flags", np.uint8), kind=cat(nparts, "kind", np.int32),
-                nin=cat(nparts, "nin", np.int32), nout=cat(nparts, "nout", np.int32),
-                nattr=cat(nparts, "nattr", np.int32), attrs=cat(nparts, "attrs", np.int64),
-                device=cat(nparts, "device", np.int32), seq=cat(nparts, "seq", np.int64))
-    strs = dict(tn=b"".join(p["tn"] for p in tparts) or b"\0",
-                ids=b"".join(p["ids"] for p in nparts) or b"\0",
-                ins=b"".join(p["ins"] for p in nparts) or b"\0",
-                outs=b"".join(p["outs"] for p in nparts) or b"\0",
-                inputs=_joined(g.inputs))
+    cols, (nt, nn, ng) = _pack_columns(g, consts)
+    arrs = {k: np.ascontiguousarray(cols[k] if cols[k].size else np.zeros(1, cols[k].dtype))
+            for k in ("ndim", "dims", "flags", "kind", "nin", "nout", "nattr", "attrs",
+                      "device", "seq")}
+    strs = {k: cols[k] or b"\0" for k in ("tn", "ids", "ins", "outs", "inputs")}
     keep.append((arrs, strs))
 
     def p(a, t):
@@ -306,7 +259,7 @@ def _pack_graph(g: Graph, consts: _Consts, keep: list) -> _GraphDesc:
                       p(arrs["flags"], _U8P), nn, strs["ids"], p(arrs["kind"], _I32P),
                       p(arrs["nin"], _I32P), p(arrs["nout"], _I32P), strs["ins"], strs["outs"],
                       p(arrs["nattr"], _I32P), p(arrs["attrs"], _I64P), p(arrs["device"], _I32P),
-                      p(arrs["seq"], _I64P), len(g.inputs), strs["inputs"])
+                      p(arrs["seq"], _I64P), ng, strs["inputs"])
 
 
 def _pack_lineage(lineage, keep: list) -> _LineageDesc:

@@ -160,3 +160,31 @@ def test_verify_plan_reports_stage_errors_of_the_host(lib):
     assert not nat.build_stages()
     with pytest.raises(GraphError):
         build_stages(plan)
+
+
+@pytest.mark.parametrize("name,rel", PLANS[:8] + PLANS[-4:], ids=[n for n, _ in PLANS[:8] + PLANS[-4:]])
+def test_cpp_packer_matches_python_packer(lib, name, rel):
+    """csrc/pack.cpp (the _pqw_pack extension) emits the columns of native.py's
+    Python packer, byte for byte, for both graphs."""
+    from paper_2506_15961_b200 import native as N
+    ext = N._ext()
+    assert ext is not None, "the _pqw_pack extension is not built"
+    plan = load_plan(rel)
+    for g in (plan.logical, plan.parallel):
+        c1, c2 = N._Consts(), N._Consts()
+        got, cnt = N._pack_columns(g, c1)
+        try:
+            N._ext = lambda: None
+            want, cnt2 = N._pack_columns(g, c2)
+        finally:
+            N._ext = lambda: ext
+        assert cnt == cnt2
+        assert c1.triples == c2.triples
+        for k in want:
+            if k == "consts":
+                continue
+            a, b = got[k], want[k]
+            if isinstance(b, bytes):
+                assert a == b, (name, k)
+            else:
+                assert np.array_equal(np.asarray(a), np.asarray(b)), (name, k)
