@@ -24,6 +24,8 @@
 #include "schedule.hpp"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <deque>
 #include <queue>
 #include <set>
@@ -375,6 +377,11 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
         rdb_off[u + 1] = (uint32_t)rdb.size();
       }
     }
+    // A spilled VAR or CONST is rematerialised instead of going through global
+    // memory: its witness value (key from L1, one hash) or residue is recomputed
+    // into a temporary before every reading bundle, it is never stored, and its
+    // defining bundle drops it.
+    auto remat_ok = [&](uint32_t v) { return U[v].op == I_VAR || U[v].op == I_CONST; };
     // slots the exact colouring below will need for a spill choice: the most
     // shared-memory intervals alive at once (a slot frees strictly after its
     // interval's end), without building the intervals themselves
@@ -390,7 +397,7 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
         if (!spilled[v]) {
           add(vdef[v], vend[v]);
         } else {
-          add(vdef[v], rend(bdef) + 1);
+          if (!remat_ok(v)) add(vdef[v], rend(bdef) + 1);
           for (uint32_t i = rdb_off[v]; i < rdb_off[v + 1]; ++i) add(bts[rdb[i]] - 1, rend(rdb[i]));
         }
       }
@@ -490,7 +497,7 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
       std::vector<uint8_t> needs_fill(NB, 0), needs_spill(NB, 0);
       for (uint32_t v : values) {
         if (!spilled[v]) continue;
-        needs_spill[bundle_of[v]] = 1;
+        if (!remat_ok(v)) needs_spill[bundle_of[v]] = 1;
         for (uint32_t i = cons_off[v]; i < cons_off[v + 1]; ++i) needs_fill[bundle_of[cons[i]]] = 1;
       }
       for (uint32_t b = 0; b < NB; ++b) {
@@ -518,6 +525,13 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
           for (const uint32_t* b = rd0; b != rd1; ++b) I.readers.push_back((uint32_t)main_exec[*b]);
           v_iv[v] = (uint32_t)sm.size();
           sm.push_back(std::move(I));
+        } else if (remat_ok(v)) {
+          for (const uint32_t* pb = rd0; pb != rd1; ++pb) {
+            const uint32_t b = *pb;
+            Interval Fi{bts[b] - 1, rend(b), (uint32_t)fill_of[b], {(uint32_t)main_exec[b]}};
+            fill_iv[((uint64_t)b << 32) | v] = (uint32_t)sm.size();
+            sm.push_back(std::move(Fi));
+          }
         } else {
           Interval T1{vdef[v], rend(bdef) + 1, (uint32_t)main_exec[bdef], {(uint32_t)spill_of[bdef]}};
           v_iv[v] = (uint32_t)sm.size();
@@ -581,7 +595,7 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
         const uint32_t bdef = bundle_of[v];
         if (!spilled[v]) {
           for (uint32_t r : sm[v_iv[v]].readers) need(r, (uint32_t)main_exec[bdef]);
-        } else {
+        } else if (!remat_ok(v)) {
           for (uint32_t r : gm[v_giv[v]].readers) need(r, (uint32_t)spill_of[bdef]);
         }
       }
@@ -666,26 +680,54 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
             prog.op_hist[I_WAIT]++;
           }
           prog.n_waits += (uint32_t)nwait;
-          const size_t hdr = code.size();  // header of this exec's instruction
+          const size_t hdr = code.size();  // header of this exec's (first) instruction
+          size_t last_hdr = hdr;            // header that publishes the exec's progress
           const auto& B = bundles[E.main];
           if (E.kind == 1 || E.kind == 2) {
             fields.clear();
             uint32_t n = 0;
             if (E.kind == 1) {
-              std::vector<uint32_t> seen;
+              // global fills, then rematerialised VARs, then CONSTs (one exec:
+              // the wait rides on the first header, the signal on the last)
+              std::vector<uint32_t> seen, fvar, fcst;
+              uint32_t nv = 0, nc = 0;
               for (uint32_t u : B.units)
                 for (uint32_t a = 0; a < U[u].nargs; ++a) {
                   const uint32_t v = dag.pool[U[u].arg0 + a];
                   if (!spilled[v] || std::find(seen.begin(), seen.end(), v) != seen.end()) continue;
                   seen.push_back(v);
-                  fields.push_back(soff(fill_iv.at(((uint64_t)E.main << 32) | v)));
-                  fields.push_back(gm[v_giv[v]].slot * SLOT_BYTES);
-                  n++;
+                  const uint32_t dst = soff(fill_iv.at(((uint64_t)E.main << 32) | v));
+                  if (U[v].op == I_VAR) {
+                    fvar.push_back(dst);
+                    fvar.push_back(U[v].aux);
+                    nv++;
+                  } else if (U[v].op == I_CONST) {
+                    fcst.push_back(dst);
+                    fcst.push_back(U[v].aux);
+                    nc++;
+                  } else {
+                    fields.push_back(dst);
+                    fields.push_back(gm[v_giv[v]].slot * SLOT_BYTES);
+                    n++;
+                  }
                 }
-              put_bundle(I_FILL, 0, 0, n, 0, fields, 2);
+              if (n) {
+                last_hdr = code.size();
+                put_bundle(I_FILL, 0, 0, n, 0, fields, 2);
+              }
+              if (nv) {
+                last_hdr = code.size();
+                put_bundle(I_VAR, 0, 0, nv, 0, fvar, 2);
+                prog.n_remat += nv;
+              }
+              if (nc) {
+                last_hdr = code.size();
+                put_bundle(I_CONST, 0, 0, nc, 0, fcst, 2);
+                prog.n_remat += nc;
+              }
             } else {
               for (uint32_t u : B.units)
-                if (U[u].defines() && spilled[u]) {
+                if (U[u].defines() && spilled[u] && !remat_ok(u)) {
                   fields.push_back(gm[v_giv[u]].slot * SLOT_BYTES);
                   fields.push_back(soff(v_iv[u]));
                   n++;
@@ -714,6 +756,7 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
                   break;
                 case I_VAR:
                 case I_CONST:
+                  if (spilled[u]) break;  // rematerialised at every reader instead
                   fields.push_back(soff(v_iv[u]));
                   fields.push_back(d.aux);
                   break;
@@ -727,7 +770,7 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
                 case I_DOT: prog.cls[0] += d.k; prog.cls[1] += d.k - 1; break;
                 case I_SUM: prog.cls[1] += d.k - 1; break;
                 case I_SUB: case I_NEG: prog.cls[1] += 1; break;
-                case I_HASH: case I_VAR: prog.cls[2] += 1; break;
+                case I_HASH: case I_VAR: prog.cls[2] += 1; break;  // remat copies not counted
                 case I_CHK: case I_DEN: prog.cls[4] += 1; break;
                 default: break;
               }
@@ -738,7 +781,7 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
               prog.cls[0] += 3 * (n - 1);
               prog.cls[3] += 1;
             }
-            put_bundle(H.op, H.fn, H.k, (uint32_t)B.units.size(), 0, fields, nf);
+            put_bundle(H.op, H.fn, H.k, (uint32_t)(fields.size() / nf), 0, fields, nf);
           }
           if (nwait) {
             const auto& pr = waits[e][nwait - 1];
@@ -746,7 +789,7 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
             code[hdr].a = ((pr.first + 1) << 24) | pr.second;
           }
           if (signal_after[e]) {
-            code[hdr].b = E.seq + 1;  // header.w: publish progress after this bundle
+            code[last_hdr].b = E.seq + 1;  // header.w: publish progress after this exec
             prog.op_hist[I_SIGNAL]++;
           }
         }
@@ -757,6 +800,18 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
       prog.n_bundles = NB;
       prog.makespan = makespan;
       for (uint32_t v : values) prog.n_spilled_values += spilled[v];
+      if (getenv("PQW_DEBUG_SPILL")) {
+        uint64_t by[I_NUM_OPS] = {}, fills[I_NUM_OPS] = {};
+        for (uint32_t v : values)
+          if (spilled[v]) {
+            by[U[v].op]++;
+            fills[U[v].op] += rdb_off[v + 1] - rdb_off[v];
+          }
+        fprintf(stderr, "SPILLDBG values=%zu spilled:", values.size());
+        for (int i = 0; i < I_NUM_OPS; ++i)
+          if (by[i]) fprintf(stderr, " op%d=%llu(fills %llu)", i, (unsigned long long)by[i], (unsigned long long)fills[i]);
+        fprintf(stderr, "\n");
+      }
       return true;
     }
     return false;

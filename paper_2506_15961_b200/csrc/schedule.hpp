@@ -45,6 +45,7 @@ struct Program {
   uint32_t n_slots = 0;        // shared slots used
   uint32_t n_spill = 0;        // global spill slots used
   uint32_t n_spilled_values = 0;
+  uint32_t n_remat = 0;        // VAR/CONST ops recomputed at readers instead of filled
   uint32_t n_bundles = 0;
   uint32_t n_waits = 0;        // (warp, count) pairs waited on
   uint64_t makespan = 0;       // cost-model length of the schedule
