@@ -225,6 +225,21 @@ __device__ __forceinline__ uint32_t run_elementwise(CodeRing& cr, uint32_t pc, u
   return pc;
 }
 
+// FILL bundle: global spill slots -> shared value file.
+__device__ __forceinline__ uint32_t run_fill(CodeRing& cr, uint32_t pc, uint32_t n, uint32_t sb,
+                                             const uint8_t* gl) {
+  for (uint32_t g = 0; g < n; g += 8, pc += 4) {
+    cr.ensure(pc, 4);
+    const F8 D = cr.rd8(pc), G = cr.rd8(pc + 2);
+    uint32_t a[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const uint32_t*>(gl + G.v[i]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sts(sb, D.v[i], a[i]);
+  }
+  return pc;
+}
+
 // Wait (all lanes) until a warp's published progress reaches `target`.
 __device__ __forceinline__ void wait_progress(const Params& p, const uint32_t* flag,
                                               uint32_t target) {
@@ -271,6 +286,24 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
     const uint32_t cls = op == I_DOT ? (kk == 1 ? 0 : kk == 2 ? 1 : 2)
                        : op == I_SUM ? (kk == 2 ? 3 : 4)
                        : op + 2;  // SUB 5 .. WAIT 15
+#endif
+#ifdef PQW_IFCHAIN
+    // the most frequent bundles by direct, predictable branches; the rest
+    // through the jump table
+    const uint32_t kx = h.x >> 16;
+    if (op == I_WAIT) {
+      wait_progress(p, prog + h.z, h.w);
+    } else if (op == I_DOT && kx == 1) {
+      pc = run_elementwise<2>(cr, pc, n, sb, [](const uint32_t* x) { return fmul(x[0], x[1]); });
+    } else if (op == I_FILL) {
+      pc = run_fill(cr, pc, n, sb, gl);
+    } else if (op == I_SUM && kx == 2) {
+      pc = run_elementwise<2>(cr, pc, n, sb, [](const uint32_t* x) { return fadd(x[0], x[1]); });
+    } else if (op == I_DOT && kx == 2) {
+      pc = run_elementwise<4>(cr, pc, n, sb, [](const uint32_t* x) {
+        return red64((uint64_t)x[0] * x[1] + (uint64_t)x[2] * x[3]);
+      });
+    } else
 #endif
     switch (op) {
       case I_END:
@@ -437,15 +470,7 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
         }
         break;
       case I_FILL:
-        for (uint32_t g = 0; g < n; g += 8, pc += 4) {
-          cr.ensure(pc, 4);
-          const F8 D = cr.rd8(pc), G = cr.rd8(pc + 2);
-          uint32_t a[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const uint32_t*>(gl + G.v[i]);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) sts(sb, D.v[i], a[i]);
-        }
+        pc = run_fill(cr, pc, n, sb, gl);
         break;
       case I_SPILL:
         for (uint32_t g = 0; g < n; g += 8, pc += 4) {

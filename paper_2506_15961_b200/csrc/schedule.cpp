@@ -377,11 +377,15 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
         rdb_off[u + 1] = (uint32_t)rdb.size();
       }
     }
-    // A spilled VAR or CONST is rematerialised instead of going through global
-    // memory: its witness value (key from L1, one hash) or residue is recomputed
-    // into a temporary before every reading bundle, it is never stored, and its
-    // defining bundle drops it.
-    auto remat_ok = [&](uint32_t v) { return U[v].op == I_VAR || U[v].op == I_CONST; };
+    // A spilled CONST is rematerialised instead of going through global memory:
+    // its residue is written into a temporary before every reading bundle, it
+    // is never stored, and its defining bundle drops it. (Rematerialising
+    // spilled VARs the same way -- key load plus hash per reader -- measured
+    // slower than filling them: the keys miss the L1 the value file leaves.)
+    const bool remat_var = getenv("PQW_REMAT_VAR") != nullptr;
+    auto remat_ok = [&](uint32_t v) {
+      return U[v].op == I_CONST || (remat_var && U[v].op == I_VAR);
+    };
     // slots the exact colouring below will need for a spill choice: the most
     // shared-memory intervals alive at once (a slot frees strictly after its
     // interval's end), without building the intervals themselves
@@ -416,6 +420,18 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
     // keeping at most keff values resident; when full, the resident value (or
     // the new one) that ends last is spilled. Two heaps over (end, value) with
     // lazy deletion: the earliest end expires, the latest end is evicted.
+    // default: evict the value whose live length per squared read count is
+    // largest (rarely read, long-lived values go to global memory first);
+    // PQW_SPILL_MODE=0 restores the latest-ending rule (fewest spilled values)
+    static const int spill_mode = getenv("PQW_SPILL_MODE") ? atoi(getenv("PQW_SPILL_MODE")) : 3;
+    auto evict_key = [&](uint32_t v) -> uint64_t {
+      if (spill_mode == 0) return vend[v];
+      const uint64_t reads = rdb_off[v + 1] - rdb_off[v];
+      if (spill_mode == 1) return (vend[v] - vdef[v]) / (reads + 1);
+      if (spill_mode == 3) return (vend[v] - vdef[v]) / ((reads + 1) * (reads + 1));
+      if (spill_mode == 4) return (vend[v] - vdef[v]) * 4 / (reads + 4);
+      return vend[v] / (reads + 1);
+    };
     auto select = [&](uint32_t keff, std::vector<uint8_t>& spilled) {
       spilled.assign(N, 0);
       using E = std::pair<uint64_t, uint32_t>;
@@ -435,15 +451,15 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
         while (!by_last.empty() && gone[by_last.top().second]) by_last.pop();
         if (n_active < keff) {
           by_first.push({vend[v], v});
-          by_last.push({vend[v], v});
+          by_last.push({evict_key(v), v});
           n_active++;
-        } else if (by_last.top().first > vend[v]) {
+        } else if (by_last.top().first > evict_key(v)) {
           const uint32_t x = by_last.top().second;
           by_last.pop();
           gone[x] = 1;
           spilled[x] = 1;
           by_first.push({vend[v], v});
-          by_last.push({vend[v], v});
+          by_last.push({evict_key(v), v});
         } else {
           spilled[v] = 1;
         }
@@ -697,11 +713,11 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
                   if (!spilled[v] || std::find(seen.begin(), seen.end(), v) != seen.end()) continue;
                   seen.push_back(v);
                   const uint32_t dst = soff(fill_iv.at(((uint64_t)E.main << 32) | v));
-                  if (U[v].op == I_VAR) {
+                  if (U[v].op == I_VAR && remat_ok(v)) {
                     fvar.push_back(dst);
                     fvar.push_back(U[v].aux);
                     nv++;
-                  } else if (U[v].op == I_CONST) {
+                  } else if (U[v].op == I_CONST && remat_ok(v)) {
                     fcst.push_back(dst);
                     fcst.push_back(U[v].aux);
                     nc++;
@@ -756,7 +772,7 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
                   break;
                 case I_VAR:
                 case I_CONST:
-                  if (spilled[u]) break;  // rematerialised at every reader instead
+                  if (spilled[u] && remat_ok(u)) break;  // rematerialised at every reader
                   fields.push_back(soff(v_iv[u]));
                   fields.push_back(d.aux);
                   break;

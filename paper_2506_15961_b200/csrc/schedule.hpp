@@ -34,7 +34,7 @@ struct SchedOptions {
   uint32_t window = 0;         // look-ahead in units past the lowest unscheduled one (0: adaptive)
   uint32_t bmax = 32;          // max ops per bundle
   uint32_t xlat = 32;          // cost-model penalty of a cross-warp dependence
-  uint32_t bundle_base = 100;  // cost-model constant per bundle (dispatch + latency)
+  uint32_t bundle_base = 600;  // cost-model constant per bundle (dispatch + latency; measured best on 405B)
   uint32_t spill_cost = 8;     // cost-model weight of one FILL/SPILL op when choosing a window
   uint32_t pick_scan = 0;      // >0: pick the longest-path unit among that many eligible ones
   uint32_t active_warps = 32;  // warps that receive work (the rest run empty streams)
