@@ -588,6 +588,25 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
       if (n_sm > K) fail("internal: colouring needs more slots than the interval count");
       owners(gm, g_own, g_wr);
       const uint32_t n_gm = colour(gm, gprev, g_own, g_wr, NW);
+      if (getenv("PQW_DEBUG_QUAD")) {
+        // slot-time of shared intervals whose writer and readers share a quadrant
+        uint64_t tot = 0, loc = 0, nloc = 0, same_warp = 0;
+        for (const auto& I : sm) {
+          const uint64_t len = I.end - I.start;
+          tot += len;
+          const uint32_t q = ex[I.writer].warp % 4;
+          bool l = true, sw = true;
+          for (uint32_t r : I.readers) {
+            l = l && ex[r].warp % 4 == q;
+            sw = sw && ex[r].warp == ex[I.writer].warp;
+          }
+          if (l) { loc += len; nloc++; }
+          if (sw) same_warp += len;
+        }
+        fprintf(stderr, "QUADDBG intervals=%zu slots=%u quad-local slot-time %.1f%% (n=%llu) same-warp %.1f%%\n",
+                sm.size(), n_sm, 100.0 * loc / std::max<uint64_t>(tot, 1), (unsigned long long)nloc,
+                100.0 * same_warp / std::max<uint64_t>(tot, 1));
+      }
 
       // ---- 3. synchronisation -------------------------------------------------
       const uint32_t NE = (uint32_t)ex.size();
