@@ -101,3 +101,61 @@ def test_two_rank_gloo_discharge_matches_single_process(rec, no_cancel):
         assert cancelled == want_cancelled
         assert sum(per_rank) == len(stages) and min(per_rank) > 0
     assert stage_cost(stages[0]) > 0
+
+
+def _native_worker(rank, world, port, plan_name, q):
+    """One rank of the product's native partition (distributed._native_share up
+    to the discharge): lower every stage, cost it with the compiler front end,
+    LPT-partition the costs, select this rank's share."""
+    import torch.distributed as dist
+    from paper_2506_15961_b200 import field as F
+    from paper_2506_15961_b200.engine import STAGE_OK, Engine
+    from paper_2506_15961_b200.native import NativePlan
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        plan = load_plan(plan_name)
+        nat = NativePlan(plan)
+        assert nat.validate() and nat.build_stages()
+        eng = Engine(0, 3, F.fn_keys(3))
+        idx = nat.add_stages(eng, 3)
+        costs = [eng.cost(int(k)) for k in idx]
+        ok = [eng.stage_status(int(k)).status == STAGE_OK for k in idx]
+        parts = partition(costs, world)
+        flags = [0] * eng.n_stages
+        for i in parts[rank]:
+            flags[int(idx[i])] = 1
+        eng.select(flags)
+        st = eng.image_stats()  # back ends of the selected share only
+        gathered = [None] * world
+        dist.all_gather_object(gathered, parts)
+        q.put((rank, parts, gathered, costs, ok, st["gpu_stages"]))
+        eng.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_native_partition_is_consistent():
+    """gloo, world size 2: every rank derives the same partition of the native
+    plan's stages from front-end device costs (decided stages cost 0), the
+    shares are disjoint and complete, and each rank schedules only the
+    GPU stages of its own share."""
+    rec = next(r for r in verdicts() if r["name"] == "dp2tp2pp2nm2")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_native_worker, args=(r, 2, port, rec["work_plan"], q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    out.sort()
+    (_, p0, g0, c0, ok0, n0), (_, p1, g1, c1, ok1, n1) = out
+    assert g0 == g1 == [p0, p1]
+    assert sorted(p0[0] + p0[1]) == list(range(len(c0)))
+    assert c0 == c1 and ok0 == ok1
+    assert all((c > 0) == o for c, o in zip(c0, ok0))
+    assert n0 == sum(1 for i in p0[0] if ok0[i]) and n1 == sum(1 for i in p0[1] if ok0[i])

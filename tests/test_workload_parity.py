@@ -150,6 +150,11 @@ def test_full_workload_stage_verdicts_match_reference(gpu, rec):
     for r, (target, status) in zip(results, want):
         if status in ("proven", "refuted"):
             assert r.status == status, target
+        elif status == "error":
+            # the reference itself failed on this stage (out of memory under
+            # the sweep's per-worker cap on the MoE stages, stage_reason); the
+            # engine must still decide it
+            assert r.status in ("proven", "refuted"), target
         elif r.status == "refuted":
             # the reference's replay did not confirm its countermodel; ours must
             # carry an exact or real-valued counterexample
