@@ -109,7 +109,7 @@ def host_confirm(eng: Engine, index: int, target: str, names: list[str], witness
     return envs, eng.confirm(index, witness, envs, REPLAY_TOL)
 
 
-def _confirm(eng: Engine, ref, comp, first_bad: int, seed: int):
+def _confirm(eng: Engine, ref, comp, first_bad: int, seed: int, source=None):
     """A field witness broke an obligation; decide what the reference reports
     (stages.py:221-264): an obligation free of uninterpreted functions that
     fails at the witness is an exact rational counterexample ("refuted",
@@ -123,7 +123,7 @@ def _confirm(eng: Engine, ref, comp, first_bad: int, seed: int):
     names = [lw.var_name(j) for j in range(comp.n_vars)]
     envs, (exact, k, o2, lv, rv, n_uf) = host_confirm(eng, comp.index, ref.target, names, w)
     if exact >= 0:
-        d = _witness_detail(eng, lw, comp, (w << 32) | exact, seed)
+        d = _witness_detail(eng, lw, comp, (w << 32) | exact, seed, source)
         d["confirmation"] = "exact"
         return "refuted", d, None
     field = {"witness": w, "obligation": obl, "field": f"F_p, p={F.P}", "seed": seed,
@@ -146,9 +146,9 @@ def _confirm(eng: Engine, ref, comp, first_bad: int, seed: int):
 
 
 def _witness_detail(engine: Engine, lw: LoweredStage, comp, first_bad: int,
-                    seed: int) -> dict[str, Any]:
+                    seed: int, source=None) -> dict[str, Any]:
     w, obl = int(first_bad) >> 32, int(first_bad) & 0xFFFFFFFF
-    lhs, rhs, vals = engine.probe(comp.index, w, obl, comp.n_vars)
+    lhs, rhs, vals = (source or EngineWitnesses(engine)).probe(comp, w, obl)
     label, idx = lw.locate(obl)
     support = engine.support(comp.index, obl)
     names = sorted((lw.var_name(i), int(vals[i])) for i in support)
@@ -171,10 +171,11 @@ class _StageRef:
     counterexample reports and to raise deferred lowering errors), and its
     engine compile handle (None when the host lowering raises)."""
 
-    __slots__ = ("target", "lower", "comp", "lw")
+    __slots__ = ("target", "lower", "comp", "lw", "stage")
 
-    def __init__(self, target: str, lower, comp, lw=None):
+    def __init__(self, target: str, lower, comp, lw=None, stage: int = -1):
         self.target, self.lower, self.comp, self.lw = target, lower, comp, lw
+        self.stage = stage  # index in the plan's stage list
 
     def lowered(self) -> LoweredStage:
         if self.lw is None:
@@ -182,8 +183,27 @@ class _StageRef:
         return self.lw
 
 
+class EngineWitnesses:
+    """Where witness outcomes come from: the engine's device image (upload,
+    one launch, results; probe re-evaluates one witness on the GPU). The one
+    implementation the product uses; tests may substitute a CPU source with
+    the same two methods to drive the host logic without a device."""
+
+    def __init__(self, eng: Engine):
+        self.eng = eng
+
+    def run(self, refs, opts) -> tuple:
+        self.eng.upload()
+        self.eng.launch(opts.witnesses)
+        fb, nv, nb = self.eng.results()
+        return fb, nv, nb, self.eng.last_launch_ms()
+
+    def probe(self, comp, w: int, obl: int):
+        return self.eng.probe(comp.index, w, obl, comp.n_vars)
+
+
 def _run(refs: list[_StageRef], eng: Engine, opts: VerifyOptions, host_s: float,
-         stats: dict, errors: str = "raise") -> tuple[list, int, dict]:
+         stats: dict, errors: str = "raise", source=None) -> tuple[list, int, dict]:
     """Compile (pending front/back ends), launch once, and turn the engine's
     per-stage outcome into StageResults in stage order with the reference's
     cancellation (verify.py:119-122). errors="collect": a stage whose
@@ -193,11 +213,9 @@ def _run(refs: list[_StageRef], eng: Engine, opts: VerifyOptions, host_s: float,
     needs_gpu = any(c is not None and c.status == STAGE_OK for c in comps)
     gpu_ms = 0.0
     fb = nv = nb = None
+    source = source or EngineWitnesses(eng)
     if needs_gpu:
-        eng.upload()
-        eng.launch(opts.witnesses)
-        fb, nv, nb = eng.results()
-        gpu_ms = eng.last_launch_ms()
+        fb, nv, nb, gpu_ms = source.run(refs, opts)
     t_dev = time.perf_counter() - t0
     n_gpu = sum(1 for c in comps if c is not None and c.status == STAGE_OK)
     per_stage = (host_s + t_dev) / max(len(refs), 1)
@@ -205,7 +223,7 @@ def _run(refs: list[_StageRef], eng: Engine, opts: VerifyOptions, host_s: float,
     cancelled = 0
     for ref in refs:
         try:
-            r = _one(ref, eng, opts, fb, nv, nb, per_stage)
+            r = _one(ref, eng, opts, fb, nv, nb, per_stage, source)
         except PlanEqError as e:
             if errors != "collect":
                 raise
@@ -218,7 +236,7 @@ def _run(refs: list[_StageRef], eng: Engine, opts: VerifyOptions, host_s: float,
             break
     stats.update({"gpu_ms": round(gpu_ms, 4), "gpu_stages": n_gpu, "witnesses": opts.witnesses,
                   "device_s": round(t_dev, 6)})
-    if needs_gpu:
+    if needs_gpu and isinstance(source, EngineWitnesses):
         stats.update(eng.image_stats())
     return results, cancelled, stats
 
@@ -231,7 +249,7 @@ def _device(opts: VerifyOptions) -> int:
 
 
 def _one(ref: _StageRef, eng: Engine, opts: VerifyOptions, fb, nv, nb,
-         per_stage: float) -> StageResult:
+         per_stage: float, source=None) -> StageResult:
     comp = ref.comp
     if comp is None:
         ref.lowered()  # the host lowering raises the reference's exception
@@ -264,7 +282,7 @@ def _one(ref: _StageRef, eng: Engine, opts: VerifyOptions, fb, nv, nb,
         r.failing_witnesses = int(nb[i])
         r.false_equiv_log2 = bound_log2(comp.degree, int(nv[i]))
         if int(fb[i]) != 0xFFFFFFFFFFFFFFFF:
-            r.status, r.detail, r.note = _confirm(eng, ref, comp, int(fb[i]), opts.seed)
+            r.status, r.detail, r.note = _confirm(eng, ref, comp, int(fb[i]), opts.seed, source)
         elif int(nv[i]) == 0:
             r.status = "unknown"
             r.note = "no witness kept every denominator nonzero"
@@ -304,7 +322,7 @@ def _raiser(exc: BaseException):
 
 def discharge_native(nplan, opts: VerifyOptions, engine: Engine | None = None,
                      which: list[int] | None = None, indices=None,
-                     errors: str = "raise") -> tuple[list, int, dict]:
+                     errors: str = "raise", source=None) -> tuple[list, int, dict]:
     """Run the stages of a NativePlan (all, or the listed indices) through the
     witness engine: lowering and compilation in C++ on host threads.
     `indices`: engine indices of every plan stage already queued into
@@ -328,10 +346,11 @@ def discharge_native(nplan, opts: VerifyOptions, engine: Engine | None = None,
                 if owner is None:
                     owner = shard_owner(plan, entry_order(plan))
                 return lower_stage(plan, nplan.stage(i), owner, opts.seed)
-            refs.append(_StageRef(targets[i], lower, eng.stage_lazy(k) if k >= 0 else None))
+            refs.append(_StageRef(targets[i], lower, eng.stage_lazy(k) if k >= 0 else None,
+                                  stage=i))
         t_add = time.perf_counter() - t0
         stats = {"host_path": "native", "lower_s": round(t_add, 6)}
-        return _run(refs, eng, opts, t_add, stats, errors)
+        return _run(refs, eng, opts, t_add, stats, errors, source)
     finally:
         if own:
             eng.close()
