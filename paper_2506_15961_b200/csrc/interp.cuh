@@ -112,8 +112,16 @@ __device__ __forceinline__ uint32_t red64(uint64_t x) { return fred64(x); }
 // group. Every read unit (a header, one payload group, or one pair/term of a
 // wide DOT/SUM) is at most 33 records, so it spans at most two chunks.
 constexpr uint32_t RING_RECS = 64;
+#if !defined(PQW_PLAIN_RING) && !defined(PQW_MIRROR_RING)
+#define PQW_MIRROR_RING  // default (A/B r2m: 405B kernel 13.97 -> 13.30 ms)
+#endif
 #ifdef PQW_NO_RING
 constexpr uint32_t RING_BYTES = 0;
+#elif defined(PQW_MIRROR_RING)
+// chunks landing at ring positions 0..31 are also copied to 64..95, so every
+// read unit (<= 33 records) is contiguous in shared memory: one address per
+// group, record offsets become load immediates
+constexpr uint32_t RING_BYTES = (RING_RECS + 32) * 16;
 #else
 constexpr uint32_t RING_BYTES = RING_RECS * 16;
 #endif
@@ -125,6 +133,11 @@ __device__ __noinline__ uint2 ring_refill(const uint4* src, uint32_t base, uint3
     const uint32_t r = issued * 32u;
     const uint32_t dst = base + ((r & (RING_RECS - 1)) << 4) + lane4;
     const char* g = reinterpret_cast<const char*>(src + r) + lane4;
+#ifdef PQW_MIRROR_RING
+    if ((r & (RING_RECS - 1)) == 0)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + RING_RECS * 16), "l"(g)
+                   : "memory");
+#endif
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n\tcp.async.commit_group;" ::"r"(dst),
                  "l"(g)
                  : "memory");
@@ -149,6 +162,10 @@ struct CodeRing {
   uint32_t lane4;     // lane * 16
   uint32_t issued;    // chunks requested
   uint32_t ready;     // chunks known landed (and synced across the warp)
+#ifdef PQW_MIRROR_RING
+  uint32_t pbase = 0;  // first record of the current read unit
+  uint32_t gaddr = 0;  // its shared address
+#endif
 
   __device__ __forceinline__ void issue() {
     const uint32_t r = issued * 32u;
@@ -174,15 +191,24 @@ struct CodeRing {
       issued = st.x;
       ready = st.y;
     }
+#ifdef PQW_MIRROR_RING
+    pbase = p;
+    gaddr = base + ((p & (RING_RECS - 1)) << 4);
+#endif
   }
   __device__ __forceinline__ uint4 rec(uint32_t p) const {
 #ifdef PQW_NO_RING
     return __ldg(src + p);
 #endif
     uint4 v;
+#ifdef PQW_MIRROR_RING
+    const uint32_t a = gaddr + ((p - pbase) << 4);  // p - pbase: a constant of the unit
+#else
+    const uint32_t a = base + ((p & (RING_RECS - 1)) << 4);
+#endif
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "r"(base + ((p & (RING_RECS - 1)) << 4)));
+                 : "r"(a));
     return v;
   }
   __device__ __forceinline__ F8 rd8(uint32_t p) const {
