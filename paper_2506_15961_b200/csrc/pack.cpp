@@ -14,7 +14,10 @@
 #include <Python.h>
 #include <structmember.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstring>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -106,14 +109,25 @@ void put(std::string& out, T v) {
   out.append(reinterpret_cast<const char*>(&v), sizeof(T));
 }
 
-// interned attribute keys (no temporary string per lookup)
+// interned attribute keys (no temporary string per lookup), created at module
+// init so that worker threads only read the table
+const char* const KEYS[] = {"factor", "addend", "value", "shape", "exponent", "den_positive",
+                            "axis", "size", "perm", "vocab", "keepdims", "axes", "spec", "parts",
+                            "index", "group", "split_axis", "concat_axis", "enum"};
+constexpr size_t N_KEYS = sizeof(KEYS) / sizeof(KEYS[0]);
+PyObject* KEY_OBJS[N_KEYS];
+
+PyObject* key_obj_cached(const char* key) {
+  for (size_t i = 0; i < N_KEYS; ++i)
+    if (KEYS[i] == key || std::strcmp(KEYS[i], key) == 0) return KEY_OBJS[i];
+  return nullptr;
+}
 PyObject* key_obj(const char* key) {
-  static std::vector<std::pair<const char*, PyObject*>> cache;
-  for (auto& kv : cache)
-    if (kv.first == key) return kv.second;
-  PyObject* o = PyUnicode_InternFromString(key);
-  if (!o) throw Err{};
-  cache.push_back({key, o});
+  PyObject* o = key_obj_cached(key);
+  if (!o) {
+    PyErr_Format(PyExc_KeyError, "%s", key);
+    throw Err{};
+  }
   return o;
 }
 
@@ -233,8 +247,302 @@ void encode(int k, PyObject* a, PyObject* const_id, std::vector<long long>& w) {
   }
 }
 
+// ---- parallel fast path ------------------------------------------------------
+// For the common case -- graph.py's slotted Tensor/Node objects holding exact
+// small ints, compact-ASCII names, tuples/lists and dicts -- the per-object
+// work runs on host threads while the calling thread keeps the GIL and
+// waits: the workers only read (borrowed references, no refcount changes, no
+// Python code, no exceptions). Anything else makes the fast path decline and
+// the serial path below (which raises the proper Python errors) runs instead.
+// Rational attributes are numbered afterwards, serially, in node order.
+
+struct Cols {
+  std::string tn, ndim, dims, flags, ids, kind, nin, nout, ins, outs, nattr, attrs, device, seq;
+  std::vector<std::pair<size_t, PyObject*>> consts;  // (attr word index, value) to number
+};
+
+bool fast_str(PyObject* s, std::string& out) {
+  if (!s || !PyUnicode_Check(s) || !PyUnicode_IS_COMPACT_ASCII(s)) return false;
+  out.append((const char*)PyUnicode_DATA(s), (size_t)PyUnicode_GET_LENGTH(s));
+  out.push_back('\0');
+  return true;
+}
+bool fast_int(PyObject* o, long long& x) {
+  if (!o || !PyLong_CheckExact(o) || !PyUnstable_Long_IsCompact((PyLongObject*)o)) return false;
+  x = (long long)PyUnstable_Long_CompactValue((PyLongObject*)o);
+  return true;
+}
+bool fast_seq(PyObject* o, PyObject** & it, Py_ssize_t& n) {
+  if (o && PyTuple_CheckExact(o)) {
+    it = &PyTuple_GET_ITEM(o, 0);
+    n = PyTuple_GET_SIZE(o);
+    return true;
+  }
+  if (o && PyList_CheckExact(o)) {
+    it = PyList_GET_SIZE(o) ? &PyList_GET_ITEM(o, 0) : nullptr;
+    n = PyList_GET_SIZE(o);
+    return true;
+  }
+  return false;
+}
+bool fast_ints(PyObject* o, std::vector<long long>& w, bool with_len) {
+  PyObject** it;
+  Py_ssize_t n;
+  if (!fast_seq(o, it, n)) return false;
+  if (with_len) w.push_back(n);
+  for (Py_ssize_t i = 0; i < n; ++i) {
+    long long x;
+    if (!fast_int(it[i], x)) return false;
+    w.push_back(x);
+  }
+  return true;
+}
+PyObject* fast_get(PyObject* d, const char* key) {
+  return PyDict_GetItemWithError(d, key_obj_cached(key));  // str keys: a read-only lookup
+}
+bool fast_ascii_eq(PyObject* s, const char* lit) {
+  return s && PyUnicode_Check(s) && PyUnicode_IS_COMPACT_ASCII(s) &&
+         std::strcmp((const char*)PyUnicode_DATA(s), lit) == 0;
+}
+bool fast_truth(PyObject* a, const char* key, long long& t) {
+  PyObject* v = fast_get(a, key);
+  if (!v || v == Py_None || v == Py_False) {
+    t = 0;
+    return true;
+  }
+  if (v == Py_True) {
+    t = 1;
+    return true;
+  }
+  long long x;
+  if (!fast_int(v, x)) return false;
+  t = x != 0;
+  return true;
+}
+
+// fast_* form of encode(); rational attributes get a placeholder word and are
+// queued in `cq` (word index within this part's attrs, value)
+bool encode_fast(int k, PyObject* a, std::vector<long long>& w, size_t word0,
+                 std::vector<std::pair<size_t, PyObject*>>& cq) {
+  long long x;
+  auto req_int = [&](const char* key) {
+    long long v;
+    if (!fast_int(fast_get(a, key), v)) return false;
+    w.push_back(v);
+    return true;
+  };
+  auto cst = [&](const char* key) {
+    PyObject* v = fast_get(a, key);
+    if (!v) return false;
+    cq.push_back({word0 + w.size(), v});
+    w.push_back(0);
+    return true;
+  };
+  switch (k) {
+    case T_SCALE: return cst("factor");
+    case T_SHIFT: return cst("addend");
+    case T_FULL: return cst("value") && fast_ints(fast_get(a, "shape"), w, true);
+    case T_POW: {
+      PyObject* v = fast_get(a, "exponent");
+      if (!v) {
+        w.push_back(0);
+        return true;
+      }
+      if (!fast_int(v, x)) return false;
+      w.push_back(x);
+      return true;
+    }
+    case T_DIV:
+      if (!fast_truth(a, "den_positive", x)) return false;
+      w.push_back(x);
+      return true;
+    case T_SOFTMAX: {
+      PyObject* v = fast_get(a, "axis");
+      if (!v) {
+        w.push_back(-1);
+        return true;
+      }
+      if (!fast_int(v, x)) return false;
+      w.push_back(x);
+      return true;
+    }
+    case T_CREATE_MASK: return req_int("size");
+    case T_TRANSPOSE: return fast_ints(fast_get(a, "perm"), w, false);
+    case T_VIEW:
+    case T_EXPAND: return fast_ints(fast_get(a, "shape"), w, true);
+    case T_EMBEDDING_GRAD: return req_int("vocab");
+    case T_SUM:
+    case T_MEAN: {
+      if (!fast_truth(a, "keepdims", x)) return false;
+      w.push_back(x);
+      PyObject* axes = fast_get(a, "axes");
+      if (!axes || axes == Py_None) {
+        w.push_back(0);
+        return true;
+      }
+      w.push_back(1);
+      return fast_ints(axes, w, true);
+    }
+    case T_EINSUM: {
+      PyObject* sp = fast_get(a, "spec");
+      if (!sp || !PyUnicode_Check(sp) || !PyUnicode_IS_COMPACT_ASCII(sp)) return false;
+      const Py_ssize_t n = PyUnicode_GET_LENGTH(sp);
+      const char* c = (const char*)PyUnicode_DATA(sp);
+      w.push_back(n);
+      for (Py_ssize_t i = 0; i < n; ++i) w.push_back((unsigned char)c[i]);
+      return true;
+    }
+    case T_CHUNK: return req_int("axis") && req_int("parts") && req_int("index");
+    case T_ALL_REDUCE:
+    case T_ALL_GATHER:
+    case T_REDUCE_SCATTER:
+    case T_ALL_TO_ALL: {
+      PyObject** it;
+      Py_ssize_t g;
+      if (!fast_seq(fast_get(a, "group"), it, g)) return false;
+      w.push_back(g);
+      if (k == T_ALL_GATHER || k == T_REDUCE_SCATTER) return req_int("axis");
+      if (k == T_ALL_TO_ALL) return req_int("split_axis") && req_int("concat_axis");
+      return true;
+    }
+    default:
+      return true;
+  }
+}
+
 PyObject* bytes_of(const std::string& s) {
   return PyBytes_FromStringAndSize(s.data(), (Py_ssize_t)s.size());
+}
+
+struct KindTable {
+  std::vector<std::pair<std::string, int>> kv;
+  int find(PyObject* s) const {
+    if (!s || !PyUnicode_Check(s) || !PyUnicode_IS_COMPACT_ASCII(s)) return -2;
+    const char* c = (const char*)PyUnicode_DATA(s);
+    for (auto& e : kv)
+      if (e.first == c) return e.second;
+    return -1;
+  }
+};
+
+template <class T>
+void putv(std::string& out, T v) {
+  out.append(reinterpret_cast<const char*>(&v), sizeof(T));
+}
+
+bool pack_fast(PyObject* tensors, PyObject* const* nodes, Py_ssize_t nn, const KindTable& kinds,
+               Cols& out) {
+  std::vector<std::pair<PyObject*, PyObject*>> tv;
+  tv.reserve((size_t)PyDict_GET_SIZE(tensors));
+  {
+    Py_ssize_t pos = 0;
+    PyObject *k, *v;
+    while (PyDict_Next(tensors, &pos, &k, &v)) tv.push_back({k, v});
+  }
+  PyObject* const tnames[3] = {S_shape, S_dtype, S_meta};
+  PyObject* const nnames[7] = {S_id, S_kind, S_inputs, S_outputs, S_attrs, S_device, S_seq};
+  Fields tf, nf;
+  if (!tv.empty()) {
+    tf.bind(tv[0].second, tnames, 3);
+    for (auto o : tf.off)
+      if (o < 0) return false;
+  }
+  if (nn) {
+    nf.bind(nodes[0], nnames, 7);
+    for (auto o : nf.off)
+      if (o < 0) return false;
+  }
+  auto slot = [](PyObject* obj, const Fields& f, int i) {
+    return *reinterpret_cast<PyObject**>(reinterpret_cast<char*>(obj) + f.off[i]);
+  };
+  unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const size_t work = tv.size() + (size_t)nn;
+  if (work < 50000) nt = 1;
+  std::vector<Cols> parts(nt);
+  std::vector<char> ok(nt, 1);
+  auto run = [&](unsigned t) {
+    Cols& c = parts[t];
+    const size_t t0 = tv.size() * t / nt, t1 = tv.size() * (t + 1) / nt;
+    for (size_t i = t0; i < t1 && ok[t]; ++i) {
+      PyObject* o = tv[i].second;
+      if (Py_TYPE(o) != tf.type || !fast_str(tv[i].first, c.tn)) {
+        ok[t] = 0;
+        break;
+      }
+      std::vector<long long> sh;
+      if (!fast_ints(slot(o, tf, 0), sh, false)) {
+        ok[t] = 0;
+        break;
+      }
+      putv<int32_t>(c.ndim, (int32_t)sh.size());
+      for (long long d : sh) putv<int64_t>(c.dims, d);
+      uint8_t fl = 0;
+      if (fast_ascii_eq(slot(o, tf, 1), "int")) {
+        fl = 1;
+        PyObject* meta = slot(o, tf, 2);
+        if (!meta || !PyDict_CheckExact(meta)) {
+          ok[t] = 0;
+          break;
+        }
+        if (fast_ascii_eq(fast_get(meta, "enum"), "position")) fl |= 2;
+      }
+      c.flags.push_back((char)fl);
+    }
+    const size_t n0 = (size_t)nn * t / nt, n1 = (size_t)nn * (t + 1) / nt;
+    std::vector<long long> w;
+    size_t words = 0;
+    for (size_t i = n0; i < n1 && ok[t]; ++i) {
+      PyObject* n = nodes[i];
+      bool good = Py_TYPE(n) == nf.type && fast_str(slot(n, nf, 0), c.ids);
+      const int k = good ? kinds.find(slot(n, nf, 1)) : -2;
+      good = good && k >= -1;
+      PyObject** it = nullptr;
+      Py_ssize_t ni = 0, no = 0;
+      good = good && fast_seq(slot(n, nf, 2), it, ni);
+      for (Py_ssize_t j = 0; good && j < ni; ++j) good = fast_str(it[j], c.ins);
+      good = good && fast_seq(slot(n, nf, 3), it, no);
+      for (Py_ssize_t j = 0; good && j < no; ++j) good = fast_str(it[j], c.outs);
+      w.clear();
+      if (good && has_attrs(k)) {
+        PyObject* at = slot(n, nf, 4);
+        good = at && PyDict_CheckExact(at) && encode_fast(k, at, w, words, c.consts);
+      }
+      long long dv = -1, sq = 0;
+      PyObject* dvo = good ? slot(n, nf, 5) : nullptr;
+      good = good && dvo && (dvo == Py_None || fast_int(dvo, dv));
+      good = good && fast_int(slot(n, nf, 6), sq);
+      if (!good) {
+        ok[t] = 0;
+        break;
+      }
+      putv<int32_t>(c.kind, k);
+      putv<int32_t>(c.nin, (int32_t)ni);
+      putv<int32_t>(c.nout, (int32_t)no);
+      putv<int32_t>(c.nattr, (int32_t)w.size());
+      for (long long x : w) putv<int64_t>(c.attrs, x);
+      words += w.size();
+      putv<int32_t>(c.device, (int32_t)dv);
+      putv<int64_t>(c.seq, sq);
+    }
+  };
+  {
+    std::vector<std::thread> pool;
+    for (unsigned t = 1; t < nt; ++t) pool.emplace_back(run, t);
+    run(0);
+    for (auto& th : pool) th.join();
+  }
+  for (char o : ok)
+    if (!o) return false;
+  size_t words = 0;
+  for (auto& c : parts) {
+    out.tn += c.tn; out.ndim += c.ndim; out.dims += c.dims; out.flags += c.flags;
+    out.ids += c.ids; out.kind += c.kind; out.nin += c.nin; out.nout += c.nout;
+    out.ins += c.ins; out.outs += c.outs; out.nattr += c.nattr; out.attrs += c.attrs;
+    out.device += c.device; out.seq += c.seq;
+    for (auto& q : c.consts) out.consts.push_back({words + q.first, q.second});
+    words += c.attrs.size() / sizeof(int64_t);
+  }
+  return true;
 }
 
 // pack_graph(graph, opcodes: dict[str, int], const_id) -> dict[str, bytes]
@@ -243,14 +551,50 @@ PyObject* pack_graph(PyObject*, PyObject* args) {
   if (!PyArg_ParseTuple(args, "OO!O", &g, &PyDict_Type, &opcodes, &const_id)) return nullptr;
   try {
     std::string tn, ndim, dims, flags;
+    std::string ids, kind, nin, nout, ins, outs, nattr, attrs, device, seq;
     Ref tensors(PyObject_GetAttr(g, S_tensors));
     if (!PyDict_Check(tensors.p)) {
       PyErr_SetString(PyExc_TypeError, "graph.tensors is not a dict");
       throw Err{};
     }
+    Ref nodes_o(PyObject_GetAttr(g, S_nodes));
+    Ref nodes(PySequence_Fast(nodes_o.p, "graph.nodes"));
+    const Py_ssize_t nn = PySequence_Fast_GET_SIZE(nodes.p);
+    PyObject** nv = PySequence_Fast_ITEMS(nodes.p);
+    long long nt = PyDict_GET_SIZE(tensors.p);
+    bool fast = false;
+    if (!getenv("PQW_PACK_SERIAL")) {
+      KindTable kt;
+      Py_ssize_t pos = 0;
+      PyObject *kk, *vv;
+      bool tab_ok = true;
+      while (PyDict_Next(opcodes, &pos, &kk, &vv)) {
+        long long c;
+        if (!PyUnicode_Check(kk) || !PyUnicode_IS_COMPACT_ASCII(kk) || !fast_int(vv, c)) {
+          tab_ok = false;
+          break;
+        }
+        kt.kv.push_back({std::string((const char*)PyUnicode_DATA(kk)), (int)c});
+      }
+      Cols c;
+      if (tab_ok && pack_fast(tensors.p, nv, nn, kt, c)) {
+        fast = true;
+        tn.swap(c.tn); ndim.swap(c.ndim); dims.swap(c.dims); flags.swap(c.flags);
+        ids.swap(c.ids); kind.swap(c.kind); nin.swap(c.nin); nout.swap(c.nout);
+        ins.swap(c.ins); outs.swap(c.outs); nattr.swap(c.nattr); attrs.swap(c.attrs);
+        device.swap(c.device); seq.swap(c.seq);
+        for (auto& q : c.consts) {  // rational attributes, numbered in node order
+          Ref r(PyObject_CallOneArg(const_id, q.second));
+          const int64_t id = as_int(r.p);
+          std::memcpy(&attrs[q.first * sizeof(int64_t)], &id, sizeof(id));
+        }
+      }
+    }
+    if (!fast) {
+    tn.clear(); ndim.clear(); dims.clear(); flags.clear();
+    nt = 0;
     Py_ssize_t pos = 0;
     PyObject *key, *t;
-    long long nt = 0;
     PyObject* const tnames[3] = {S_shape, S_dtype, S_meta};
     Fields tf;
     while (PyDict_Next(tensors.p, &pos, &key, &t)) {
@@ -273,11 +617,6 @@ PyObject* pack_graph(PyObject*, PyObject* args) {
       flags.push_back((char)fl);
       ++nt;
     }
-    Ref nodes_o(PyObject_GetAttr(g, S_nodes));
-    Ref nodes(PySequence_Fast(nodes_o.p, "graph.nodes"));
-    const Py_ssize_t nn = PySequence_Fast_GET_SIZE(nodes.p);
-    PyObject** nv = PySequence_Fast_ITEMS(nodes.p);
-    std::string ids, kind, nin, nout, ins, outs, nattr, attrs, device, seq;
     std::vector<long long> w;
     PyObject* const nnames[7] = {S_id, S_kind, S_inputs, S_outputs, S_attrs, S_device, S_seq};
     Fields nf;
@@ -315,6 +654,7 @@ PyObject* pack_graph(PyObject*, PyObject* args) {
       Ref sq(field(n, nf, 6, nnames, 7));
       put<int64_t>(seq, as_int(sq.p));
     }
+    }  // serial path
     std::string gin;
     Ref gi(PyObject_GetAttr(g, S_inputs_g));
     Ref gif(PySequence_Fast(gi.p, "graph.inputs"));
@@ -376,5 +716,10 @@ PyMODINIT_FUNC PyInit__pqw_pack(void) {
   S_tensors = PyUnicode_InternFromString("tensors");
   S_nodes = PyUnicode_InternFromString("nodes");
   S_inputs_g = PyUnicode_InternFromString("inputs");
+  for (size_t i = 0; i < N_KEYS; ++i) {
+    KEY_OBJS[i] = PyUnicode_InternFromString(KEYS[i]);
+    if (!KEY_OBJS[i]) return nullptr;
+    (void)PyObject_Hash(KEY_OBJS[i]);  // cache the hash before any worker reads it
+  }
   return PyModule_Create(&module);
 }

@@ -188,3 +188,24 @@ def test_cpp_packer_matches_python_packer(lib, name, rel):
                 assert a == b, (name, k)
             else:
                 assert np.array_equal(np.asarray(a), np.asarray(b)), (name, k)
+
+
+def test_parallel_packer_matches_serial_packer(lib):
+    """The threaded fast path of csrc/pack.cpp (large graphs) emits exactly the
+    serial path's columns and constant numbering."""
+    from paper_2506_15961_b200 import native as N
+    from paper_2506_15961_b200.stages import OPCODE
+    from paper_2506_15961_b200.workloads import get_workload
+    ext = N._ext()
+    _d, plan = get_workload("llama3-8b-tp4pp2dp2-sp")
+    assert len(plan.parallel.nodes) + len(plan.parallel.tensors) > 50000  # threads engage
+    for g in (plan.logical, plan.parallel):
+        c1, c2 = N._Consts(), N._Consts()
+        fast = ext.pack_graph(g, OPCODE, c1)
+        os.environ["PQW_PACK_SERIAL"] = "1"
+        try:
+            serial = ext.pack_graph(g, OPCODE, c2)
+        finally:
+            del os.environ["PQW_PACK_SERIAL"]
+        assert fast == serial
+        assert c1.triples == c2.triples
