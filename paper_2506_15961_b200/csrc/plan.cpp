@@ -587,8 +587,8 @@ bool validate_graph(const GraphData& g, std::string& why) {
   }
   // dangling inputs (graph.py topo_sort) and cycles
   const size_t n = g.nn();
-  std::vector<int32_t> indeg(n, 0);
-  std::vector<std::vector<int32_t>> succ(n);
+  // successor lists in CSR form (no per-node allocation)
+  std::vector<int32_t> indeg(n, 0), soff(n + 1, 0);
   for (size_t v = 0; v < n; ++v)
     for (int64_t j = g.in_off[v]; j < g.in_off[v + 1]; ++j) {
       const int32_t t = g.ins[j];
@@ -599,9 +599,17 @@ bool validate_graph(const GraphData& g, std::string& why) {
         return false;
       }
       indeg[v]++;
-      succ[src].push_back((int32_t)v);
+      soff[(size_t)src + 1]++;
     }
+  for (size_t v = 0; v < n; ++v) soff[v + 1] += soff[v];
   {
+    std::vector<int32_t> succ((size_t)soff[n]), fill(soff.begin(), soff.end() - 1);
+    for (size_t v = 0; v < n; ++v)
+      for (int64_t j = g.in_off[v]; j < g.in_off[v + 1]; ++j) {
+        const int32_t t = g.ins[j];
+        if (g.is_input[t]) continue;
+        succ[(size_t)fill[(size_t)g.producer[t]]++] = (int32_t)v;
+      }
     std::vector<int32_t> q;
     for (size_t v = 0; v < n; ++v)
       if (!indeg[v]) q.push_back((int32_t)v);
@@ -610,14 +618,19 @@ bool validate_graph(const GraphData& g, std::string& why) {
       int32_t v = q.back();
       q.pop_back();
       seen++;
-      for (int32_t s : succ[v])
-        if (--indeg[s] == 0) q.push_back(s);
+      for (int32_t i = soff[(size_t)v]; i < soff[(size_t)v + 1]; ++i)
+        if (--indeg[(size_t)succ[(size_t)i]] == 0) q.push_back(succ[(size_t)i]);
     }
     if (seen != n) {
       why = "cycle";
       return false;
     }
   }
+  auto same_shape = [&](int32_t a, int32_t b) {
+    const int64_t la = g.dim_off[a + 1] - g.dim_off[a], lb = g.dim_off[b + 1] - g.dim_off[b];
+    return la == lb && std::equal(g.dims.begin() + g.dim_off[a], g.dims.begin() + g.dim_off[a + 1],
+                                  g.dims.begin() + g.dim_off[b]);
+  };
   std::atomic<bool> ok{true};
   std::mutex mu;
   const size_t chunk = 4096;
@@ -625,6 +638,17 @@ bool validate_graph(const GraphData& g, std::string& why) {
     std::vector<Shape> ins;
     for (size_t v = c * chunk; v < std::min(n, (c + 1) * chunk) && ok.load(std::memory_order_relaxed); ++v) {
       const int k = g.kind[v];
+      const int64_t ni = g.in_off[v + 1] - g.in_off[v], nov = g.out_off[v + 1] - g.out_off[v];
+      // the common kinds without allocation: outputs equal the (shared) input shape
+      if ((is_elementwise2(k) && ni == 2 &&
+           same_shape(g.ins[g.in_off[v]], g.ins[g.in_off[v] + 1])) ||
+          (is_unary(k) && ni == 1 &&
+           (k != PQW_T_POW || (g.attr_off[v + 1] > g.attr_off[v] && g.attrs[g.attr_off[v]] >= 1)))) {
+        bool good = true;
+        for (int64_t j = 0; j < nov && j < 1; ++j)
+          good = good && same_shape(g.outs[g.out_off[v] + j], g.ins[g.in_off[v]]);
+        if (good) continue;
+      }
       ins.clear();
       for (int64_t j = g.in_off[v]; j < g.in_off[v + 1]; ++j) ins.push_back(g.shape_vec(g.ins[j]));
       bool good = true;
