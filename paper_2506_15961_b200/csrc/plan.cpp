@@ -849,30 +849,65 @@ struct Program {
   std::vector<uint64_t> var_keys;
 };
 
+// tensor index -> local value, with O(1) reset: generation-stamped arrays
+// that live per host thread across the stages it lowers
+struct StampMap {
+  std::vector<uint32_t> stamp;
+  std::vector<int32_t> val;
+  uint32_t gen = 0;
+  void begin(size_t n) {
+    if (stamp.size() < n) {
+      stamp.assign(n, 0);
+      val.assign(n, -1);
+      gen = 0;
+    }
+    if (++gen == 0) {
+      std::fill(stamp.begin(), stamp.end(), 0);
+      gen = 1;
+    }
+  }
+  int32_t get(int32_t k) const { return stamp[(size_t)k] == gen ? val[(size_t)k] : -1; }
+  void set(int32_t k, int32_t v) {
+    stamp[(size_t)k] = gen;
+    val[(size_t)k] = v;
+  }
+};
+
+struct LowerScratch {
+  StampMap lt, pt, boxes, prod_l, prod_p;
+};
+
 struct Lowerer {
   const pqw_plan* p = nullptr;
   uint64_t seed = 0;
-  std::vector<Shape> shapes;
+  std::vector<int64_t> sdims;          // local tensor shapes, flat
+  std::vector<int32_t> soff{0};
   std::vector<int32_t> ops;
   int32_t n_ops = 0;
   std::vector<int64_t> consts;
   std::unordered_map<int64_t, int32_t> const_idx;  // plan const id -> stage const index
   std::vector<uint64_t> var_keys;
   int64_t n_vars = 0;
-  std::unordered_map<int32_t, int32_t> lt, pt;      // "L:"/"P:" keys -> local tensor
-  std::unordered_map<int32_t, int32_t> boxes;       // logical tensor -> local tensor
+  StampMap* lt_ = nullptr;             // "L:" keys -> local tensor
+  StampMap* pt_ = nullptr;             // "P:" keys -> local tensor
+  StampMap* boxes_ = nullptr;          // logical tensor -> local tensor
+  std::vector<int32_t> abuf;           // attribute words of the node being emitted
 
-  int32_t temp(const Shape& s) {
-    shapes.push_back(s);
-    return (int32_t)shapes.size() - 1;
+  int32_t temp(const int64_t* d, size_t n) {
+    sdims.insert(sdims.end(), d, d + n);
+    soff.push_back((int32_t)sdims.size());
+    return (int32_t)soff.size() - 2;
   }
-  int32_t tensor(std::unordered_map<int32_t, int32_t>& m, int32_t key, const Shape& s) {
-    auto it = m.find(key);
-    if (it != m.end()) return it->second;
-    const int32_t idx = temp(s);
-    m.emplace(key, idx);
+  int32_t temp(const Shape& s) { return temp(s.data(), s.size()); }
+  size_t rank(int32_t t) const { return (size_t)(soff[(size_t)t + 1] - soff[(size_t)t]); }
+  int32_t tensor(StampMap& m, int32_t key, const int64_t* d, size_t n) {
+    const int32_t got = m.get(key);
+    if (got >= 0) return got;
+    const int32_t idx = temp(d, n);
+    m.set(key, idx);
     return idx;
   }
+  int32_t tensor(StampMap& m, int32_t key, const Shape& s) { return tensor(m, key, s.data(), s.size()); }
   int32_t cst(int64_t cid) {
     auto it = const_idx.find(cid);
     if (it != const_idx.end()) return it->second;
@@ -905,8 +940,8 @@ struct Lowerer {
     return out;
   }
   int32_t box_of(int32_t tid) {
-    auto it = boxes.find(tid);
-    if (it != boxes.end()) return it->second;
+    const int32_t got = boxes_->get(tid);
+    if (got >= 0) return got;
     const GraphData& L = p->L;
     const Shape s = L.shape_vec(tid);
     int32_t idx;
@@ -924,7 +959,7 @@ struct Lowerer {
     } else {
       idx = vars_for("v.", L.tname[tid], s);
     }
-    boxes.emplace(tid, idx);
+    boxes_->set(tid, idx);
     return idx;
   }
 
@@ -938,7 +973,7 @@ struct Lowerer {
     };
     auto rank0 = [&]() -> int64_t {
       if (in.empty()) throw PlanError("no input");
-      return (int64_t)shapes[in[0]].size();
+      return (int64_t)rank(in[0]);
     };
     switch (k) {
       case PQW_T_SCALE:
@@ -1007,8 +1042,7 @@ struct Lowerer {
     }
   }
 
-  void run_nodes(const GraphData& g, const std::vector<int32_t>& nodes,
-                 std::unordered_map<int32_t, int32_t>& m, int side) {
+  void run_nodes(const GraphData& g, const std::vector<int32_t>& nodes, StampMap& m, int side) {
     emit(PQW_T_SIDE, {}, {}, {side});
     std::vector<int32_t> in, out;
     for (int32_t v : nodes) {
@@ -1016,12 +1050,15 @@ struct Lowerer {
       in.clear();
       out.clear();
       for (int64_t j = g.in_off[v]; j < g.in_off[v + 1]; ++j) {
-        auto it = m.find(g.ins[j]);
-        if (it == m.end()) throw PlanError("unbound input");
-        in.push_back(it->second);
+        const int32_t got = m.get(g.ins[j]);
+        if (got < 0) throw PlanError("unbound input");
+        in.push_back(got);
       }
-      for (int64_t j = g.out_off[v]; j < g.out_off[v + 1]; ++j)
-        out.push_back(tensor(m, g.outs[j], g.shape_vec(g.outs[j])));
+      for (int64_t j = g.out_off[v]; j < g.out_off[v + 1]; ++j) {
+        const int32_t t = g.outs[j];
+        out.push_back(tensor(m, t, g.dims.data() + g.dim_off[t],
+                             (size_t)(g.dim_off[t + 1] - g.dim_off[t])));
+      }
       emit(g.kind[v], in, out, node_attrs(g, v, in));
     }
   }
@@ -1055,21 +1092,27 @@ struct Lowerer {
 
   Program lower(const StageRec& st) {
     const GraphData &L = p->L, &P = p->P;
-    {
-      std::vector<char> produced;
-      std::unordered_map<int32_t, char> prod_l;
-      for (int32_t v : st.lnodes)
-        for (int64_t j = L.out_off[v]; j < L.out_off[v + 1]; ++j) prod_l[L.outs[j]] = 1;
-      for (int32_t t : st.l_inputs)
-        if (!prod_l.count(t)) lt[t] = box_of(t);
-    }
+    static thread_local LowerScratch scratch;
+    scratch.lt.begin(L.nt());
+    scratch.boxes.begin(L.nt());
+    scratch.prod_l.begin(L.nt());
+    scratch.pt.begin(P.nt());
+    scratch.prod_p.begin(P.nt());
+    StampMap &lt = scratch.lt, &pt = scratch.pt, &prod_l = scratch.prod_l,
+             &prod_p = scratch.prod_p;
+    lt_ = &lt;
+    pt_ = &pt;
+    boxes_ = &scratch.boxes;
+    for (int32_t v : st.lnodes)
+      for (int64_t j = L.out_off[v]; j < L.out_off[v + 1]; ++j) prod_l.set(L.outs[j], 1);
+    for (int32_t t : st.l_inputs)
+      if (prod_l.get(t) < 0) lt.set(t, box_of(t));
     run_nodes(L, st.lnodes, lt, 0);
-    std::unordered_map<int32_t, char> prod_p;
     for (int32_t v : st.pnodes)
-      for (int64_t j = P.out_off[v]; j < P.out_off[v + 1]; ++j) prod_p[P.outs[j]] = 1;
+      for (int64_t j = P.out_off[v]; j < P.out_off[v + 1]; ++j) prod_p.set(P.outs[j], 1);
     std::vector<int32_t> done;
     for (int32_t s : st.p_inputs) {
-      if (prod_p.count(s)) continue;
+      if (prod_p.get(s) >= 0) continue;
       const int32_t ei = p->owner[s];
       if (ei < 0) throw PlanError("shard without owner");
       if (std::find(done.begin(), done.end(), ei) != done.end()) continue;
@@ -1089,7 +1132,7 @@ struct Lowerer {
         std::vector<int32_t> frees;
         for (size_t i = 0; i + 1 < g.second.size(); ++i) {
           const int32_t v = vars_for("ps.", P.tname[g.second[i]], ext);
-          pt[g.second[i]] = v;
+          pt.set(g.second[i], v);
           frees.push_back(v);
         }
         const int32_t sl = temp(ext);
@@ -1100,21 +1143,20 @@ struct Lowerer {
           ins.insert(ins.end(), frees.begin(), frees.end());
           emit(PQW_T_RESID, ins, {last}, {});
         } else {
-          pt[g.second.back()] = sl;
+          pt.set(g.second.back(), sl);
         }
       }
     }
     run_nodes(P, st.pnodes, pt, 1);
     // obligations (stages.py:316-340 order)
     const Entry& e = p->entries[st.entry];
-    auto tit = lt.find(st.target);
-    if (tit == lt.end()) throw PlanError("target not computed");
-    const int32_t tgt = tit->second;
+    const int32_t tgt = lt.get(st.target);
+    if (tgt < 0) throw PlanError("target not computed");
     int32_t n_obl = 0;
     auto shard_tensor = [&](int32_t s) {
-      auto it = pt.find(s);
-      if (it == pt.end()) throw PlanError("shard never computed");
-      return it->second;
+      const int32_t got = pt.get(s);
+      if (got < 0) throw PlanError("shard never computed");
+      return got;
     };
     if (e.mode == 0) {
       for (size_t i = 0; i < e.shards.size(); ++i) {
@@ -1139,10 +1181,12 @@ struct Lowerer {
       }
     }
     Program out;
-    out.ir = {IR_MAGIC, (int32_t)shapes.size(), n_ops, n_obl};
-    for (auto& s : shapes) {
-      out.ir.push_back((int32_t)s.size());
-      for (auto d : s) out.ir.push_back((int32_t)d);
+    const size_t nts = soff.size() - 1;
+    out.ir.reserve(4 + nts + sdims.size() + ops.size());
+    out.ir = {IR_MAGIC, (int32_t)nts, n_ops, n_obl};
+    for (size_t t = 0; t < nts; ++t) {
+      out.ir.push_back((int32_t)(soff[t + 1] - soff[t]));
+      for (int32_t i = soff[t]; i < soff[t + 1]; ++i) out.ir.push_back((int32_t)sdims[(size_t)i]);
     }
     out.ir.insert(out.ir.end(), ops.begin(), ops.end());
     out.consts = std::move(consts);
