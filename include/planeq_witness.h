@@ -319,6 +319,12 @@ void pqw_plan_destroy(pqw_plan* p);
  * (validate_concrete). PQW_EPLAN when anything is off. */
 int pqw_plan_validate(pqw_plan* p);
 
+/* validate_lineage (graph.py:227-252) as counts: out[0] = hard problems
+ * (unknown tensors, bad mode, shard shape != range extents), out[1] = entries
+ * whose shard ranges do not tile the logical shape. Any nonzero: the host's
+ * validate_lineage produces the reference's messages. */
+int pqw_plan_check_lineage(pqw_plan* p, int64_t out[2]);
+
 /* build_stages: out[0] = stages, out[1] = uncovered logical nodes, out[2] =
  * uncovered parallel nodes. PQW_EPLAN when stage construction would raise
  * (it does not require pqw_plan_validate: the reference builds the stages of

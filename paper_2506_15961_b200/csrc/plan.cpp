@@ -1263,6 +1263,66 @@ int pqw_plan_validate(pqw_plan* p) {
   return PQW_OK;
 }
 
+int pqw_plan_check_lineage(pqw_plan* p, int64_t out[2]) {
+  if (!p || !out) return pfail(PQW_EINVAL, "null argument");
+  int64_t hard = 0, tiling = 0;
+  for (const auto& e : p->entries) {
+    if (e.logical < 0) {
+      hard++;
+      continue;
+    }
+    if (e.mode > 1) hard++;
+    const auto shape = p->L.shape_vec(e.logical);
+    for (size_t i = 0; i < e.shards.size(); ++i) {
+      if (e.shards[i] < 0) {
+        hard++;
+        continue;
+      }
+      const auto ps = p->P.shape_vec(e.shards[i]);
+      bool same = ps.size() == e.ranges[i].size();
+      for (size_t a = 0; same && a < ps.size(); ++a)
+        same = ps[a] == e.ranges[i][a].second - e.ranges[i][a].first;
+      if (!same) hard++;
+    }
+    // graph.py entry_tiles_exactly: distinct boxes in bounds, disjoint, covering
+    std::vector<const std::vector<std::pair<int64_t, int64_t>>*> boxes;
+    for (const auto& r : e.ranges) {
+      bool seen = false;
+      for (auto* b : boxes) seen = seen || *b == r;
+      if (!seen) boxes.push_back(&r);
+    }
+    bool ok = true;
+    int64_t vol = 0, total = 1;
+    for (int64_t d : shape) total *= d;
+    for (auto* b : boxes) {
+      if (b->size() != shape.size()) {
+        ok = false;
+        break;
+      }
+      int64_t v = 1;
+      for (size_t a = 0; a < shape.size(); ++a) {
+        const auto& [lo, hi] = (*b)[a];
+        if (!(0 <= lo && lo < hi && hi <= shape[a])) ok = false;
+        v *= hi - lo;
+      }
+      vol += v;
+    }
+    if (ok && vol != total) ok = false;
+    for (size_t i = 0; ok && i < boxes.size(); ++i)
+      for (size_t j = i + 1; ok && j < boxes.size(); ++j) {
+        bool overlap = true;
+        for (size_t a = 0; a < shape.size(); ++a)
+          overlap = overlap && (*boxes[i])[a].first < (*boxes[j])[a].second &&
+                    (*boxes[j])[a].first < (*boxes[i])[a].second;
+        if (overlap) ok = false;
+      }
+    if (!ok) tiling++;
+  }
+  out[0] = hard;
+  out[1] = tiling;
+  return PQW_OK;
+}
+
 int pqw_plan_build_stages(pqw_plan* p, int64_t out[3]) {
   if (!p || !out) return pfail(PQW_EINVAL, "null argument");
   if (!p->L.resolved || !p->P.resolved || !p->lineage_ok || !p->L.unique_producers ||

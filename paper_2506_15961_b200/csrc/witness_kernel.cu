@@ -521,14 +521,17 @@ int pqw_upload(pqw_engine* e) {
   if (descs.empty()) descs.push_back({0, 0, 0, 0});
   if (work.empty()) work.push_back(0);
 
-  cudaDeviceProp prop;
-  CU(cudaGetDeviceProperties(&prop, e->device));
+  // two attributes, not cudaGetDeviceProperties (which queries everything and
+  // costs tens of milliseconds per call)
+  int smem_optin = 0, n_sm = 0;
+  CU(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
+  CU(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, e->device));
   // the shared value file is as large as the largest stage needs (at most the
   // capacity the stages were compiled for); spills live in per-CTA scratch
   const size_t slot_bytes = pqw::SLOT_BYTES;
   e->smem_slots = std::max<uint32_t>(e->max_slots, 1);
   const size_t smem_bytes = (size_t)e->smem_slots * slot_bytes + (size_t)e->n_warps * pqw::RING_BYTES;
-  if (smem_bytes + 512 > prop.sharedMemPerBlockOptin)
+  if (smem_bytes + 512 > (size_t)smem_optin)
     return fail(PQW_EINVAL, "value file does not fit in shared memory");
   int per_sm = 0;
   auto setup = [&](auto kern_false, auto kern_true, int threads) -> cudaError_t {
@@ -548,7 +551,7 @@ int pqw_upload(pqw_engine* e) {
   else
     CU(setup(pqw::eval_kernel<8, false>, pqw::eval_kernel<8, true>, 8 * 32));
   if (per_sm < 1) per_sm = 1;
-  e->grid = (uint32_t)(prop.multiProcessorCount * per_sm);
+  e->grid = (uint32_t)(n_sm * per_sm);
 
   CU(cudaMalloc(&e->d_code, code.size() * sizeof(pqw_ins)));
   CU(cudaMemcpy(e->d_code, code.data(), code.size() * sizeof(pqw_ins), cudaMemcpyHostToDevice));

@@ -43,7 +43,8 @@ EXPORTS = ("pqw_abi_version", "pqw_last_error", "pqw_device_count", "pqw_engine_
            "pqw_last_launch_ms", "pqw_image_stats", "pqw_peak_fieldops", "pqw_stage_select",
            "pqw_stage_cost", "pqw_confirm",
            # native plan core (native.py)
-           "pqw_plan_create", "pqw_plan_destroy", "pqw_plan_validate", "pqw_plan_build_stages",
+           "pqw_plan_create", "pqw_plan_destroy", "pqw_plan_validate", "pqw_plan_check_lineage",
+           "pqw_plan_build_stages",
            "pqw_plan_stage_target", "pqw_plan_stage_nodes", "pqw_plan_uncovered",
            "pqw_plan_add_stages", "pqw_plan_stage_program")
 

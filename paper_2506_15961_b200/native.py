@@ -79,6 +79,8 @@ def _bind(lib):
     lib.pqw_plan_destroy.restype = None
     lib.pqw_plan_validate.argtypes = [vp]
     lib.pqw_plan_validate.restype = C.c_int
+    lib.pqw_plan_check_lineage.argtypes = [vp, _I64P]
+    lib.pqw_plan_check_lineage.restype = C.c_int
     lib.pqw_plan_build_stages.argtypes = [vp, _I64P]
     lib.pqw_plan_build_stages.restype = C.c_int
     lib.pqw_plan_stage_target.argtypes = [vp, C.c_int]
@@ -330,6 +332,14 @@ class NativePlan:
         if rc < 0:
             raise EngineError(self._err())
         return True
+
+    def lineage_clean(self) -> bool:
+        """True iff validate_lineage would report no problem (else the host's
+        validate_lineage gives the reference's messages)."""
+        out = (C.c_int64 * 2)()
+        if self.lib.pqw_plan_check_lineage(self.h, out) < 0:
+            raise EngineError(self._err())
+        return out[0] == 0 and out[1] == 0
 
     def build_stages(self) -> bool:
         """Stage construction; False: stage construction would raise."""

@@ -383,7 +383,8 @@ def verify_plan(plan: Plan, opts: VerifyOptions | None = None) -> dict[str, Any]
         validate_concrete(plan.logical)
         validate_concrete(plan.parallel)
         nat = None  # well formed after all: the host path takes it from here
-    problems = validate_lineage(plan.logical, plan.parallel, plan.lineage)
+    problems = [] if nat is not None and nat.lineage_clean() else \
+        validate_lineage(plan.logical, plan.parallel, plan.lineage)
     times["validate_s"] = time.perf_counter() - t
     tiling = [p for p in problems if "do not tile" in p]
     hard = [p for p in problems if "do not tile" not in p]

@@ -53,6 +53,9 @@ def test_native_stages_and_programs_match_host(lib, name, rel):
     nat = NativePlan(plan)
     ok_py = all(_python_ok(validate_concrete, g)[0] for g in (plan.logical, plan.parallel))
     assert nat.validate() == ok_py, name
+    from paper_2506_15961_b200.graph import validate_lineage
+    assert nat.lineage_clean() == (validate_lineage(plan.logical, plan.parallel,
+                                                    plan.lineage) == []), name
     ok, got = _python_ok(build_stages, plan)
     assert nat.build_stages() == ok, (name, got)
     if not ok:
@@ -209,3 +212,49 @@ def test_parallel_packer_matches_serial_packer(lib):
             del os.environ["PQW_PACK_SERIAL"]
         assert fast == serial
         assert c1.triples == c2.triples
+
+
+def _lineage_mutations():
+    from paper_2506_15961_b200.graph import LineageEntry, Shard
+
+    def first_split(plan):
+        return next(t for t, e in plan.lineage.items()
+                    if len({s.ranges for s in e.shards}) > 1)
+
+    def overlap(plan):
+        t = first_split(plan)
+        e = plan.lineage[t]
+        r0 = e.shards[0].ranges
+        shards = (Shard(e.shards[0].tensor, r0),) + tuple(Shard(s.tensor, r0) for s in e.shards[1:])
+        plan.lineage[t] = LineageEntry(e.logical, e.mode, shards)
+
+    def unknown_shard(plan):
+        t = first_split(plan)
+        e = plan.lineage[t]
+        plan.lineage[t] = LineageEntry(e.logical, e.mode,
+                                       (Shard("no-such-tensor", e.shards[0].ranges),) + e.shards[1:])
+
+    def bad_mode(plan):
+        t = first_split(plan)
+        e = plan.lineage[t]
+        plan.lineage[t] = LineageEntry(e.logical, "mirrored", e.shards)
+
+    def out_of_bounds(plan):
+        t = first_split(plan)
+        e = plan.lineage[t]
+        (lo, hi), rest = e.shards[0].ranges[0], e.shards[0].ranges[1:]
+        shards = (Shard(e.shards[0].tensor, ((lo + 100, hi + 100),) + rest),) + e.shards[1:]
+        plan.lineage[t] = LineageEntry(e.logical, e.mode, shards)
+    return {"overlap": overlap, "unknown_shard": unknown_shard, "bad_mode": bad_mode,
+            "out_of_bounds": out_of_bounds}
+
+
+@pytest.mark.parametrize("kind", sorted(_lineage_mutations()))
+def test_lineage_check_matches_host(lib, kind):
+    """pqw_plan_check_lineage flags exactly the plans validate_lineage flags."""
+    from paper_2506_15961_b200.graph import validate_lineage
+    plan = _base()
+    _lineage_mutations()[kind](plan)
+    nat = NativePlan(plan)
+    assert validate_lineage(plan.logical, plan.parallel, plan.lineage)
+    assert not nat.lineage_clean()
