@@ -16,10 +16,13 @@
 #include <sched.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <atomic>
 #include <cstdint>
 #include <cstring>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <queue>
 #include <stdexcept>
@@ -102,10 +105,11 @@ void parallel_for(size_t n, F&& f) {
   for (auto& t : pool) t.join();
 }
 
-// Open-addressing name -> index table (built once, then read from many threads).
+// Open-addressing name -> index table, built in parallel (CAS on the slots)
+// and then read from many threads.
 struct NameTable {
-  std::vector<uint64_t> hash;
-  std::vector<int32_t> slot;  // -1 empty
+  std::vector<uint64_t> hs;                    // hash per name index
+  std::unique_ptr<std::atomic<int32_t>[]> slot;  // name index per slot, -1 empty
   const std::vector<std::string_view>* names = nullptr;
   uint64_t mask = 0;
 
@@ -127,34 +131,40 @@ struct NameTable {
     size_t cap = 16;
     while (cap < ns.size() * 2) cap <<= 1;
     mask = cap - 1;
-    hash.assign(cap, 0);
-    slot.assign(cap, -1);
-    std::vector<uint64_t> hs(ns.size());
-    parallel_for((ns.size() + 65535) / 65536, [&](size_t c, unsigned) {
-      for (size_t i = c * 65536; i < std::min(ns.size(), (c + 1) * 65536); ++i) hs[i] = h(ns[i]);
+    slot.reset(new std::atomic<int32_t>[cap]);
+    hs.assign(ns.size(), 0);
+    const size_t chunk = 65536;
+    const size_t nc = (std::max(ns.size(), cap) + chunk - 1) / chunk;
+    parallel_for(nc, [&](size_t c, unsigned) {
+      for (size_t k = c * chunk; k < std::min(cap, (c + 1) * chunk); ++k)
+        slot[k].store(-1, std::memory_order_relaxed);
+      for (size_t i = c * chunk; i < std::min(ns.size(), (c + 1) * chunk); ++i) hs[i] = h(ns[i]);
     });
-    bool unique = true;
-    for (size_t i = 0; i < ns.size(); ++i) {
-      uint64_t k = hs[i] & mask;
-      for (;; k = (k + 1) & mask) {
-        if (slot[k] < 0) {
-          slot[k] = (int32_t)i;
-          hash[k] = hs[i];
-          break;
-        }
-        if (hash[k] == hs[i] && ns[slot[k]] == ns[i]) {
-          unique = false;
-          break;
+    std::atomic<bool> unique{true};
+    parallel_for((ns.size() + chunk - 1) / chunk, [&](size_t c, unsigned) {
+      for (size_t i = c * chunk; i < std::min(ns.size(), (c + 1) * chunk); ++i) {
+        for (uint64_t k = hs[i] & mask;; k = (k + 1) & mask) {
+          int32_t cur = slot[k].load(std::memory_order_acquire);
+          if (cur < 0) {
+            if (slot[k].compare_exchange_strong(cur, (int32_t)i, std::memory_order_acq_rel))
+              break;
+            // lost the race: cur now holds the winner, compare with it below
+          }
+          if (hs[(size_t)cur] == hs[i] && ns[(size_t)cur] == ns[i]) {
+            unique.store(false, std::memory_order_relaxed);
+            break;
+          }
         }
       }
-    }
-    return unique;
+    });
+    return unique.load();
   }
   int32_t find(std::string_view s) const {
     const uint64_t hv = h(s);
     for (uint64_t k = hv & mask;; k = (k + 1) & mask) {
-      if (slot[k] < 0) return -1;
-      if (hash[k] == hv && (*names)[slot[k]] == s) return slot[k];
+      const int32_t cur = slot[k].load(std::memory_order_relaxed);
+      if (cur < 0) return -1;
+      if (hs[(size_t)cur] == hv && (*names)[(size_t)cur] == s) return cur;
     }
   }
 };
@@ -190,26 +200,65 @@ struct GraphData {
     return nid[a] < nid[b];
   }
 
-  void resolve(const char* names, int64_t n, std::string& store, std::vector<int32_t>& out) {
-    std::vector<std::string_view> tmp;
-    split_names(names, n, store, tmp);
-    out.resize(tmp.size());
+  // n NUL-terminated names -> tensor indices, read in place: the buffer is cut
+  // into chunks at name boundaries, names counted per chunk, then resolved in
+  // parallel (no copy of the names is kept)
+  void resolve(const char* names, int64_t n, std::string& /*unused*/, std::vector<int32_t>& out) {
+    out.assign((size_t)n, -1);
+    if (n == 0) return;
+    size_t len = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      const void* z = std::memchr(names + len, 0, SIZE_MAX >> 1);
+      len = (size_t)((const char*)z - names) + 1;
+    }
+    const unsigned K = host_threads(std::max<size_t>(1, len / (1u << 20)));
+    std::vector<size_t> cut(K + 1, len);
+    cut[0] = 0;
+    for (unsigned k = 1; k < K; ++k) {
+      size_t c = len * k / K;
+      if (c < cut[k - 1]) c = cut[k - 1];
+      while (c < len && c > 0 && names[c - 1] != 0) ++c;  // start right after a NUL
+      cut[k] = c;
+    }
+    std::vector<size_t> cnt(K + 1, 0);
+    parallel_for(K, [&](size_t k, unsigned) {
+      size_t c = 0;
+      for (size_t i = cut[k]; i < cut[k + 1]; ++i) c += names[i] == 0;
+      cnt[k + 1] = c;
+    });
+    for (unsigned k = 0; k < K; ++k) cnt[k + 1] += cnt[k];
     std::atomic<bool> all{true};
-    parallel_for((tmp.size() + 65535) / 65536, [&](size_t c, unsigned) {
-      for (size_t i = c * 65536; i < std::min(tmp.size(), (c + 1) * 65536); ++i) {
-        out[i] = find(tmp[i]);
-        if (out[i] < 0) all = false;
+    parallel_for(K, [&](size_t k, unsigned) {
+      size_t idx = cnt[k];
+      for (size_t i = cut[k]; i < cut[k + 1] && idx < (size_t)n;) {
+        const size_t l = std::strlen(names + i);
+        out[idx] = find(std::string_view(names + i, l));
+        if (out[idx] < 0) all = false;
+        ++idx;
+        i += l + 1;
       }
     });
     if (!all) resolved = false;
   }
 
   void load(const pqw_graph_desc& d) {
+    static const bool timing = getenv("PQW_TIMING") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto t0 = now();
+    auto lap = [&](const char* what) {
+      if (!timing) return;
+      auto t = now();
+      fprintf(stderr, "PQW_TIMING load %s %.1f ms\n", what,
+              std::chrono::duration<double, std::milli>(t - t0).count());
+      t0 = t;
+    };
     split_names(d.tensor_names, d.n_tensors, tstore, tname);
+    lap("tensor names");
     if (!index.build(tname)) {
       resolved = false;
       problem = "duplicate tensor id";
     }
+    lap("tensor table");
     dim_off.assign((size_t)d.n_tensors + 1, 0);
     for (int64_t i = 0; i < d.n_tensors; ++i) dim_off[i + 1] = dim_off[i] + d.tensor_ndim[i];
     dims.assign(d.tensor_dims, d.tensor_dims + dim_off.back());
@@ -228,8 +277,10 @@ struct GraphData {
       attr_off[i + 1] = attr_off[i] + d.node_nattr[i];
     }
     attrs.assign(d.node_attrs, d.node_attrs + attr_off[n]);
+    lap("node columns");
     resolve(d.node_inputs, in_off[n], istore, ins);
     resolve(d.node_outputs, out_off[n], ostore, outs);
+    lap("resolve io");
     {
       std::vector<int32_t> gin;
       std::string gs;
@@ -248,12 +299,14 @@ struct GraphData {
         if (producer[t] >= 0) unique_producers = false;
         producer[t] = (int32_t)v;
       }
+    lap("inputs+producers");
     // node ids must be unique for the (device, seq, id) order to be total
     NameTable ids;
     if (!ids.build(nid)) {
       resolved = false;
       problem = "duplicate node id";
     }
+    lap("node id table");
   }
 };
 
