@@ -241,7 +241,8 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2506_15961_b200 import field as F
-    from paper_2506_15961_b200.distributed import partition
+    from paper_2506_15961_b200.distributed import partition, share_host_threads
+    share_host_threads()
     from paper_2506_15961_b200.engine import Engine, peak_fieldops
     from paper_2506_15961_b200.native import NativePlan
     from paper_2506_15961_b200.verify import VerifyOptions, verify_plan

@@ -456,6 +456,7 @@ bool pack_fast(PyObject* tensors, PyObject* const* nodes, Py_ssize_t nn, const K
     return *reinterpret_cast<PyObject**>(reinterpret_cast<char*>(obj) + f.off[i]);
   };
   unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  if (const char* e = getenv("PQW_THREADS")) nt = (unsigned)std::max(1, std::min(16, atoi(e)));
   const size_t work = tv.size() + (size_t)nn;
   if (work < 50000) nt = 1;
   std::vector<Cols> parts(nt);

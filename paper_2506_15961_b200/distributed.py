@@ -71,6 +71,20 @@ def local_device() -> int:
     return local % n if n > 0 else local
 
 
+def share_host_threads() -> None:
+    """Ranks of one box share its host cores: unless PQW_THREADS is set, each
+    rank's native plan core and compiler use cores / local world size."""
+    if "PQW_THREADS" in os.environ:
+        return
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+    if local_world > 1:
+        try:
+            cores = len(os.sched_getaffinity(0))
+        except (AttributeError, OSError):
+            cores = os.cpu_count() or 1
+        os.environ["PQW_THREADS"] = str(max(1, cores // local_world))
+
+
 class StageFailure:
     """A stage whose discharge raised, as sent through the gather."""
 
@@ -149,6 +163,7 @@ def discharge_sharded(plan, stages: list[Stage] | None, opts, group=None,
     rank, world = world_info(group)
     if opts.device is None:
         opts = replace(opts, device=local_device())
+    share_host_threads()
     if nplan is not None:
         pairs, stats, parts = _native_share(nplan, opts, rank, world)
         n_stages = nplan.n_stages
