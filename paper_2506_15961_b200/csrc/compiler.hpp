@@ -50,7 +50,7 @@ CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* con
 // Defaults (overridable per engine: PQW_FAST_SLOTS, PQW_WARPS, PQW_WINDOW,
 // PQW_BMAX, PQW_XLAT env vars): 1680 slots = 210 KB of shared memory, which
 // leaves room for the per-warp code rings (16 x 1 KB).
-constexpr uint32_t DEFAULT_FAST_SLOTS = 1680;
+constexpr uint32_t DEFAULT_FAST_SLOTS = 1800;
 constexpr uint32_t DEFAULT_WARPS = 16;
 
 // Host confirmation of a refutation (pqw_confirm in include/planeq_witness.h):

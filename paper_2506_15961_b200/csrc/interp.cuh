@@ -111,7 +111,13 @@ __device__ __forceinline__ uint32_t red64(uint64_t x) { return fred64(x); }
 // decode reads LDS.128 broadcasts instead of waiting out an L2 round trip per
 // group. Every read unit (a header, one payload group, or one pair/term of a
 // wide DOT/SUM) is at most 33 records, so it spans at most two chunks.
-constexpr uint32_t RING_RECS = 64;
+#ifndef PQW_RING_CHUNK
+#define PQW_RING_CHUNK 32
+#endif
+constexpr uint32_t RING_CHUNK = PQW_RING_CHUNK;  // records per chunk (one cp.async per lane)
+constexpr uint32_t RING_SHIFT = RING_CHUNK == 16 ? 4 : 5;
+static_assert(RING_CHUNK == 16 || RING_CHUNK == 32, "ring chunk of 16 or 32 records");
+constexpr uint32_t RING_RECS = 2 * RING_CHUNK;
 #if !defined(PQW_PLAIN_RING) && !defined(PQW_MIRROR_RING)
 #define PQW_MIRROR_RING  // default (A/B r2m: 405B kernel 13.97 -> 13.30 ms)
 #endif
@@ -121,7 +127,7 @@ constexpr uint32_t RING_BYTES = 0;
 // chunks landing at ring positions 0..31 are also copied to 64..95, so every
 // read unit (<= 33 records) is contiguous in shared memory: one address per
 // group, record offsets become load immediates
-constexpr uint32_t RING_BYTES = (RING_RECS + 32) * 16;
+constexpr uint32_t RING_BYTES = (RING_RECS + RING_CHUNK) * 16;
 #else
 constexpr uint32_t RING_BYTES = RING_RECS * 16;
 #endif
@@ -130,17 +136,18 @@ __device__ __noinline__ uint2 ring_refill(const uint4* src, uint32_t base, uint3
                                           uint32_t issued, uint32_t ready, uint32_t c0,
                                           uint32_t c1) {
   auto issue = [&]() {
-    const uint32_t r = issued * 32u;
+    const uint32_t r = issued * RING_CHUNK;
     const uint32_t dst = base + ((r & (RING_RECS - 1)) << 4) + lane4;
     const char* g = reinterpret_cast<const char*>(src + r) + lane4;
+    const bool mine = lane4 < RING_CHUNK * 16;  // lanes past the chunk copy nothing
 #ifdef PQW_MIRROR_RING
-    if ((r & (RING_RECS - 1)) == 0)
+    if (mine && (r & (RING_RECS - 1)) == 0)
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + RING_RECS * 16), "l"(g)
                    : "memory");
 #endif
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n\tcp.async.commit_group;" ::"r"(dst),
-                 "l"(g)
-                 : "memory");
+    if (mine)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(g) : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
     ++issued;
   };
   if (issued <= c0 + 1) issue();  // look-ahead: the slot of chunk c0+1 held c0-1
@@ -168,12 +175,13 @@ struct CodeRing {
 #endif
 
   __device__ __forceinline__ void issue() {
-    const uint32_t r = issued * 32u;
+    const uint32_t r = issued * RING_CHUNK;
     const uint32_t dst = base + ((r & (RING_RECS - 1)) << 4) + lane4;
     const char* g = reinterpret_cast<const char*>(src + r) + lane4;
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n\tcp.async.commit_group;" ::"r"(dst),
-                 "l"(g)
-                 : "memory");
+    const bool mine = lane4 < RING_CHUNK * 16;  // lanes past the chunk copy nothing
+    if (mine)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(g) : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
     ++issued;
   }
   // make records [p, p + r) resident (r <= 33). The common case -- the range
@@ -185,7 +193,7 @@ struct CodeRing {
 #ifdef PQW_NO_RING
     return;
 #endif
-    const uint32_t c0 = p >> 5, c1 = (p + r - 1) >> 5;
+    const uint32_t c0 = p >> RING_SHIFT, c1 = (p + r - 1) >> RING_SHIFT;
     if (issued <= c0 + 1 || c1 >= ready) {
       const uint2 st = ring_refill(src, base, lane4, issued, ready, c0, c1);
       issued = st.x;
