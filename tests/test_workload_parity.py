@@ -171,3 +171,34 @@ def test_full_workload_generator_reproduces_the_verified_plan(rec):
     from paper_2506_15961_b200.plan import dumps
     _desc, plan = get_workload(rec["name"])
     assert hashlib.sha256(dumps(plan).encode()).hexdigest() == rec["plan_sha256"]
+
+
+def _partial_records():
+    import glob
+    import json
+    import os
+    from golden_io import GOLDEN
+    return [json.load(open(p))
+            for p in sorted(glob.glob(os.path.join(GOLDEN, "verdicts_partial_*.json")))]
+
+
+PARTIAL = _partial_records()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rec", PARTIAL, ids=[r["name"] for r in PARTIAL])
+def test_full_405b_stage_verdicts_match_reference_prefix(gpu, rec):
+    """configs[3] itself, the full 126-layer Llama3-405B plan: the reference's
+    own verdicts on its first stages (the full reference sweep projects to ~23 h,
+    see the record's note) equal verify_plan's, through the native path."""
+    import hashlib
+    from paper_2506_15961_b200.plan import dumps
+    from paper_2506_15961_b200.verify import VerifyOptions, verify_plan
+    _desc, plan = get_workload(rec["name"])
+    assert hashlib.sha256(dumps(plan).encode()).hexdigest() == rec["plan_sha256"]
+    rep = verify_plan(plan, VerifyOptions(no_reduce=True, no_cancel=True, witnesses=256))
+    assert rep["engine"]["host_path"] == "native"
+    got = [(s["target"], s["status"]) for s in rep["stages"]]
+    want = [tuple(x) for x in rec["stage_status"]]
+    assert got[: len(want)] == want
+    assert rep["verdict"] == "proven"
