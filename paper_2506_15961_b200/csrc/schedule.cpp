@@ -603,9 +603,18 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
           if (l) { loc += len; nloc++; }
           if (sw) same_warp += len;
         }
-        fprintf(stderr, "QUADDBG intervals=%zu slots=%u quad-local slot-time %.1f%% (n=%llu) same-warp %.1f%%\n",
+        uint64_t by_op[I_NUM_OPS] = {};
+        for (const auto& I : sm) {
+          const auto& E = ex[I.writer];
+          const uint32_t op = E.kind == 0 ? U[bundles[E.main].units[0]].op : (E.kind == 1 ? I_FILL : I_SPILL);
+          by_op[op] += I.end - I.start;
+        }
+        fprintf(stderr, "QUADDBG intervals=%zu slots=%u quad-local slot-time %.1f%% (n=%llu) same-warp %.1f%% | by def op:",
                 sm.size(), n_sm, 100.0 * loc / std::max<uint64_t>(tot, 1), (unsigned long long)nloc,
                 100.0 * same_warp / std::max<uint64_t>(tot, 1));
+        for (int i = 0; i < I_NUM_OPS; ++i)
+          if (by_op[i]) fprintf(stderr, " op%d=%.1f%%", i, 100.0 * by_op[i] / std::max<uint64_t>(tot, 1));
+        fprintf(stderr, "\n");
       }
 
       // ---- 3. synchronisation -------------------------------------------------
@@ -842,7 +851,14 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
             by[U[v].op]++;
             fills[U[v].op] += rdb_off[v + 1] - rdb_off[v];
           }
-        fprintf(stderr, "SPILLDBG values=%zu spilled:", values.size());
+        uint64_t var_vals = 0, var_reads = 0;
+        for (uint32_t v : values)
+          if (U[v].op == I_VAR) {
+            var_vals++;
+            var_reads += rdb_off[v + 1] - rdb_off[v];
+          }
+        fprintf(stderr, "SPILLDBG values=%zu vars=%llu var-reading-bundles=%llu bundles=%u spilled:", values.size(),
+                (unsigned long long)var_vals, (unsigned long long)var_reads, NB);
         for (int i = 0; i < I_NUM_OPS; ++i)
           if (by[i]) fprintf(stderr, " op%d=%llu(fills %llu)", i, (unsigned long long)by[i], (unsigned long long)fills[i]);
         fprintf(stderr, "\n");
