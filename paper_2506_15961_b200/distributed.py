@@ -22,7 +22,7 @@ schedules, uploads and launches only its share (pqw_stage_select).
 from __future__ import annotations
 
 import os
-from dataclasses import asdict, replace
+from dataclasses import replace
 from typing import Callable
 
 from . import errors as _errors
@@ -183,7 +183,7 @@ def discharge_sharded(plan, stages: list[Stage] | None, opts, group=None,
             pairs = [(i, fail) for i in mine]
             stats = {"error": repr(fail)}
         n_stages = len(stages)
-    payload = [(i, r if isinstance(r, StageFailure) else asdict(r)) for i, r in pairs]
+    payload = [(i, r if isinstance(r, StageFailure) else r.as_dict()) for i, r in pairs]
     gathered: list = [None] * world
     dist.all_gather_object(gathered, (payload, stats), group=group)
     results, cancelled = merge_results([g[0] for g in gathered], n_stages, opts.no_cancel)

@@ -22,7 +22,7 @@ per-stage outcome into the reference's StageResult shape.
 from __future__ import annotations
 
 import time
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, fields
 from fractions import Fraction
 from typing import Any
 
@@ -76,6 +76,14 @@ class StageResult:
     failing_witnesses: int = 0
     degree_bound: int = 0
     false_equiv_log2: float | None = None
+
+    def as_dict(self) -> dict[str, Any]:
+        """dataclasses.asdict without its recursive deep copy (the detail dict
+        is built fresh for each result): the report's per-stage record."""
+        return {f: getattr(self, f) for f in _RESULT_FIELDS}
+
+
+_RESULT_FIELDS = tuple(f.name for f in fields(StageResult))
 
 
 def entry_order(plan: Plan, order: list[Node] | None = None) -> list[str]:

@@ -16,7 +16,7 @@ from __future__ import annotations
 
 import hashlib
 import time
-from dataclasses import asdict, dataclass
+from dataclasses import dataclass
 from typing import Any
 
 import numpy as np
@@ -455,7 +455,7 @@ def _verify_plan(plan: Plan, opts: VerifyOptions | None) -> dict[str, Any]:
     stats["times"] = {k: round(v, 6) for k, v in times.items()}
     report.update(
         verdict=verdict,
-        stages=[asdict(r) for r in results],
+        stages=[r.as_dict() for r in results],
         cancelled=cancelled,
         obligations=total_ob,
         fastpath_rate=round(total_fast / total_ob, 6) if total_ob else None,
