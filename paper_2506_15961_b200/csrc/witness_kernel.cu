@@ -42,6 +42,60 @@ int fail(int code, const std::string& msg) {
 }  // namespace
 
 int set_last_error(int code, const std::string& msg) { return fail(code, msg); }
+
+// Device memory of uploaded images comes from a per-device pool of blocks
+// that outlive engines: verify_plan creates an engine per call, and a fresh
+// cudaMalloc/cudaFree of ~30 MB per call measured 30-150 ms of variance.
+// A returned block is reused by the next upload that fits in it; at most two
+// blocks per device stay cached.
+std::mutex g_pool_mu;
+std::unordered_map<int, std::vector<std::pair<void*, size_t>>> g_pool;
+
+void* arena_get(int device, size_t need, size_t* got) {
+  {
+    std::lock_guard<std::mutex> l(g_pool_mu);
+    auto& v = g_pool[device];
+    size_t best = SIZE_MAX;
+    for (size_t i = 0; i < v.size(); ++i)
+      if (v[i].second >= need && (best == SIZE_MAX || v[i].second < v[best].second)) best = i;
+    if (best != SIZE_MAX) {
+      auto blk = v[best];
+      v.erase(v.begin() + (long)best);
+      *got = blk.second;
+      return blk.first;
+    }
+  }
+  void* p = nullptr;
+  const size_t bytes = need + need / 4;  // headroom for the next, slightly larger image
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    // drop the cached blocks and retry at the exact size
+    std::vector<std::pair<void*, size_t>> drop;
+    {
+      std::lock_guard<std::mutex> l(g_pool_mu);
+      drop.swap(g_pool[device]);
+    }
+    for (auto& b : drop) cudaFree(b.first);
+    if (cudaMalloc(&p, need) != cudaSuccess) return nullptr;
+    *got = need;
+    return p;
+  }
+  *got = bytes;
+  return p;
+}
+
+void arena_put(int device, void* p, size_t bytes) {
+  cudaSetDevice(device);
+  cudaDeviceSynchronize();  // no launch of the owning engine may still use it
+  std::lock_guard<std::mutex> l(g_pool_mu);
+  auto& v = g_pool[device];
+  v.push_back({p, bytes});
+  if (v.size() > 2) {  // keep the two largest
+    std::sort(v.begin(), v.end(), [](auto& a, auto& b) { return a.second > b.second; });
+    for (size_t i = 2; i < v.size(); ++i) cudaFree(v[i].first);
+    v.resize(2);
+  }
+}
 }  // namespace pqw
 
 struct pqw_engine {
@@ -97,18 +151,13 @@ struct pqw_engine {
   bool results_ready = false;
   unsigned long long* d_prof_last = nullptr;
 
+  void* arena = nullptr;     // one device block holding every buffer of the image
+  size_t arena_bytes = 0;
+
   void free_device() {
-    cudaFree(d_code);
-    cudaFree(d_stages);
-    cudaFree(d_work);
-    cudaFree(d_var_keys);
-    cudaFree(d_fn_keys);
-    cudaFree(d_counter);
-    cudaFree(d_scratch);
-    cudaFree(d_first_bad);
-    cudaFree(d_n_valid);
-    cudaFree(d_n_bad);
-    cudaFree(d_probe);
+    if (arena) pqw::arena_put(device, arena, arena_bytes);
+    arena = nullptr;
+    arena_bytes = 0;
     d_code = nullptr;
     d_stages = nullptr;
     d_work = nullptr;
@@ -553,28 +602,42 @@ int pqw_upload(pqw_engine* e) {
   if (per_sm < 1) per_sm = 1;
   e->grid = (uint32_t)(n_sm * per_sm);
 
-  CU(cudaMalloc(&e->d_code, code.size() * sizeof(pqw_ins)));
+  // one block for the whole image (pooled across engines, see arena_get)
+  const size_t nk = std::max<size_t>(e->var_keys.size(), 1);
+  const size_t nr = std::max<size_t>(ids.size(), 1);
+  e->scratch_bytes = (size_t)e->grid * std::max<uint32_t>(e->spill_slots, 1) * slot_bytes;
+  const size_t sizes[11] = {code.size() * sizeof(pqw_ins), descs.size() * sizeof(pqw::StageDesc),
+                            work.size() * sizeof(uint32_t), nk * sizeof(uint64_t),
+                            3 * sizeof(uint64_t), sizeof(uint32_t), e->scratch_bytes,
+                            nr * sizeof(unsigned long long), nr * sizeof(uint32_t),
+                            nr * sizeof(uint32_t), 2 * sizeof(uint32_t)};
+  size_t offs[11], total = 0;
+  for (int i = 0; i < 11; ++i) {
+    offs[i] = total;
+    total += (sizes[i] + 255) & ~(size_t)255;
+  }
+  e->arena = pqw::arena_get(e->device, total, &e->arena_bytes);
+  if (!e->arena) return fail(PQW_ECUDA, "device allocation of the image failed");
+  char* base = static_cast<char*>(e->arena);
+  e->d_code = reinterpret_cast<uint4*>(base + offs[0]);
+  e->d_stages = reinterpret_cast<pqw::StageDesc*>(base + offs[1]);
+  e->d_work = reinterpret_cast<uint32_t*>(base + offs[2]);
+  e->d_var_keys = reinterpret_cast<uint64_t*>(base + offs[3]);
+  e->d_fn_keys = reinterpret_cast<uint64_t*>(base + offs[4]);
+  e->d_counter = reinterpret_cast<uint32_t*>(base + offs[5]);
+  e->d_scratch = reinterpret_cast<uint32_t*>(base + offs[6]);
+  e->d_first_bad = reinterpret_cast<unsigned long long*>(base + offs[7]);
+  e->d_n_valid = reinterpret_cast<uint32_t*>(base + offs[8]);
+  e->d_n_bad = reinterpret_cast<uint32_t*>(base + offs[9]);
+  e->d_probe = reinterpret_cast<uint32_t*>(base + offs[10]);
   CU(cudaMemcpy(e->d_code, code.data(), code.size() * sizeof(pqw_ins), cudaMemcpyHostToDevice));
-  CU(cudaMalloc(&e->d_stages, descs.size() * sizeof(pqw::StageDesc)));
   CU(cudaMemcpy(e->d_stages, descs.data(), descs.size() * sizeof(pqw::StageDesc),
                 cudaMemcpyHostToDevice));
-  CU(cudaMalloc(&e->d_work, work.size() * sizeof(uint32_t)));
   CU(cudaMemcpy(e->d_work, work.data(), work.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
-  size_t nk = std::max<size_t>(e->var_keys.size(), 1);
-  CU(cudaMalloc(&e->d_var_keys, nk * sizeof(uint64_t)));
   if (!e->var_keys.empty())
     CU(cudaMemcpy(e->d_var_keys, e->var_keys.data(), e->var_keys.size() * sizeof(uint64_t),
                   cudaMemcpyHostToDevice));
-  CU(cudaMalloc(&e->d_fn_keys, 3 * sizeof(uint64_t)));
   CU(cudaMemcpy(e->d_fn_keys, e->fn_keys, 3 * sizeof(uint64_t), cudaMemcpyHostToDevice));
-  CU(cudaMalloc(&e->d_counter, sizeof(uint32_t)));
-  e->scratch_bytes = (size_t)e->grid * std::max<uint32_t>(e->spill_slots, 1) * slot_bytes;
-  CU(cudaMalloc(&e->d_scratch, e->scratch_bytes));
-  size_t nr = std::max<size_t>(ids.size(), 1);
-  CU(cudaMalloc(&e->d_first_bad, nr * sizeof(unsigned long long)));
-  CU(cudaMalloc(&e->d_n_valid, nr * sizeof(uint32_t)));
-  CU(cudaMalloc(&e->d_n_bad, nr * sizeof(uint32_t)));
-  CU(cudaMalloc(&e->d_probe, 2 * sizeof(uint32_t)));
   e->h2d_bytes = code.size() * sizeof(pqw_ins) + descs.size() * sizeof(pqw::StageDesc) +
                  work.size() * sizeof(uint32_t) + e->var_keys.size() * sizeof(uint64_t) +
                  3 * sizeof(uint64_t);

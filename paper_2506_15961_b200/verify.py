@@ -193,9 +193,12 @@ class EngineWitnesses:
         self.eng = eng
 
     def run(self, refs, opts) -> tuple:
+        t0 = time.perf_counter()
         self.eng.upload()
+        t1 = time.perf_counter()
         self.eng.launch(opts.witnesses)
         fb, nv, nb = self.eng.results()
+        self.times = {"upload_s": t1 - t0, "launch_results_s": time.perf_counter() - t1}
         return fb, nv, nb, self.eng.last_launch_ms()
 
     def probe(self, comp, w: int, obl: int):
@@ -211,12 +214,15 @@ def _run(refs: list[_StageRef], eng: Engine, opts: VerifyOptions, host_s: float,
     t0 = time.perf_counter()
     comps = [r.comp for r in refs]
     needs_gpu = any(c is not None and c.status == STAGE_OK for c in comps)
+    t_front = time.perf_counter() - t0
     gpu_ms = 0.0
     fb = nv = nb = None
     source = source or EngineWitnesses(eng)
     if needs_gpu:
         fb, nv, nb, gpu_ms = source.run(refs, opts)
     t_dev = time.perf_counter() - t0
+    stats["phases"] = {"front_s": round(t_front, 6), **{k: round(v, 6) for k, v in
+                                                         getattr(source, "times", {}).items()}}
     n_gpu = sum(1 for c in comps if c is not None and c.status == STAGE_OK)
     per_stage = (host_s + t_dev) / max(len(refs), 1)
     results: list[StageResult] = []
@@ -234,6 +240,7 @@ def _run(refs: list[_StageRef], eng: Engine, opts: VerifyOptions, host_s: float,
         if r.status == "refuted" and not opts.no_cancel:
             cancelled = len(refs) - len(results)
             break
+    stats["phases"]["report_s"] = round(time.perf_counter() - t0 - t_dev, 6)
     stats.update({"gpu_ms": round(gpu_ms, 4), "gpu_stages": n_gpu, "witnesses": opts.witnesses,
                   "device_s": round(t_dev, 6)})
     if needs_gpu and isinstance(source, EngineWitnesses):

@@ -12,11 +12,12 @@ from paper_2506_15961_b200.workloads import get_workload  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "llama-2l-tp2dp2"
 _d, plan = get_workload(name)
-for i in range(4):
+for i in range(8):
     t0 = time.perf_counter()
     rep = verify_plan(plan, VerifyOptions(no_reduce=True, witnesses=512, device=0))
     t1 = time.perf_counter()
-    print(f"verify_plan {t1 - t0:.4f}s", rep["engine"].get("times"), flush=True)
+    print(f"verify_plan {t1 - t0:.4f}s", rep["engine"].get("times"), rep["engine"].get("phases"),
+          "lower_s", rep["engine"].get("lower_s"), flush=True)
 for i in range(3):
     t = [time.perf_counter()]
     nat = NativePlan(plan); nat.validate(); nat.build_stages(); t.append(time.perf_counter())
