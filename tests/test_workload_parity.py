@@ -78,7 +78,7 @@ def test_full_size_workload_matches_oracle(gpu, name):
     nat.close()
 
 
-@pytest.mark.parametrize("name", ["llama3-405b-tp8pp16dp2"])
+@pytest.mark.parametrize("name", ["llama3-405b-16l-tp8pp16dp2"])
 def test_full_size_programs_are_deduplicated_exactly(lib, name):
     """CPU: the distinct-program count that the GPU test covers (no sampling:
     every stage's program text is hashed)."""
@@ -163,7 +163,12 @@ def test_full_workload_stage_verdicts_match_reference(gpu, rec):
             assert r.status == "unknown", target
 
 
-@pytest.mark.parametrize("rec", FULL, ids=[r["name"] for r in FULL])
+# the bug-injected variants regenerate the same base plan: one of them on CPU
+# (the GPU test re-checks every record's digest before comparing)
+GEN = [r for r in FULL if "~" not in r["name"]] + [r for r in FULL if "~" in r["name"]][:1]
+
+
+@pytest.mark.parametrize("rec", GEN, ids=[r["name"] for r in GEN])
 def test_full_workload_generator_reproduces_the_verified_plan(rec):
     """CPU: the generator still emits, byte for byte, the plan whose stage
     verdicts the reference computed (so the GPU comparison is meaningful)."""
