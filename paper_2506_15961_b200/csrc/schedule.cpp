@@ -225,6 +225,8 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
 
   // One scheduling attempt with look-ahead window o.window and bundle width
   // o.bmax; false if the value file cannot hold even its temporaries.
+  static const uint32_t leaf_window =
+      getenv("PQW_LEAF_WINDOW") ? (uint32_t)atoi(getenv("PQW_LEAF_WINDOW")) : 0;
   auto try_once = [&](const SchedOptions& o, Program& prog) -> bool {
     // ---- 1. list scheduling -------------------------------------------------
     std::vector<uint64_t> fin(N, 0), F1(N, 0), F2(N, 0);
@@ -311,7 +313,13 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
       cand.push_back(head);
       if (!(H.op == I_INV && !H.guarded)) {
         const IdSet& rc = ready_cls[cls[head]];
-        for (uint32_t j = rc.next(frontier); j < lim && cand.size() < o.bmax; j = rc.next(j + 1))
+        // leaves (VAR, CONST) are ready from the start: bundling them from the
+        // whole window would load witness values long before their readers
+        // and hold slots meanwhile; they join a bundle only from near the head
+        uint32_t blim = lim;
+        if ((H.op == I_VAR || H.op == I_CONST) && leaf_window)
+          blim = (uint32_t)std::min<uint64_t>(lim, (uint64_t)head + leaf_window);
+        for (uint32_t j = rc.next(frontier); j < blim && cand.size() < o.bmax; j = rc.next(j + 1))
           if (j != head && est(j, w) <= t) cand.push_back(j);
       }
       const uint64_t cost = bundle_cost(H, cand.size());
