@@ -132,7 +132,8 @@ struct Builder {
   std::unordered_map<uint64_t, uint32_t> head;
   std::vector<uint32_t> chain;
   std::unordered_map<ConstKey, uint32_t, ConstKeyHash> const_ids;
-  bool lossy = false;        // an exact constant vanishes mod p (nonzero multiple of p)
+  bool lossy = false;        // an exact constant vanishes mod p, or two collide
+  std::unordered_map<uint32_t, std::pair<int64_t, int64_t>> exact_of_res;
   std::vector<uint32_t> dens;  // definedness conditions, creation order
   const uint64_t* fn_keys = nullptr;
   int side = 0;
@@ -158,6 +159,13 @@ struct Builder {
       return it->second;
     }
     if (ex.ok && ex.num != 0 && ex.num % (int64_t)P == 0) lossy = true;
+    if (ex.ok) {
+      // two distinct exact constants with one image in F_p: the field cannot
+      // tell apart what they scale
+      auto r_it = exact_of_res.find(r);
+      if (r_it == exact_of_res.end()) exact_of_res.emplace(r, std::make_pair(ex.num, ex.den));
+      else if (r_it->second != std::make_pair(ex.num, ex.den)) lossy = true;
+    }
     Val v{};
     v.kind = K_CONST;
     v.aux = r;
@@ -170,6 +178,14 @@ struct Builder {
     return cst(residue_of(n, 1), Exact{true, n, 1}, (double)n, false, is_int);
   }
   bool ufc(uint32_t x) const { return (vals[x].flags & F_UF) != 0; }
+  // algebraic identities fold on the exact value when the compiler knows it
+  // (a constant congruent to 0 or 1 mod p is not 0 or 1 over the rationals)
+  bool is_zero(uint32_t x) const {
+    return is_const(x) && (exact[x].ok ? exact[x].num == 0 : res(x) == 0);
+  }
+  bool is_one(uint32_t x) const {
+    return is_const(x) && (exact[x].ok ? exact[x].num == 1 && exact[x].den == 1 : res(x) == 1);
+  }
   uint32_t cst_exact(const Exact& ex, uint32_t r, double real) { return cst(r, ex, real); }
   bool is_const(uint32_t id) const { return vals[id].kind == K_CONST; }
   uint32_t res(uint32_t id) const { return (uint32_t)vals[id].aux; }
@@ -261,8 +277,8 @@ struct Builder {
 
   // -- arithmetic with folding -------------------------------------------
   uint32_t add(uint32_t x, uint32_t y) {
-    if (is_const(x) && res(x) == 0) return y;
-    if (is_const(y) && res(y) == 0) return x;
+    if (is_zero(x)) return y;
+    if (is_zero(y)) return x;
     if (is_const(x) && is_const(y)) {
       Exact ex = (exact[x].ok && exact[y].ok)
                      ? make_exact((__int128)exact[x].num * exact[y].den +
@@ -278,7 +294,7 @@ struct Builder {
   }
   uint32_t sub(uint32_t x, uint32_t y) {
     if (x == y) return zero();
-    if (is_const(y) && res(y) == 0) return x;
+    if (is_zero(y)) return x;
     if (is_const(x) && is_const(y)) {
       Exact ex = (exact[x].ok && exact[y].ok)
                      ? make_exact((__int128)exact[x].num * exact[y].den -
@@ -299,10 +315,9 @@ struct Builder {
     return intern(O_NEG, x, 0, 0, nullptr, 0, vals[x].dnum, vals[x].dden);
   }
   uint32_t mul(uint32_t x, uint32_t y) {
-    if (is_const(x) && res(x) == 0) return zero();
-    if (is_const(y) && res(y) == 0) return zero();
-    if (is_const(x) && res(x) == 1) return y;
-    if (is_const(y) && res(y) == 1) return x;
+    if (is_zero(x) || is_zero(y)) return zero();
+    if (is_one(x)) return y;
+    if (is_one(y)) return x;
     if (is_const(x) && is_const(y)) {
       Exact ex = (exact[x].ok && exact[y].ok)
                      ? make_exact((__int128)exact[x].num * exact[y].num,
@@ -342,7 +357,7 @@ struct Builder {
                      : Exact{false, 0, 0};
       return mul(x, cst(inv, ex, 1.0 / realc[y], ufc(y)));
     }
-    if (is_const(x) && res(x) == 0) return zero();
+    if (is_zero(x)) return zero();
     // x / y = x * y^-1 with the inverse value-numbered: rows that share a
     // denominator (softmax normalizers, expanded sums) invert it once
     uint32_t iv = intern(O_INV, y, 0, 0, nullptr, 0, vals[y].dden, vals[y].dnum);
@@ -365,7 +380,7 @@ struct Builder {
         terms.push_back(x);
       }
     }
-    if (cacc != NONE && res(cacc) != 0) terms.push_back(cacc);
+    if (cacc != NONE && !is_zero(cacc)) terms.push_back(cacc);
     if (terms.empty()) return cacc == NONE ? zero() : cacc;
     if (terms.size() == 1) return terms[0];
     if (terms.size() == 2) return add(terms[0], terms[1]);
@@ -398,7 +413,7 @@ struct Builder {
     pr.reserve(xs.size());
     for (size_t i = 0; i < xs.size(); ++i) {
       uint32_t a = xs[i], b = ys[i];
-      if ((is_const(a) && res(a) == 0) || (is_const(b) && res(b) == 0)) continue;
+      if (is_zero(a) || is_zero(b)) continue;
       if (is_const(a) || is_const(b) || (is_const(a) && is_const(b))) {
         extra.push_back(mul(a, b));
         continue;

@@ -102,3 +102,52 @@ def test_front_end_errors_surface_at_status(lib):
     with pytest.raises(EngineError):
         _ = c.status
     e.close()
+
+
+def _scale_check_program(c_lhs, c_rhs):
+    """x (2 vars); obligations scale(x, c_lhs) == scale(x, c_rhs) (c = None: x itself)."""
+    import numpy as np
+    from paper_2506_15961_b200 import field as F
+    from paper_2506_15961_b200.stages import IR_MAGIC, OPCODE, T_CHECK, T_VARS
+    consts, ops, n_t = [], [T_VARS, 0, 1, 1, 0, 0], 1
+    sides = []
+    for c in (c_lhs, c_rhs):
+        if c is None:
+            sides.append(0)
+            continue
+        consts.append(F.const_triple(c))
+        ops += [OPCODE["scale"], 1, 1, 1, 0, n_t, len(consts) - 1]
+        sides.append(n_t)
+        n_t += 1
+    ops += [T_CHECK, 2, 0, 1, sides[0], sides[1], 0]
+    head = [IR_MAGIC, n_t, 1 + sum(c is not None for c in (c_lhs, c_rhs)) + 1, 2]
+    ir = head + [1, 2] * n_t + ops
+    return (np.array(ir, dtype=np.int32), np.array(consts or [(0, 0, 0)], dtype=np.int64)[:len(consts)],
+            np.array([5, 6], dtype=np.uint64))
+
+
+def test_constants_that_collide_mod_p_are_not_decided(lib):
+    """Distinct exact constants with one image in F_p (or a nonzero multiple of
+    p): the field cannot separate what they scale, so the stage is LOSSY
+    (reported unknown) instead of closing or passing as equal."""
+    P = (1 << 31) - 1
+    e = engine.Engine(0, 1, (1, 2, 3))
+    for lhs, rhs in ((1, 1 - P), (P, 0), (2, 2 + P)):
+        c = e.add_stage(*_scale_check_program(lhs, rhs))
+        assert c.status == engine.STAGE_LOSSY, (lhs, rhs)
+    # the same constant on both sides still closes at compile time
+    c = e.add_stage(*_scale_check_program(3, 3))
+    assert c.status == engine.STAGE_PROVEN
+    e.close()
+
+
+def test_identities_fold_on_exact_values(lib):
+    """x * c with c congruent to 1 mod p but not 1 is not folded to x: no
+    compile-time proof of x == scale(x, 1 - p)."""
+    P = (1 << 31) - 1
+    e = engine.Engine(0, 1, (1, 2, 3))
+    c = e.add_stage(*_scale_check_program(None, 1 - P))
+    assert c.status != engine.STAGE_PROVEN
+    c = e.add_stage(*_scale_check_program(None, 1))
+    assert c.status == engine.STAGE_PROVEN
+    e.close()
