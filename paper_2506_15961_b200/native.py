@@ -40,7 +40,7 @@ import numpy as np
 from . import field as F
 from .engine import Engine, load_library
 from .errors import EngineError
-from .graph import Graph, Node
+from .graph import Graph
 from .plan import Plan
 from .stages import OPCODE, Stage
 
@@ -179,8 +179,7 @@ def _pack_tensors(tv: list) -> dict:
     for i in np.flatnonzero(is_int).tolist():
         flags[i] = 1 | (2 if tv[i].meta.get("enum") == "position" else 0)
     return dict(ndim=np.fromiter(map(len, shapes), np.int32, nt),
-                dims=np.fromiter(chain.from_iterable(shapes), np.int64), flags=flags,
-                tn=_zjoin(map(attrgetter("id"), tv), nt))
+                dims=np.fromiter(chain.from_iterable(shapes), np.int64), flags=flags)
 
 
 def _pack_nodes(nodes: list) -> dict:
@@ -236,7 +235,7 @@ def _pack_columns(g: Graph, consts: _Consts) -> tuple[dict, tuple[int, int, int]
         return cols, d["counts"]
     tv = list(g.tensors.values())
     t = _pack_tensors(tv)
-    t["tn"] = _zjoin(g.tensors, len(tv))
+    t["tn"] = _zjoin(g.tensors, len(tv))  # the dict keys: what node inputs name
     n = _pack_nodes(g.nodes)
     if n["consts"]:  # slice-local constant ids -> plan ids
         remap = np.array([consts(Fraction(a, b)) for a, b in n["consts"]], dtype=np.int64)
@@ -453,7 +452,3 @@ class NativePlan:
                                         ir.size, cs.ctypes.data_as(_I64P), cs.shape[0],
                                         vk.ctypes.data_as(C.POINTER(C.c_uint64)), vk.size, lens)
         return ir[: lens[0]], cs[: lens[1]], vk[: lens[2]]
-
-
-def node_of(plan: Plan, side: int, i: int) -> Node:
-    return (plan.parallel if side else plan.logical).nodes[i]
