@@ -184,6 +184,10 @@ def discharge_sharded(plan, stages: list[Stage] | None, opts, group=None,
             stats = {"error": repr(fail)}
         n_stages = len(stages)
     payload = [(i, r if isinstance(r, StageFailure) else r.as_dict()) for i, r in pairs]
+    if dist.get_backend(group) == "nccl":
+        # all_gather_object stages the pickles on the current CUDA device
+        import torch
+        torch.cuda.set_device(opts.device)
     gathered: list = [None] * world
     dist.all_gather_object(gathered, (payload, stats), group=group)
     results, cancelled = merge_results([g[0] for g in gathered], n_stages, opts.no_cancel)
