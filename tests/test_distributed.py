@@ -159,3 +159,25 @@ def test_two_rank_native_partition_is_consistent():
     assert c0 == c1 and ok0 == ok1
     assert all((c > 0) == o for c, o in zip(c0, ok0))
     assert n0 == sum(1 for i in p0[0] if ok0[i]) and n1 == sum(1 for i in p0[1] if ok0[i])
+
+
+def test_merge_raises_failures_in_stage_order():
+    """A stage whose discharge raised on some rank re-raises after the gather
+    only when the single-GPU loop would have reached it (reference
+    verify.py:115-126: the first refutation stops the loop unless no_cancel)."""
+    from paper_2506_15961_b200.distributed import StageFailure
+    from paper_2506_15961_b200.errors import GraphError
+
+    def res(t, status):
+        return StageResult(t, status, 1, 0, 1, 0.0).as_dict()
+
+    fail = StageFailure(GraphError("stage s2: logical side divides by zero"))
+    # rank 0 owns stages 0 and 2, rank 1 owns 1 and 3
+    late = [[(0, res("s0", "proven")), (2, fail)], [(1, res("s1", "refuted")), (3, res("s3", "proven"))]]
+    results, cancelled = merge_results(late, 4, no_cancel=False)
+    assert [r.status for r in results] == ["proven", "refuted"] and cancelled == 2
+    with pytest.raises(GraphError, match="divides by zero"):
+        merge_results(late, 4, no_cancel=True)
+    early = [[(0, fail), (2, res("s2", "proven"))], [(1, res("s1", "refuted")), (3, res("s3", "proven"))]]
+    with pytest.raises(GraphError):
+        merge_results(early, 4, no_cancel=False)
