@@ -15,8 +15,14 @@
 #include <structmember.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
+#include <new>
+#include <unordered_map>
+
+#include <sys/mman.h>
 #include <thread>
 #include <string>
 #include <vector>
@@ -256,15 +262,59 @@ void encode(int k, PyObject* a, PyObject* const_id, std::vector<long long>& w) {
 // the serial path below (which raises the proper Python errors) runs instead.
 // Rational attributes are numbered afterwards, serially, in node order.
 
-struct Cols {
-  std::string tn, ndim, dims, flags, ids, kind, nin, nout, ins, outs, nattr, attrs, device, seq;
+// Large buffers (the columns run to tens of MB): ask for transparent huge
+// pages, so first touch costs one fault per 2 MB instead of per 4 KB.
+void advise_huge(void* p, size_t n) {
+  constexpr uintptr_t H = 2u << 20;
+  if (n < 2 * H) return;
+  const uintptr_t a = (reinterpret_cast<uintptr_t>(p) + H - 1) & ~(H - 1);
+  const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + n) & ~(H - 1);
+  if (e > a) madvise(reinterpret_cast<void*>(a), e - a, MADV_HUGEPAGE);
+}
+
+// Growable byte buffer on malloc/realloc: large blocks grow by remapping
+// pages instead of copying them.
+struct Buf {
+  char* p = nullptr;
+  size_t n = 0, cap = 0;
+  Buf() = default;
+  Buf(const Buf&) = delete;
+  Buf& operator=(const Buf&) = delete;
+  ~Buf() { std::free(p); }
+  void grow(size_t need) {
+    size_t c = std::max<size_t>(4096, cap * 2);
+    while (c < need) c *= 2;
+    char* q = static_cast<char*>(std::realloc(p, c));
+    if (!q) throw std::bad_alloc();
+    p = q;
+    cap = c;
+    advise_huge(p, cap);
+  }
+  void append(const void* s, size_t k) {
+    if (n + k > cap) grow(n + k);
+    std::memcpy(p + n, s, k);
+    n += k;
+  }
+  void push_back(char c) {
+    if (n + 1 > cap) grow(n + 1);
+    p[n++] = c;
+  }
+};
+
+// the columns of pqw_graph_desc, in the order of the result dict
+enum Col { C_TN, C_NDIM, C_DIMS, C_FLAGS, C_IDS, C_KIND, C_NIN, C_NOUT, C_INS, C_OUTS,
+           C_NATTR, C_ATTRS, C_DEVICE, C_SEQ, NCOL };
+const char* const COL_NAMES[NCOL] = {"tn",  "ndim", "dims", "flags", "ids",   "kind",   "nin",
+                                     "nout", "ins", "outs", "nattr", "attrs", "device", "seq"};
+
+struct Cols {  // one worker's share (a contiguous range of tensors and of nodes)
+  Buf c[NCOL];
   std::vector<std::pair<size_t, PyObject*>> consts;  // (attr word index, value) to number
 };
 
-bool fast_str(PyObject* s, std::string& out) {
+bool fast_str(PyObject* s, Buf& out) {
   if (!s || !PyUnicode_Check(s) || !PyUnicode_IS_COMPACT_ASCII(s)) return false;
-  out.append((const char*)PyUnicode_DATA(s), (size_t)PyUnicode_GET_LENGTH(s));
-  out.push_back('\0');
+  out.append(PyUnicode_DATA(s), (size_t)PyUnicode_GET_LENGTH(s) + 1);  // with its NUL
   return true;
 }
 bool fast_int(PyObject* o, long long& x) {
@@ -425,13 +475,55 @@ struct KindTable {
   }
 };
 
+// per-worker memo of kind strings by object identity (the plan's kind
+// strings are a handful of shared objects)
+struct KindMemo {
+  PyObject* key[64] = {};
+  int val[64] = {};
+  int find(const KindTable& kt, PyObject* s) {
+    const size_t h = (reinterpret_cast<uintptr_t>(s) >> 4) & 63u;
+    if (s && key[h] == s) return val[h];
+    const int v = kt.find(s);
+    if (v >= -1) {
+      key[h] = s;
+      val[h] = v;
+    }
+    return v;
+  }
+};
+
 template <class T>
-void putv(std::string& out, T v) {
+void putv(Buf& out, T v) {
   out.append(reinterpret_cast<const char*>(&v), sizeof(T));
 }
 
+// PQW_TIMING=1: phase times on stderr
+void lap(const char* what) {
+  static const bool on = getenv("PQW_TIMING") != nullptr;
+  static auto t0 = std::chrono::steady_clock::now();
+  if (!on) return;
+  const auto t = std::chrono::steady_clock::now();
+  fprintf(stderr, "PQW_TIMING pack %s %.1f ms\n", what,
+          std::chrono::duration<double, std::milli>(t - t0).count());
+  t0 = t;
+}
+
+unsigned pack_threads(size_t work) {
+  unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  if (const char* e = getenv("PQW_THREADS")) nt = (unsigned)std::max(1, std::min(16, atoi(e)));
+  return work < 50000 ? 1u : nt;
+}
+
+template <class F>
+void on_threads(unsigned nt, F&& f) {
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < nt; ++t) pool.emplace_back(f, t);
+  f(0u);
+  for (auto& th : pool) th.join();
+}
+
 bool pack_fast(PyObject* tensors, PyObject* const* nodes, Py_ssize_t nn, const KindTable& kinds,
-               Cols& out) {
+               std::vector<Cols>& parts) {
   std::vector<std::pair<PyObject*, PyObject*>> tv;
   tv.reserve((size_t)PyDict_GET_SIZE(tensors));
   {
@@ -439,6 +531,7 @@ bool pack_fast(PyObject* tensors, PyObject* const* nodes, Py_ssize_t nn, const K
     PyObject *k, *v;
     while (PyDict_Next(tensors, &pos, &k, &v)) tv.push_back({k, v});
   }
+  lap("tensor list");
   PyObject* const tnames[3] = {S_shape, S_dtype, S_meta};
   PyObject* const nnames[7] = {S_id, S_kind, S_inputs, S_outputs, S_attrs, S_device, S_seq};
   Fields tf, nf;
@@ -455,28 +548,24 @@ bool pack_fast(PyObject* tensors, PyObject* const* nodes, Py_ssize_t nn, const K
   auto slot = [](PyObject* obj, const Fields& f, int i) {
     return *reinterpret_cast<PyObject**>(reinterpret_cast<char*>(obj) + f.off[i]);
   };
-  unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-  if (const char* e = getenv("PQW_THREADS")) nt = (unsigned)std::max(1, std::min(16, atoi(e)));
-  const size_t work = tv.size() + (size_t)nn;
-  if (work < 50000) nt = 1;
-  std::vector<Cols> parts(nt);
+  const unsigned nt = pack_threads(tv.size() + (size_t)nn);
+  parts = std::vector<Cols>(nt);
   std::vector<char> ok(nt, 1);
   auto run = [&](unsigned t) {
     Cols& c = parts[t];
+    std::vector<long long> sh, w;
+    KindMemo memo;
     const size_t t0 = tv.size() * t / nt, t1 = tv.size() * (t + 1) / nt;
     for (size_t i = t0; i < t1 && ok[t]; ++i) {
       PyObject* o = tv[i].second;
-      if (Py_TYPE(o) != tf.type || !fast_str(tv[i].first, c.tn)) {
+      sh.clear();
+      if (Py_TYPE(o) != tf.type || !fast_str(tv[i].first, c.c[C_TN]) ||
+          !fast_ints(slot(o, tf, 0), sh, false)) {
         ok[t] = 0;
         break;
       }
-      std::vector<long long> sh;
-      if (!fast_ints(slot(o, tf, 0), sh, false)) {
-        ok[t] = 0;
-        break;
-      }
-      putv<int32_t>(c.ndim, (int32_t)sh.size());
-      for (long long d : sh) putv<int64_t>(c.dims, d);
+      putv<int32_t>(c.c[C_NDIM], (int32_t)sh.size());
+      c.c[C_DIMS].append(sh.data(), sh.size() * sizeof(int64_t));
       uint8_t fl = 0;
       if (fast_ascii_eq(slot(o, tf, 1), "int")) {
         fl = 1;
@@ -487,22 +576,21 @@ bool pack_fast(PyObject* tensors, PyObject* const* nodes, Py_ssize_t nn, const K
         }
         if (fast_ascii_eq(fast_get(meta, "enum"), "position")) fl |= 2;
       }
-      c.flags.push_back((char)fl);
+      c.c[C_FLAGS].push_back((char)fl);
     }
     const size_t n0 = (size_t)nn * t / nt, n1 = (size_t)nn * (t + 1) / nt;
-    std::vector<long long> w;
     size_t words = 0;
     for (size_t i = n0; i < n1 && ok[t]; ++i) {
       PyObject* n = nodes[i];
-      bool good = Py_TYPE(n) == nf.type && fast_str(slot(n, nf, 0), c.ids);
-      const int k = good ? kinds.find(slot(n, nf, 1)) : -2;
+      bool good = Py_TYPE(n) == nf.type && fast_str(slot(n, nf, 0), c.c[C_IDS]);
+      const int k = good ? memo.find(kinds, slot(n, nf, 1)) : -2;
       good = good && k >= -1;
       PyObject** it = nullptr;
       Py_ssize_t ni = 0, no = 0;
       good = good && fast_seq(slot(n, nf, 2), it, ni);
-      for (Py_ssize_t j = 0; good && j < ni; ++j) good = fast_str(it[j], c.ins);
+      for (Py_ssize_t j = 0; good && j < ni; ++j) good = fast_str(it[j], c.c[C_INS]);
       good = good && fast_seq(slot(n, nf, 3), it, no);
-      for (Py_ssize_t j = 0; good && j < no; ++j) good = fast_str(it[j], c.outs);
+      for (Py_ssize_t j = 0; good && j < no; ++j) good = fast_str(it[j], c.c[C_OUTS]);
       w.clear();
       if (good && has_attrs(k)) {
         PyObject* at = slot(n, nf, 4);
@@ -516,33 +604,91 @@ bool pack_fast(PyObject* tensors, PyObject* const* nodes, Py_ssize_t nn, const K
         ok[t] = 0;
         break;
       }
-      putv<int32_t>(c.kind, k);
-      putv<int32_t>(c.nin, (int32_t)ni);
-      putv<int32_t>(c.nout, (int32_t)no);
-      putv<int32_t>(c.nattr, (int32_t)w.size());
-      for (long long x : w) putv<int64_t>(c.attrs, x);
+      putv<int32_t>(c.c[C_KIND], k);
+      putv<int32_t>(c.c[C_NIN], (int32_t)ni);
+      putv<int32_t>(c.c[C_NOUT], (int32_t)no);
+      putv<int32_t>(c.c[C_NATTR], (int32_t)w.size());
+      c.c[C_ATTRS].append(w.data(), w.size() * sizeof(int64_t));
       words += w.size();
-      putv<int32_t>(c.device, (int32_t)dv);
-      putv<int64_t>(c.seq, sq);
+      putv<int32_t>(c.c[C_DEVICE], (int32_t)dv);
+      putv<int64_t>(c.c[C_SEQ], sq);
     }
   };
-  {
-    std::vector<std::thread> pool;
-    for (unsigned t = 1; t < nt; ++t) pool.emplace_back(run, t);
-    run(0);
-    for (auto& th : pool) th.join();
-  }
+  on_threads(nt, [&](unsigned t) {
+    try {
+      run(t);
+    } catch (...) {  // out of memory: let the serial path raise
+      ok[t] = 0;
+    }
+  });
+  lap("workers");
   for (char o : ok)
     if (!o) return false;
-  size_t words = 0;
-  for (auto& c : parts) {
-    out.tn += c.tn; out.ndim += c.ndim; out.dims += c.dims; out.flags += c.flags;
-    out.ids += c.ids; out.kind += c.kind; out.nin += c.nin; out.nout += c.nout;
-    out.ins += c.ins; out.outs += c.outs; out.nattr += c.nattr; out.attrs += c.attrs;
-    out.device += c.device; out.seq += c.seq;
-    for (auto& q : c.consts) out.consts.push_back({words + q.first, q.second});
-    words += c.attrs.size() / sizeof(int64_t);
+  return true;
+}
+
+// The workers' shares, concatenated straight into new bytes objects (one
+// parallel copy, pages first touched on the workers); rational attributes
+// then numbered through const_id in node order. Returns false with a Python
+// error set.
+bool gather_parts(std::vector<Cols>& parts, PyObject* const_id, PyObject* out[NCOL]) {
+  const size_t nt = parts.size();
+  std::vector<size_t> off((nt + 1) * NCOL, 0);
+  for (int k = 0; k < NCOL; ++k)
+    for (size_t t = 0; t < nt; ++t) off[(t + 1) * NCOL + k] = off[t * NCOL + k] + parts[t].c[k].n;
+  for (int k = 0; k < NCOL; ++k) {
+    out[k] = PyBytes_FromStringAndSize(nullptr, (Py_ssize_t)off[nt * NCOL + k]);
+    if (!out[k]) return false;
   }
+  char* dst[NCOL];
+  for (int k = 0; k < NCOL; ++k) {
+    dst[k] = PyBytes_AS_STRING(out[k]);
+    advise_huge(dst[k], (size_t)PyBytes_GET_SIZE(out[k]));
+  }
+  on_threads((unsigned)nt, [&](unsigned t) {
+    for (int k = 0; k < NCOL; ++k)
+      if (parts[t].c[k].n) std::memcpy(dst[k] + off[t * NCOL + k], parts[t].c[k].p, parts[t].c[k].n);
+  });
+  lap("gather");
+  // const_id is a function of the exact value: memoise it per exact int /
+  // float value, and per object for anything else (Fraction, numpy scalars)
+  struct Key {
+    uint64_t tag, bits;
+    bool operator==(const Key& o) const { return tag == o.tag && bits == o.bits; }
+  };
+  struct KeyHash {
+    size_t operator()(const Key& k) const { return std::hash<uint64_t>()(k.bits * 0x9E3779B97F4A7C15ull ^ k.tag); }
+  };
+  std::unordered_map<Key, int64_t, KeyHash> memo;
+  for (size_t t = 0; t < nt; ++t) {
+    const size_t word0 = off[t * NCOL + C_ATTRS] / sizeof(int64_t);
+    for (auto& q : parts[t].consts) {
+      PyObject* v = q.second;
+      Key key{3, reinterpret_cast<uintptr_t>(v)};
+      long long x;
+      if (PyFloat_CheckExact(v)) {
+        const double d = PyFloat_AS_DOUBLE(v);
+        key = {1, 0};
+        std::memcpy(&key.bits, &d, sizeof(d));
+      } else if (fast_int(v, x)) {
+        key = {2, static_cast<uint64_t>(x)};
+      }
+      auto it = memo.find(key);
+      int64_t id;
+      if (it != memo.end()) {
+        id = it->second;
+      } else {
+        PyObject* r = PyObject_CallOneArg(const_id, v);
+        if (!r) return false;
+        id = PyLong_AsLongLong(r);
+        Py_DECREF(r);
+        if (id == -1 && PyErr_Occurred()) return false;
+        memo.emplace(key, id);
+      }
+      std::memcpy(dst[C_ATTRS] + (word0 + q.first) * sizeof(int64_t), &id, sizeof(id));
+    }
+  }
+  lap("constants");
   return true;
 }
 
@@ -550,9 +696,12 @@ bool pack_fast(PyObject* tensors, PyObject* const* nodes, Py_ssize_t nn, const K
 PyObject* pack_graph(PyObject*, PyObject* args) {
   PyObject *g, *opcodes, *const_id;
   if (!PyArg_ParseTuple(args, "OO!O", &g, &PyDict_Type, &opcodes, &const_id)) return nullptr;
+  PyObject* cols[NCOL] = {};
+  lap("start");
+  auto release = [&] {
+    for (auto& o : cols) Py_CLEAR(o);
+  };
   try {
-    std::string tn, ndim, dims, flags;
-    std::string ids, kind, nin, nout, ins, outs, nattr, attrs, device, seq;
     Ref tensors(PyObject_GetAttr(g, S_tensors));
     if (!PyDict_Check(tensors.p)) {
       PyErr_SetString(PyExc_TypeError, "graph.tensors is not a dict");
@@ -577,35 +726,27 @@ PyObject* pack_graph(PyObject*, PyObject* args) {
         }
         kt.kv.push_back({std::string((const char*)PyUnicode_DATA(kk)), (int)c});
       }
-      Cols c;
-      if (tab_ok && pack_fast(tensors.p, nv, nn, kt, c)) {
+      std::vector<Cols> parts;
+      if (tab_ok && pack_fast(tensors.p, nv, nn, kt, parts)) {
+        if (!gather_parts(parts, const_id, cols)) throw Err{};
         fast = true;
-        tn.swap(c.tn); ndim.swap(c.ndim); dims.swap(c.dims); flags.swap(c.flags);
-        ids.swap(c.ids); kind.swap(c.kind); nin.swap(c.nin); nout.swap(c.nout);
-        ins.swap(c.ins); outs.swap(c.outs); nattr.swap(c.nattr); attrs.swap(c.attrs);
-        device.swap(c.device); seq.swap(c.seq);
-        for (auto& q : c.consts) {  // rational attributes, numbered in node order
-          Ref r(PyObject_CallOneArg(const_id, q.second));
-          const int64_t id = as_int(r.p);
-          std::memcpy(&attrs[q.first * sizeof(int64_t)], &id, sizeof(id));
-        }
       }
     }
     if (!fast) {
-    tn.clear(); ndim.clear(); dims.clear(); flags.clear();
+    std::string c[NCOL];
     nt = 0;
     Py_ssize_t pos = 0;
     PyObject *key, *t;
     PyObject* const tnames[3] = {S_shape, S_dtype, S_meta};
     Fields tf;
     while (PyDict_Next(tensors.p, &pos, &key, &t)) {
-      put_str(tn, key);
+      put_str(c[C_TN], key);
       Ref shape(field(t, tf, 0, tnames, 3));
       Ref f(PySequence_Fast(shape.p, "shape"));
       const Py_ssize_t r = PySequence_Fast_GET_SIZE(f.p);
-      put<int32_t>(ndim, (int32_t)r);
+      put<int32_t>(c[C_NDIM], (int32_t)r);
       PyObject** it = PySequence_Fast_ITEMS(f.p);
-      for (Py_ssize_t i = 0; i < r; ++i) put<int64_t>(dims, as_int(it[i]));
+      for (Py_ssize_t i = 0; i < r; ++i) put<int64_t>(c[C_DIMS], as_int(it[i]));
       Ref dt(field(t, tf, 1, tnames, 3));
       uint8_t fl = 0;
       if (PyUnicode_Check(dt.p) && PyUnicode_CompareWithASCIIString(dt.p, "int") == 0) {
@@ -615,7 +756,7 @@ PyObject* pack_graph(PyObject*, PyObject* args) {
         if (en && PyUnicode_Check(en) && PyUnicode_CompareWithASCIIString(en, "position") == 0)
           fl |= 2;
       }
-      flags.push_back((char)fl);
+      c[C_FLAGS].push_back((char)fl);
       ++nt;
     }
     std::vector<long long> w;
@@ -624,21 +765,21 @@ PyObject* pack_graph(PyObject*, PyObject* args) {
     for (Py_ssize_t i = 0; i < nn; ++i) {
       PyObject* n = nv[i];
       Ref id(field(n, nf, 0, nnames, 7));
-      put_str(ids, id.p);
+      put_str(c[C_IDS], id.p);
       Ref kd(field(n, nf, 1, nnames, 7));
       PyObject* code = PyDict_GetItem(opcodes, kd.p);
       const int k = code ? (int)PyLong_AsLong(code) : -1;
-      put<int32_t>(kind, k);
+      put<int32_t>(c[C_KIND], k);
       Ref in(field(n, nf, 2, nnames, 7));
       Ref inf(PySequence_Fast(in.p, "inputs"));
       const Py_ssize_t ni = PySequence_Fast_GET_SIZE(inf.p);
-      for (Py_ssize_t j = 0; j < ni; ++j) put_str(ins, PySequence_Fast_GET_ITEM(inf.p, j));
-      put<int32_t>(nin, (int32_t)ni);
+      for (Py_ssize_t j = 0; j < ni; ++j) put_str(c[C_INS], PySequence_Fast_GET_ITEM(inf.p, j));
+      put<int32_t>(c[C_NIN], (int32_t)ni);
       Ref out(field(n, nf, 3, nnames, 7));
       Ref outf(PySequence_Fast(out.p, "outputs"));
       const Py_ssize_t no = PySequence_Fast_GET_SIZE(outf.p);
-      for (Py_ssize_t j = 0; j < no; ++j) put_str(outs, PySequence_Fast_GET_ITEM(outf.p, j));
-      put<int32_t>(nout, (int32_t)no);
+      for (Py_ssize_t j = 0; j < no; ++j) put_str(c[C_OUTS], PySequence_Fast_GET_ITEM(outf.p, j));
+      put<int32_t>(c[C_NOUT], (int32_t)no);
       w.clear();
       if (has_attrs(k)) {
         Ref at(field(n, nf, 4, nnames, 7));
@@ -648,46 +789,34 @@ PyObject* pack_graph(PyObject*, PyObject* args) {
         }
         encode(k, at.p, const_id, w);
       }
-      put<int32_t>(nattr, (int32_t)w.size());
-      for (long long x : w) put<int64_t>(attrs, x);
+      put<int32_t>(c[C_NATTR], (int32_t)w.size());
+      for (long long x : w) put<int64_t>(c[C_ATTRS], x);
       Ref dv(field(n, nf, 5, nnames, 7));
-      put<int32_t>(device, dv.p == Py_None ? -1 : (int32_t)as_int(dv.p));
+      put<int32_t>(c[C_DEVICE], dv.p == Py_None ? -1 : (int32_t)as_int(dv.p));
       Ref sq(field(n, nf, 6, nnames, 7));
-      put<int64_t>(seq, as_int(sq.p));
+      put<int64_t>(c[C_SEQ], as_int(sq.p));
     }
+    for (int k = 0; k < NCOL; ++k)
+      if (!(cols[k] = bytes_of(c[k]))) throw Err{};
     }  // serial path
     std::string gin;
     Ref gi(PyObject_GetAttr(g, S_inputs_g));
     Ref gif(PySequence_Fast(gi.p, "graph.inputs"));
     const Py_ssize_t ng = PySequence_Fast_GET_SIZE(gif.p);
     for (Py_ssize_t j = 0; j < ng; ++j) put_str(gin, PySequence_Fast_GET_ITEM(gif.p, j));
-    PyObject* d = PyDict_New();
-    if (!d) throw Err{};
-    auto set = [&](const char* k, const std::string& v) {
-      PyObject* b = bytes_of(v);
-      if (!b || PyDict_SetItemString(d, k, b) < 0) {
-        Py_XDECREF(b);
-        throw Err{};
-      }
-      Py_DECREF(b);
-    };
-    try {
-      set("tn", tn); set("ndim", ndim); set("dims", dims); set("flags", flags);
-      set("ids", ids); set("kind", kind); set("nin", nin); set("nout", nout);
-      set("ins", ins); set("outs", outs); set("nattr", nattr); set("attrs", attrs);
-      set("device", device); set("seq", seq); set("inputs", gin);
-      PyObject* cnt = Py_BuildValue("(LnL)", nt, nn, (long long)ng);
-      if (!cnt || PyDict_SetItemString(d, "counts", cnt) < 0) {
-        Py_XDECREF(cnt);
-        throw Err{};
-      }
-      Py_DECREF(cnt);
-    } catch (const Err&) {
-      Py_DECREF(d);
-      throw;
-    }
-    return d;
+    Ref d(PyDict_New());
+    for (int k = 0; k < NCOL; ++k)
+      if (PyDict_SetItemString(d.p, COL_NAMES[k], cols[k]) < 0) throw Err{};
+    Ref gb(bytes_of(gin));
+    if (PyDict_SetItemString(d.p, "inputs", gb.p) < 0) throw Err{};
+    Ref cnt(Py_BuildValue("(LnL)", nt, nn, (long long)ng));
+    if (PyDict_SetItemString(d.p, "counts", cnt.p) < 0) throw Err{};
+    release();
+    lap("dict");
+    Py_INCREF(d.p);
+    return d.p;
   } catch (const Err&) {
+    release();
     if (!PyErr_Occurred()) PyErr_SetString(PyExc_ValueError, "graph not packable");
     return nullptr;
   }

@@ -14,6 +14,7 @@
 // Any input the reference would reject yields PQW_EPLAN; the Python host then
 // runs its own checks, which raise the reference's exception and message.
 #include <sched.h>
+#include <sys/mman.h>
 
 #include <algorithm>
 #include <chrono>
@@ -29,6 +30,7 @@
 #include <string>
 #include <string_view>
 #include <thread>
+#include <type_traits>
 #include <unordered_map>
 #include <vector>
 
@@ -66,19 +68,44 @@ int64_t pymod(int64_t a, int64_t m) {
   return r < 0 ? r + m : r;
 }
 
-void split_names(const char* s, int64_t n, std::string& store, std::vector<std::string_view>& out) {
-  // copy the NUL-separated names once, then view into the copy
-  size_t len = 0;
-  for (int64_t i = 0; i < n; ++i) len += std::strlen(s + len) + 1;
-  store.assign(s, len);
-  out.resize((size_t)n);
-  size_t off = 0;
-  for (int64_t i = 0; i < n; ++i) {
-    size_t l = std::strlen(store.data() + off);
-    out[(size_t)i] = std::string_view(store.data() + off, l);
-    off += l + 1;
+// Storage of the plan's big columns (tens of MB on the 405B plan): no
+// value-initialisation on resize -- the columns are filled by parallel copies,
+// so their pages are first touched on the workers -- and transparent huge
+// pages for blocks of 4 MB and more.
+template <class T>
+struct ColAlloc {
+  using value_type = T;
+  static constexpr size_t BIG = 4u << 20, H = 2u << 20;
+  ColAlloc() = default;
+  template <class U>
+  ColAlloc(const ColAlloc<U>&) {}
+  T* allocate(size_t n) {
+    const size_t b = n * sizeof(T);
+    if (b < BIG) return static_cast<T*>(::operator new(b));
+    const size_t r = (b + H - 1) & ~(H - 1);
+    void* q = std::aligned_alloc(H, r);
+    if (!q) throw std::bad_alloc();
+    madvise(q, r, MADV_HUGEPAGE);
+    return static_cast<T*>(q);
   }
-}
+  void deallocate(T* q, size_t n) {
+    if (n * sizeof(T) < BIG)
+      ::operator delete(q);
+    else
+      std::free(q);
+  }
+  template <class U, class... A>
+  void construct(U* q, A&&... a) {
+    if constexpr (sizeof...(A) == 0 && std::is_trivially_copyable_v<U>)
+      return;  // left for the filling copy
+    else
+      ::new (static_cast<void*>(q)) U(std::forward<A>(a)...);
+  }
+  friend bool operator==(const ColAlloc&, const ColAlloc&) { return true; }
+  friend bool operator!=(const ColAlloc&, const ColAlloc&) { return false; }
+};
+template <class T>
+using Col = std::vector<T, ColAlloc<T>>;
 
 unsigned host_threads(size_t work) {
   unsigned nt = std::max(1u, std::thread::hardware_concurrency());
@@ -105,12 +132,85 @@ void parallel_for(size_t n, F&& f) {
   for (auto& t : pool) t.join();
 }
 
+template <class T, class A>
+void par_copy(std::vector<T, A>& v, const T* src, size_t n) {
+  v.resize(n);
+  const size_t chunk = (1u << 20) / sizeof(T);
+  parallel_for((n + chunk - 1) / chunk, [&](size_t c, unsigned) {
+    const size_t a = c * chunk, e = std::min(n, a + chunk);
+    std::memcpy(v.data() + a, src + a, (e - a) * sizeof(T));
+  });
+}
+
+// Byte length of n NUL-terminated names: a word-at-a-time count of the NULs
+// (aligned 8-byte reads never cross into a page past the buffer's last one).
+size_t names_len(const char* s, int64_t n) {
+  if (n <= 0) return 0;
+  const char* p = s;
+  int64_t left = n;
+  while ((reinterpret_cast<uintptr_t>(p) & 7u) != 0) {
+    if (*p++ == 0 && --left == 0) return (size_t)(p - s);
+  }
+  constexpr uint64_t L7 = 0x7F7F7F7F7F7F7F7Full;
+  for (;;) {
+    uint64_t w;
+    std::memcpy(&w, p, 8);
+    const uint64_t z = ~(((w & L7) + L7) | w | L7);  // 0x80 in every zero byte
+    const int c = __builtin_popcountll(z);
+    if (c < left) {
+      left -= c;
+      p += 8;
+      continue;
+    }
+    for (int b = 0; b < 8; ++b)
+      if (p[b] == 0 && --left == 0) return (size_t)(p + b + 1 - s);
+  }
+}
+
+// K chunks of a names buffer cut at name boundaries, with the index of each
+// chunk's first name (cut and first have K + 1 entries).
+void cut_names(const char* s, size_t len, unsigned K, std::vector<size_t>& cut,
+               std::vector<size_t>& first) {
+  cut.assign(K + 1, len);
+  cut[0] = 0;
+  for (unsigned k = 1; k < K; ++k) {
+    size_t c = std::max(len * k / K, cut[k - 1]);
+    while (c < len && c > 0 && s[c - 1] != 0) ++c;  // start right after a NUL
+    cut[k] = c;
+  }
+  first.assign(K + 1, 0);
+  parallel_for(K, [&](size_t k, unsigned) {
+    size_t c = 0;
+    for (size_t i = cut[k]; i < cut[k + 1]; ++i) c += s[i] == 0;
+    first[k + 1] = c;
+  });
+  for (unsigned k = 0; k < K; ++k) first[k + 1] += first[k];
+}
+
+// copy the n NUL-separated names once, then view into the copy
+void split_names(const char* s, int64_t n, Col<char>& store, Col<std::string_view>& out) {
+  const size_t len = names_len(s, n);
+  par_copy(store, s, len);
+  out.resize((size_t)n);
+  const unsigned K = host_threads(std::max<size_t>(1, len / (1u << 20)));
+  std::vector<size_t> cut, first;
+  cut_names(store.data(), len, K, cut, first);
+  parallel_for(K, [&](size_t k, unsigned) {
+    size_t idx = first[k];
+    for (size_t i = cut[k]; i < cut[k + 1] && idx < (size_t)n; ++idx) {
+      const size_t l = std::strlen(store.data() + i);
+      out[idx] = std::string_view(store.data() + i, l);
+      i += l + 1;
+    }
+  });
+}
+
 // Open-addressing name -> index table, built in parallel (CAS on the slots)
 // and then read from many threads.
 struct NameTable {
-  std::vector<uint64_t> hs;                    // hash per name index
+  Col<uint64_t> hs;                            // hash per name index
   std::unique_ptr<std::atomic<int32_t>[]> slot;  // name index per slot, -1 empty
-  const std::vector<std::string_view>* names = nullptr;
+  const Col<std::string_view>* names = nullptr;
   uint64_t mask = 0;
 
   static uint64_t h(std::string_view s) {
@@ -126,13 +226,13 @@ struct NameTable {
     return mix64(x ^ s.size());
   }
   // returns false on a duplicate name
-  bool build(const std::vector<std::string_view>& ns) {
+  bool build(const Col<std::string_view>& ns) {
     names = &ns;
     size_t cap = 16;
     while (cap < ns.size() * 2) cap <<= 1;
     mask = cap - 1;
     slot.reset(new std::atomic<int32_t>[cap]);
-    hs.assign(ns.size(), 0);
+    hs.resize(ns.size());
     const size_t chunk = 65536;
     const size_t nc = (std::max(ns.size(), cap) + chunk - 1) / chunk;
     parallel_for(nc, [&](size_t c, unsigned) {
@@ -170,16 +270,16 @@ struct NameTable {
 };
 
 struct GraphData {
-  std::string tstore, nstore, istore, ostore, gstore;
-  std::vector<std::string_view> tname, nid;
-  std::vector<int64_t> dim_off, dims;
-  std::vector<uint8_t> tflags;
-  std::vector<int32_t> kind;
-  std::vector<int64_t> in_off, out_off, attr_off;
-  std::vector<int32_t> ins, outs;  // tensor indices, -1 unresolved
-  std::vector<int64_t> attrs;
-  std::vector<int32_t> device;
-  std::vector<int64_t> seq;
+  Col<char> tstore, nstore;
+  Col<std::string_view> tname, nid;
+  Col<int64_t> dim_off, dims;
+  Col<uint8_t> tflags;
+  Col<int32_t> kind;
+  Col<int64_t> in_off, out_off, attr_off;
+  Col<int32_t> ins, outs;  // tensor indices, -1 unresolved
+  Col<int64_t> attrs;
+  Col<int32_t> device;
+  Col<int64_t> seq;
   std::vector<uint8_t> is_input;
   std::vector<int32_t> producer;   // tensor -> node, -1 none
   NameTable index;
@@ -203,38 +303,21 @@ struct GraphData {
   // n NUL-terminated names -> tensor indices, read in place: the buffer is cut
   // into chunks at name boundaries, names counted per chunk, then resolved in
   // parallel (no copy of the names is kept)
-  void resolve(const char* names, int64_t n, std::string& /*unused*/, std::vector<int32_t>& out) {
-    out.assign((size_t)n, -1);
+  template <class V>
+  void resolve(const char* names, int64_t n, V& out) {
+    out.resize((size_t)n);
     if (n == 0) return;
-    size_t len = 0;
-    for (int64_t i = 0; i < n; ++i) {
-      const void* z = std::memchr(names + len, 0, SIZE_MAX >> 1);
-      len = (size_t)((const char*)z - names) + 1;
-    }
+    const size_t len = names_len(names, n);
     const unsigned K = host_threads(std::max<size_t>(1, len / (1u << 20)));
-    std::vector<size_t> cut(K + 1, len);
-    cut[0] = 0;
-    for (unsigned k = 1; k < K; ++k) {
-      size_t c = len * k / K;
-      if (c < cut[k - 1]) c = cut[k - 1];
-      while (c < len && c > 0 && names[c - 1] != 0) ++c;  // start right after a NUL
-      cut[k] = c;
-    }
-    std::vector<size_t> cnt(K + 1, 0);
-    parallel_for(K, [&](size_t k, unsigned) {
-      size_t c = 0;
-      for (size_t i = cut[k]; i < cut[k + 1]; ++i) c += names[i] == 0;
-      cnt[k + 1] = c;
-    });
-    for (unsigned k = 0; k < K; ++k) cnt[k + 1] += cnt[k];
+    std::vector<size_t> cut, first;
+    cut_names(names, len, K, cut, first);
     std::atomic<bool> all{true};
     parallel_for(K, [&](size_t k, unsigned) {
-      size_t idx = cnt[k];
-      for (size_t i = cut[k]; i < cut[k + 1] && idx < (size_t)n;) {
+      size_t idx = first[k];
+      for (size_t i = cut[k]; i < cut[k + 1] && idx < (size_t)n; ++idx) {
         const size_t l = std::strlen(names + i);
         out[idx] = find(std::string_view(names + i, l));
         if (out[idx] < 0) all = false;
-        ++idx;
         i += l + 1;
       }
     });
@@ -259,33 +342,34 @@ struct GraphData {
       problem = "duplicate tensor id";
     }
     lap("tensor table");
-    dim_off.assign((size_t)d.n_tensors + 1, 0);
+    dim_off.resize((size_t)d.n_tensors + 1);
+    dim_off[0] = 0;
     for (int64_t i = 0; i < d.n_tensors; ++i) dim_off[i + 1] = dim_off[i] + d.tensor_ndim[i];
-    dims.assign(d.tensor_dims, d.tensor_dims + dim_off.back());
-    tflags.assign(d.tensor_flags, d.tensor_flags + d.n_tensors);
+    par_copy(dims, d.tensor_dims, (size_t)dim_off.back());
+    par_copy(tflags, d.tensor_flags, (size_t)d.n_tensors);
     const size_t n = (size_t)d.n_nodes;
     split_names(d.node_ids, d.n_nodes, nstore, nid);
-    kind.assign(d.node_kind, d.node_kind + n);
-    device.assign(d.node_device, d.node_device + n);
-    seq.assign(d.node_seq, d.node_seq + n);
-    in_off.assign(n + 1, 0);
-    out_off.assign(n + 1, 0);
-    attr_off.assign(n + 1, 0);
+    par_copy(kind, d.node_kind, n);
+    par_copy(device, d.node_device, n);
+    par_copy(seq, d.node_seq, n);
+    in_off.resize(n + 1);
+    out_off.resize(n + 1);
+    attr_off.resize(n + 1);
+    in_off[0] = out_off[0] = attr_off[0] = 0;
     for (size_t i = 0; i < n; ++i) {
       in_off[i + 1] = in_off[i] + d.node_nin[i];
       out_off[i + 1] = out_off[i] + d.node_nout[i];
       attr_off[i + 1] = attr_off[i] + d.node_nattr[i];
     }
-    attrs.assign(d.node_attrs, d.node_attrs + attr_off[n]);
+    par_copy(attrs, d.node_attrs, (size_t)attr_off[n]);
     lap("node columns");
-    resolve(d.node_inputs, in_off[n], istore, ins);
-    resolve(d.node_outputs, out_off[n], ostore, outs);
+    resolve(d.node_inputs, in_off[n], ins);
+    resolve(d.node_outputs, out_off[n], outs);
     lap("resolve io");
     {
       std::vector<int32_t> gin;
-      std::string gs;
       const bool keep = resolved;
-      resolve(d.input_names, d.n_inputs, gs, gin);
+      resolve(d.input_names, d.n_inputs, gin);
       resolved = keep;  // graph.inputs may name anything (it is only a set of ids)
       is_input.assign(nt(), 0);
       for (int32_t t : gin)
@@ -1272,8 +1356,8 @@ int pqw_plan_create(const pqw_graph_desc* logical, const pqw_graph_desc* paralle
     p->L.load(*logical);
     p->P.load(*parallel);
     p->consts.assign(consts, consts + 3 * n_consts);
-    std::vector<std::string_view> lnames, snames;
-    std::string ls, ss;
+    pqw::Col<std::string_view> lnames, snames;
+    pqw::Col<char> ls, ss;
     pqw::split_names(lineage->logical_names, lineage->n_entries, ls, lnames);
     int64_t n_sh = 0;
     for (int64_t i = 0; i < lineage->n_entries; ++i) n_sh += lineage->n_shards[i];
