@@ -39,6 +39,15 @@
 
 namespace pqw {
 int set_last_error(int code, const std::string& msg);  // witness_kernel.cu (pqw_last_error)
+// engine side of pqw_stage_add (witness_kernel.cu)
+uint64_t program_hash(const int32_t* ir, size_t ir_len, const int64_t* consts, size_t n_consts,
+                      size_t n_vars);
+bool cached_program(const pqw_engine* e, uint64_t h, const std::vector<int32_t>** ir,
+                    const std::vector<int64_t>** consts, int* stage);
+int stage_add_hashed(pqw_engine* e, const int32_t* ir, size_t ir_len, const int64_t* consts,
+                     size_t n_consts, const uint64_t* var_keys, size_t n_vars, uint64_t h,
+                     int same, std::vector<int32_t>* own_ir, std::vector<int64_t>* own_consts,
+                     int64_t out_status[16]);
 namespace {
 
 int pfail(int code, const std::string& msg) { return set_last_error(code, msg); }
@@ -1513,15 +1522,78 @@ int pqw_plan_add_stages(pqw_plan* p, pqw_engine* e, uint64_t seed, const int32_t
   }
   for (int32_t s : list)
     if (s < 0 || (size_t)s >= p->stages.size()) return pfail(PQW_EINVAL, "bad stage index");
+  static const bool timing = getenv("PQW_TIMING") != nullptr;
+  auto lap = [t = std::chrono::steady_clock::now()](const char* what) mutable {
+    const auto now = std::chrono::steady_clock::now();
+    if (timing)
+      fprintf(stderr, "PQW_TIMING add_stages %s %.1f ms\n", what,
+              std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  };
+  // Lower every stage and hash its program on host threads; group equal
+  // hashes in order (the representative: the engine's cached program, else
+  // the batch's first); confirm equal texts on host threads; then queue in
+  // order, passing the verified duplicate so the engine neither hashes nor
+  // compares again. Only representatives' texts are kept.
   std::vector<pqw::Program> progs(n);
+  std::vector<uint64_t> hash(n, 0);
   std::vector<char> bad(n, 0);
   pqw::parallel_for(n, [&](size_t i, unsigned) {
     try {
       progs[i] = pqw::lower_stage(p, list[i], seed);
+      const auto& pg = progs[i];
+      hash[i] = pqw::program_hash(pg.ir.data(), pg.ir.size(), pg.consts.data(),
+                                  pg.consts.size() / 3, pg.var_keys.size());
     } catch (const std::exception&) {
       bad[i] = 1;
     }
   });
+  lap("lower+hash");
+  // rep[i]: -1 none (first of its hash), >= 0 batch index, <= -2 engine stage -(s + 2)
+  std::vector<int64_t> rep(n, -1);
+  {
+    std::unordered_map<uint64_t, int64_t> first;
+    first.reserve(n);
+    for (size_t i = 0; i < n; ++i) {
+      if (bad[i]) continue;
+      auto it = first.find(hash[i]);
+      if (it != first.end()) {
+        rep[i] = it->second;
+        continue;
+      }
+      const std::vector<int32_t>* cir;
+      const std::vector<int64_t>* cco;
+      int st;
+      if (pqw::cached_program(e, hash[i], &cir, &cco, &st)) {
+        rep[i] = -(int64_t)st - 2;
+        first.emplace(hash[i], rep[i]);
+      } else {
+        first.emplace(hash[i], (int64_t)i);
+      }
+    }
+  }
+  std::vector<char> same(n, 0);
+  pqw::parallel_for(n, [&](size_t i, unsigned) {
+    if (rep[i] == -1) return;
+    const std::vector<int32_t>* rir;
+    const std::vector<int64_t>* rco;
+    if (rep[i] >= 0) {
+      rir = &progs[(size_t)rep[i]].ir;
+      rco = &progs[(size_t)rep[i]].consts;
+    } else {
+      int st;
+      pqw::cached_program(e, hash[i], &rir, &rco, &st);
+    }
+    same[i] = *rir == progs[i].ir && *rco == progs[i].consts;
+  });
+  pqw::parallel_for(n, [&](size_t i, unsigned) {  // duplicates' texts are not needed
+    if (same[i] && rep[i] != -1) {
+      std::vector<int32_t>().swap(progs[i].ir);
+      std::vector<int64_t>().swap(progs[i].consts);
+    }
+  });
+  lap("dedup");
+  std::vector<int> eidx(n, -1);
   int64_t status[16];
   for (size_t i = 0; i < n; ++i) {
     if (bad[i]) {
@@ -1529,13 +1601,17 @@ int pqw_plan_add_stages(pqw_plan* p, pqw_engine* e, uint64_t seed, const int32_t
       continue;
     }
     auto& pg = progs[i];
-    const int idx = pqw_stage_add(e, pg.ir.data(), pg.ir.size(), pg.consts.data(),
-                                  pg.consts.size() / 3, pg.var_keys.data(), pg.var_keys.size(),
-                                  status);
+    int s_same = -1;
+    if (same[i]) s_same = rep[i] >= 0 ? eidx[(size_t)rep[i]] : (int)(-rep[i] - 2);
+    const int idx = pqw::stage_add_hashed(e, pg.ir.data(), pg.ir.size(), pg.consts.data(),
+                                          pg.consts.size() / 3, pg.var_keys.data(),
+                                          pg.var_keys.size(), hash[i], s_same, &pg.ir,
+                                          &pg.consts, status);
     if (idx < 0) return idx;
     out_index[i] = idx;
-    pqw::Program().ir.swap(pg.ir);
+    eidx[i] = idx;
   }
+  lap("queue");
   return PQW_OK;
 }
 

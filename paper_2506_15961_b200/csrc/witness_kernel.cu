@@ -295,53 +295,75 @@ void pqw_engine_destroy(pqw_engine* e) {
   delete e;
 }
 
-int pqw_stage_add(pqw_engine* e, const int32_t* ir, size_t ir_len, const int64_t* consts,
-                  size_t n_consts, const uint64_t* var_keys, size_t n_vars,
-                  int64_t out_status[16]) {
-  if (!e || !ir || !out_status) return fail(PQW_EINVAL, "null argument");
-  if (n_vars && !var_keys) return fail(PQW_EINVAL, "null var_keys");
-  if (n_consts && !consts) return fail(PQW_EINVAL, "null consts");
-  if (ir_len < 4 || ir[0] != 0x50515701) return fail(PQW_EINVAL, "stage compile: bad program magic");
-  const uint32_t base = (uint32_t)e->var_keys.size();
-  const int idx = (int)e->stages.size();
-  // identical programs (e.g. the same layer repeated) compile once: the cache
-  // key is the program text; a hit shares the compiled program and only
-  // rebases vars. The compilation itself is deferred: every distinct program
-  // is compiled on a host thread pool at the first pqw_stage_status,
-  // pqw_upload or inspection call.
-  // (a cheap multiply-xorshift over 64-bit words: this runs over every stage's
-  // text, the full mix only finalises)
+}  // extern "C"
+
+namespace pqw {
+// Key of the program cache: a cheap multiply-xorshift over the text's 64-bit
+// words (it runs over every stage's text), the full mix only finalises.
+uint64_t program_hash(const int32_t* ir, size_t ir_len, const int64_t* consts, size_t n_consts,
+                      size_t n_vars) {
   auto absorb = [](uint64_t h, uint64_t w) {
     h = (h ^ w) * 0x9E3779B97F4A7C15ull;
     return h ^ (h >> 29);
   };
   uint64_t h = 0x5157ull ^ ir_len ^ ((uint64_t)n_consts << 32) ^ ((uint64_t)n_vars << 48);
-  {
-    size_t i = 0;
-    for (; i + 2 <= ir_len; i += 2) {
-      uint64_t w;
-      std::memcpy(&w, ir + i, 8);
-      h = absorb(h, w);
-    }
-    if (i < ir_len) h = absorb(h, (uint32_t)ir[i]);
-    for (size_t j = 0; j < 3 * n_consts; ++j) h = absorb(h, (uint64_t)consts[j]);
-    h = pqw::mix64(h);
+  size_t i = 0;
+  for (; i + 2 <= ir_len; i += 2) {
+    uint64_t w;
+    std::memcpy(&w, ir + i, 8);
+    h = absorb(h, w);
   }
-  int alias = -1;
+  if (i < ir_len) h = absorb(h, (uint32_t)ir[i]);
+  for (size_t j = 0; j < 3 * n_consts; ++j) h = absorb(h, (uint64_t)consts[j]);
+  return mix64(h);
+}
+
+// The program text the engine caches under hash h and the stage compiled
+// from it; false if none.
+bool cached_program(const pqw_engine* e, uint64_t h, const std::vector<int32_t>** ir,
+                    const std::vector<int64_t>** consts, int* stage) {
   auto it = e->cache.find(h);
-  if (it != e->cache.end()) {
-    const auto& ent = e->cache_src[it->second];
-    if (ent.first.size() == ir_len && std::equal(ent.first.begin(), ent.first.end(), ir) &&
-        ent.second.size() == 3 * n_consts &&
-        std::equal(ent.second.begin(), ent.second.end(), consts)) {
-      alias = (int)it->second;
-      e->cache_hits++;
+  if (it == e->cache.end()) return false;
+  const auto& src = e->cache_src.at(it->second);
+  *ir = &src.first;
+  *consts = &src.second;
+  *stage = (int)it->second;
+  return true;
+}
+
+// pqw_stage_add with the hash already computed. same >= 0: the caller has
+// checked that this program's text equals stage `same`'s (no lookup or
+// compare here). own_ir/own_consts: the text may be moved from them when the
+// engine keeps it.
+int stage_add_hashed(pqw_engine* e, const int32_t* ir, size_t ir_len, const int64_t* consts,
+                     size_t n_consts, const uint64_t* var_keys, size_t n_vars, uint64_t h,
+                     int same, std::vector<int32_t>* own_ir, std::vector<int64_t>* own_consts,
+                     int64_t out_status[16]) {
+  const uint32_t base = (uint32_t)e->var_keys.size();
+  const int idx = (int)e->stages.size();
+  int alias = -1;
+  if (same >= 0) {
+    alias = e->alias[(size_t)same] >= 0 ? e->alias[(size_t)same] : same;
+    e->cache_hits++;
+  } else {
+    auto it = e->cache.find(h);
+    if (it != e->cache.end()) {
+      const auto& ent = e->cache_src[it->second];
+      if (ent.first.size() == ir_len && std::equal(ent.first.begin(), ent.first.end(), ir) &&
+          ent.second.size() == 3 * n_consts &&
+          std::equal(ent.second.begin(), ent.second.end(), consts)) {
+        alias = (int)it->second;
+        e->cache_hits++;
+      }
     }
-  }
-  if (alias < 0) {
-    if (it == e->cache.end()) e->cache.emplace(h, (size_t)idx);
-    e->cache_src[(size_t)idx] = {std::vector<int32_t>(ir, ir + ir_len),
-                                 std::vector<int64_t>(consts, consts + 3 * n_consts)};
+    if (alias < 0) {
+      if (it == e->cache.end()) e->cache.emplace(h, (size_t)idx);
+      auto& dst = e->cache_src[(size_t)idx];
+      if (own_ir) dst.first = std::move(*own_ir);
+      else dst.first.assign(ir, ir + ir_len);
+      if (own_consts) dst.second = std::move(*own_consts);
+      else dst.second.assign(consts, consts + 3 * n_consts);
+    }
   }
   e->stages.emplace_back();
   e->alias.push_back(alias);
@@ -356,6 +378,26 @@ int pqw_stage_add(pqw_engine* e, const int32_t* ir, size_t ir_len, const int64_t
   out_status[13] = (int64_t)n_vars;
   e->uploaded = false;
   return idx;
+}
+}  // namespace pqw
+
+extern "C" {
+
+int pqw_stage_add(pqw_engine* e, const int32_t* ir, size_t ir_len, const int64_t* consts,
+                  size_t n_consts, const uint64_t* var_keys, size_t n_vars,
+                  int64_t out_status[16]) {
+  if (!e || !ir || !out_status) return fail(PQW_EINVAL, "null argument");
+  if (n_vars && !var_keys) return fail(PQW_EINVAL, "null var_keys");
+  if (n_consts && !consts) return fail(PQW_EINVAL, "null consts");
+  if (ir_len < 4 || ir[0] != 0x50515701) return fail(PQW_EINVAL, "stage compile: bad program magic");
+  // identical programs (e.g. the same layer repeated) compile once: the cache
+  // key is the program text; a hit shares the compiled program and only
+  // rebases vars. The compilation itself is deferred: every distinct program
+  // is compiled on a host thread pool at the first pqw_stage_status,
+  // pqw_upload or inspection call.
+  const uint64_t h = pqw::program_hash(ir, ir_len, consts, n_consts, n_vars);
+  return pqw::stage_add_hashed(e, ir, ir_len, consts, n_consts, var_keys, n_vars, h, -1, nullptr,
+                               nullptr, out_status);
 }
 
 // Compile the front ends of every pending stage (distinct programs on host

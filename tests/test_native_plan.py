@@ -12,6 +12,7 @@ reference's exception (the host checks run on the declined plan).
 """
 
 import copy
+import dataclasses
 import json
 import os
 
@@ -258,3 +259,39 @@ def test_lineage_check_matches_host(lib, kind):
     nat = NativePlan(plan)
     assert validate_lineage(plan.logical, plan.parallel, plan.lineage)
     assert not nat.lineage_clean()
+
+
+def test_batched_queue_dedups_like_per_stage_add(lib):
+    """pqw_plan_add_stages groups equal programs itself (hashing and comparing
+    on host threads, then handing the engine the verified duplicate); the
+    engine must end up as if every stage had gone through pqw_stage_add one by
+    one -- same statuses, same number of distinct programs -- also when a
+    second batch lands on programs the engine already holds."""
+    from paper_2506_15961_b200 import field as F
+    from paper_2506_15961_b200.engine import Engine
+    from paper_2506_15961_b200.workloads import get_workload
+    _, plan = get_workload("llama3-8b-tp4pp2dp2-sp")
+    nat = NativePlan(plan)
+    assert nat.validate() and nat.build_stages()
+    n, seed = nat.n_stages, 5
+    one = Engine(0, 0, F.fn_keys(0))
+    for i in range(n):
+        ir, cs, vk = nat.stage_program(i, seed)
+        one.add_stage(ir, cs, vk)
+    batch = Engine(0, 0, F.fn_keys(0))
+    ia = nat.add_stages(batch, seed)
+    split = Engine(0, 0, F.fn_keys(0))
+    ib = np.concatenate([nat.add_stages(split, seed, list(range(0, n, 2))),
+                         nat.add_stages(split, seed, list(range(1, n, 2)))])
+    order = list(range(0, n, 2)) + list(range(1, n, 2))
+    assert list(ia) == list(range(n)) and sorted(ib) == list(range(n))
+    def st(e, i):
+        return dataclasses.replace(e.stage_status(i), index=0)
+    want = [st(one, i) for i in range(n)]
+    assert [st(batch, i) for i in range(n)] == want
+    assert [st(split, int(ib[k])) for k in np.argsort(order)] == want
+    s1, s2, s3 = one.image_stats(), batch.image_stats(), split.image_stats()
+    assert s1["cache_hits"] == s2["cache_hits"] == s3["cache_hits"] > n // 2
+    for e in (one, batch, split):
+        e.close()
+    nat.close()
