@@ -822,9 +822,71 @@ PyObject* pack_graph(PyObject*, PyObject* args) {
   }
 }
 
+// pack_lineage(lineage: dict[str, LineageEntry]) -> dict[str, bytes]: the
+// columns of pqw_lineage_desc (native.py _pack_lineage): entry names (the
+// dict keys), mode (0 full, 1 partial, 2 other), shards per entry, shard
+// tensor names, dims per shard, (lo, hi) per dim.
+PyObject* pack_lineage(PyObject*, PyObject* args) {
+  PyObject* lin;
+  if (!PyArg_ParseTuple(args, "O!", &PyDict_Type, &lin)) return nullptr;
+  try {
+    std::string names, mode, nsh, snames, sdim, ranges;
+    Ref s_mode(PyUnicode_InternFromString("mode"));
+    Ref s_shards(PyUnicode_InternFromString("shards"));
+    Ref s_tensor(PyUnicode_InternFromString("tensor"));
+    Ref s_ranges(PyUnicode_InternFromString("ranges"));
+    Py_ssize_t pos = 0;
+    PyObject *key, *e;
+    while (PyDict_Next(lin, &pos, &key, &e)) {
+      put_str(names, key);
+      Ref m(PyObject_GetAttr(e, s_mode.p));
+      char md = 2;
+      if (PyUnicode_Check(m.p)) {
+        if (PyUnicode_CompareWithASCIIString(m.p, "full") == 0) md = 0;
+        else if (PyUnicode_CompareWithASCIIString(m.p, "partial") == 0) md = 1;
+      }
+      mode.push_back(md);
+      Ref sh(PyObject_GetAttr(e, s_shards.p));
+      Ref shf(PySequence_Fast(sh.p, "shards"));
+      const Py_ssize_t ns = PySequence_Fast_GET_SIZE(shf.p);
+      put<int32_t>(nsh, (int32_t)ns);
+      for (Py_ssize_t i = 0; i < ns; ++i) {
+        PyObject* s = PySequence_Fast_GET_ITEM(shf.p, i);
+        Ref t(PyObject_GetAttr(s, s_tensor.p));
+        put_str(snames, t.p);
+        Ref r(PyObject_GetAttr(s, s_ranges.p));
+        Ref rf(PySequence_Fast(r.p, "ranges"));
+        const Py_ssize_t nd = PySequence_Fast_GET_SIZE(rf.p);
+        put<int32_t>(sdim, (int32_t)nd);
+        for (Py_ssize_t d = 0; d < nd; ++d) {
+          Ref pr(PySequence_Fast(PySequence_Fast_GET_ITEM(rf.p, d), "range"));
+          const Py_ssize_t k = PySequence_Fast_GET_SIZE(pr.p);
+          for (Py_ssize_t j = 0; j < k; ++j)
+            put<int64_t>(ranges, as_int(PySequence_Fast_GET_ITEM(pr.p, j)));
+        }
+      }
+    }
+    Ref d(PyDict_New());
+    const std::pair<const char*, std::string*> cols[] = {
+        {"names", &names}, {"mode", &mode}, {"n_shards", &nsh},
+        {"shard_names", &snames}, {"sdim", &sdim}, {"ranges", &ranges}};
+    for (auto& c : cols) {
+      Ref b(bytes_of(*c.second));
+      if (PyDict_SetItemString(d.p, c.first, b.p) < 0) throw Err{};
+    }
+    Py_INCREF(d.p);
+    return d.p;
+  } catch (const Err&) {
+    if (!PyErr_Occurred()) PyErr_SetString(PyExc_ValueError, "lineage not packable");
+    return nullptr;
+  }
+}
+
 PyMethodDef methods[] = {
     {"pack_graph", pack_graph, METH_VARARGS,
      "pack_graph(graph, opcodes, const_id) -> dict of flat columns (pqw_graph_desc)"},
+    {"pack_lineage", pack_lineage, METH_VARARGS,
+     "pack_lineage(lineage) -> dict of flat columns (pqw_lineage_desc)"},
     {nullptr, nullptr, 0, nullptr}};
 
 PyModuleDef module = {PyModuleDef_HEAD_INIT, "_pqw_pack",

@@ -419,15 +419,25 @@ struct StageRec {
 
 // Per-thread scratch: generation-stamped marks over tensors and nodes.
 struct Marks {
-  std::vector<uint32_t> stamp;
+  // calloc'd: a fresh large block is untouched zero pages, so a per-thread
+  // Marks over a million-node graph costs only the pages its slices visit
+  uint32_t* stamp = nullptr;
+  size_t n = 0;
   uint32_t gen = 0;
-  void reset(size_t n) {
-    if (stamp.size() != n) {
-      stamp.assign(n, 0);
+  Marks() = default;
+  Marks(const Marks&) = delete;
+  Marks& operator=(const Marks&) = delete;
+  ~Marks() { std::free(stamp); }
+  void reset(size_t m) {
+    if (m != n || !stamp) {
+      std::free(stamp);
+      stamp = static_cast<uint32_t*>(std::calloc(std::max<size_t>(m, 1), sizeof(uint32_t)));
+      if (!stamp) throw std::bad_alloc();
+      n = m;
       gen = 0;
     }
     if (++gen == 0) {
-      std::fill(stamp.begin(), stamp.end(), 0);
+      std::memset(stamp, 0, n * sizeof(uint32_t));
       gen = 1;
     }
   }
@@ -822,14 +832,20 @@ bool validate_graph(const GraphData& g, std::string& why) {
 // Deterministic Kahn order of `nodes` (graph.py topo_sort with the (device,
 // seq, id) tie-break); `picked` marks exactly `nodes`. Throws PlanError on a
 // dangling input or a cycle.
+// `nodes` sorted ascending, all marked in `picked`; graph.py:96-150 order
+// (Kahn's algorithm, ready nodes by (device, seq, id))
 std::vector<int32_t> topo_order(const GraphData& g, const std::vector<int32_t>& nodes,
                                 const Marks& picked) {
-  std::unordered_map<int32_t, int32_t> local;  // node -> position in `nodes`
-  local.reserve(nodes.size() * 2);
-  for (size_t i = 0; i < nodes.size(); ++i) local.emplace(nodes[i], (int32_t)i);
-  std::vector<int32_t> indeg(nodes.size(), 0);
-  std::vector<std::vector<int32_t>> succ(nodes.size());
-  for (size_t i = 0; i < nodes.size(); ++i) {
+  const size_t n = nodes.size();
+  auto local = [&](int32_t v) {  // position of a picked node in `nodes`
+    return (int32_t)(std::lower_bound(nodes.begin(), nodes.end(), v) - nodes.begin());
+  };
+  // in-edges within the slice as CSR of successors
+  std::vector<int32_t> indeg(n, 0), soff(n + 1, 0), src_of;
+  src_of.reserve(n * 2);
+  std::vector<int32_t> dst_of;
+  dst_of.reserve(n * 2);
+  for (size_t i = 0; i < n; ++i) {
     const int32_t v = nodes[i];
     for (int64_t j = g.in_off[v]; j < g.in_off[v + 1]; ++j) {
       const int32_t t = g.ins[j];
@@ -837,26 +853,43 @@ std::vector<int32_t> topo_order(const GraphData& g, const std::vector<int32_t>& 
       const int32_t src = g.producer[t];
       if (src >= 0 && picked.test((size_t)src)) {
         indeg[i]++;
-        succ[(size_t)local[src]].push_back((int32_t)i);
+        const int32_t k = local(src);
+        soff[(size_t)k + 1]++;
+        src_of.push_back(k);
+        dst_of.push_back((int32_t)i);
       } else if (src < 0) {
         throw PlanError("dangling tensor");
       }
     }
   }
-  auto cmp = [&](int32_t a, int32_t b) { return g.before(nodes[b], nodes[a]); };  // min-heap
-  std::priority_queue<int32_t, std::vector<int32_t>, decltype(cmp)> ready(cmp);
-  for (size_t i = 0; i < nodes.size(); ++i)
-    if (!indeg[i]) ready.push((int32_t)i);
-  std::vector<int32_t> out;
-  out.reserve(nodes.size());
-  while (!ready.empty()) {
-    const int32_t i = ready.top();
-    ready.pop();
-    out.push_back(nodes[i]);
-    for (int32_t s : succ[i])
-      if (--indeg[s] == 0) ready.push(s);
+  for (size_t i = 0; i < n; ++i) soff[i + 1] += soff[i];
+  std::vector<int32_t> succ(src_of.size());
+  {
+    std::vector<int32_t> fill(soff.begin(), soff.end() - 1);
+    for (size_t e = 0; e < src_of.size(); ++e) succ[(size_t)fill[(size_t)src_of[e]]++] = dst_of[e];
   }
-  if (out.size() != nodes.size()) throw PlanError("cycle");
+  auto cmp = [&](int32_t a, int32_t b) { return g.before(nodes[b], nodes[a]); };  // min-heap
+  std::vector<int32_t> heap;
+  heap.reserve(n);
+  for (size_t i = 0; i < n; ++i)
+    if (!indeg[i]) heap.push_back((int32_t)i);
+  std::make_heap(heap.begin(), heap.end(), cmp);
+  std::vector<int32_t> out;
+  out.reserve(n);
+  while (!heap.empty()) {
+    std::pop_heap(heap.begin(), heap.end(), cmp);
+    const int32_t i = heap.back();
+    heap.pop_back();
+    out.push_back(nodes[i]);
+    for (int32_t e = soff[(size_t)i]; e < soff[(size_t)i + 1]; ++e) {
+      const int32_t s2 = succ[(size_t)e];
+      if (--indeg[(size_t)s2] == 0) {
+        heap.push_back(s2);
+        std::push_heap(heap.begin(), heap.end(), cmp);
+      }
+    }
+  }
+  if (out.size() != n) throw PlanError("cycle");
   return out;
 }
 
@@ -893,6 +926,14 @@ void sort_by_name(const GraphData& g, std::vector<int32_t>& ts) {
 }
 
 void build(pqw_plan* p) {
+  static const bool timing = getenv("PQW_TIMING") != nullptr;
+  auto lap = [t = std::chrono::steady_clock::now()](const char* what) mutable {
+    const auto now = std::chrono::steady_clock::now();
+    if (timing)
+      fprintf(stderr, "PQW_TIMING build %s %.1f ms\n", what,
+              std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  };
   const GraphData &L = p->L, &P = p->P;
   // entry_order: logical topological position of the producer, inputs first
   std::vector<int32_t> all(L.nn());
@@ -927,6 +968,7 @@ void build(pqw_plan* p) {
   for (size_t r = 0; r < ne; ++r)
     for (int32_t s : p->entries[p->order[r]].shards)
       first_rank[s] = std::min(first_rank[s], (int32_t)r);
+  lap("entry order");
   std::vector<int32_t> produced;  // ranks of produced checkpoints
   for (size_t r = 0; r < ne; ++r)
     if (L.producer[p->entries[p->order[r]].logical] >= 0) produced.push_back((int32_t)r);
@@ -966,6 +1008,7 @@ void build(pqw_plan* p) {
     }
   });
   if (!err.empty()) throw PlanError(err);
+  lap("slices");
   // ownership in stage order: a node belongs to the first stage whose slice has it
   for (int side = 0; side < 2; ++side) {
     const GraphData& g = side ? P : L;
@@ -978,6 +1021,7 @@ void build(pqw_plan* p) {
       if (!claimed[v]) u.push_back((int32_t)v);
     std::sort(u.begin(), u.end(), [&](int32_t a, int32_t b) { return g.nid[a] < g.nid[b]; });
   }
+  lap("uncovered");
 }
 
 // ---- lowering ---------------------------------------------------------------------

@@ -263,7 +263,15 @@ def _pack_graph(g: Graph, consts: _Consts, keep: list) -> _GraphDesc:
                       p(arrs["seq"], _I64P), ng, strs["inputs"])
 
 
-def _pack_lineage(lineage, keep: list) -> _LineageDesc:
+def _lineage_columns(lineage) -> tuple:
+    """(mode, n_shards, sdim, ranges, (names, shard names)) of a lineage: through
+    the C++ packer when it is built, else in Python."""
+    ext = _ext()
+    if ext is not None and hasattr(ext, "pack_lineage") and isinstance(lineage, dict):
+        d = ext.pack_lineage(lineage)
+        return (np.frombuffer(d["mode"], np.uint8), np.frombuffer(d["n_shards"], np.int32),
+                np.frombuffer(d["sdim"], np.int32), np.frombuffer(d["ranges"], np.int64),
+                (d["names"], d["shard_names"]))
     entries = list(lineage.values())
     mode = np.array([0 if e.mode == "full" else 1 if e.mode == "partial" else 2 for e in entries]
                     or [0], dtype=np.uint8)
@@ -272,11 +280,18 @@ def _pack_lineage(lineage, keep: list) -> _LineageDesc:
     sdim = np.array([len(s.ranges) for s in shards] or [0], dtype=np.int32)
     ranges = np.fromiter(chain.from_iterable(chain.from_iterable(s.ranges) for s in shards),
                          np.int64)
+    return mode, n_sh, sdim, ranges, (_joined(lineage), _joined(s.tensor for s in shards))
+
+
+def _pack_lineage(lineage, keep: list) -> _LineageDesc:
+    mode, n_sh, sdim, ranges, strs = _lineage_columns(lineage)
+    n = len(lineage)
+    mode, n_sh, sdim = (a if a.size else np.zeros(1, a.dtype) for a in (mode, n_sh, sdim))
     if not ranges.size:
         ranges = np.zeros(2, np.int64)
-    strs = (_joined(lineage), _joined(s.tensor for s in shards))
+    strs = tuple(x or b"\0" for x in strs)
     keep.append((mode, n_sh, sdim, ranges, strs))
-    return _LineageDesc(len(entries), strs[0], mode.ctypes.data_as(_U8P),
+    return _LineageDesc(n, strs[0], mode.ctypes.data_as(_U8P),
                         n_sh.ctypes.data_as(_I32P), strs[1], sdim.ctypes.data_as(_I32P),
                         ranges.ctypes.data_as(_I64P))
 

@@ -192,6 +192,17 @@ def test_cpp_packer_matches_python_packer(lib, name, rel):
                 assert a == b, (name, k)
             else:
                 assert np.array_equal(np.asarray(a), np.asarray(b)), (name, k)
+    got = N._lineage_columns(plan.lineage)
+    try:
+        N._ext = lambda: None
+        want = N._lineage_columns(plan.lineage)
+    finally:
+        N._ext = lambda: ext
+    if not plan.lineage:  # the Python columns pad empty arrays to one element
+        want = tuple(w[:0] if isinstance(w, np.ndarray) else w for w in want)
+    for a, b in zip(got[:4], want[:4]):
+        assert np.array_equal(a, b), name
+    assert got[4] == want[4], name
 
 
 def test_parallel_packer_matches_serial_packer(lib):
