@@ -1333,6 +1333,40 @@ CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* con
   return st;
 }
 
+uint64_t dag_hash(const Dag& d) {
+  uint64_t h = 0x44414731ull ^ d.units.size() ^ ((uint64_t)d.pool.size() << 32);
+  auto absorb = [&h](uint64_t w) {
+    h = (h ^ w) * 0x9E3779B97F4A7C15ull;
+    h ^= h >> 29;
+  };
+  for (const DagUnit& u : d.units) {
+    absorb((uint64_t)u.op | (uint64_t)u.fn << 8 | (uint64_t)u.k << 16 | (uint64_t)u.guarded << 63);
+    absorb((uint64_t)u.aux | (uint64_t)u.arg0 << 32);
+    absorb(u.nargs);
+  }
+  for (size_t i = 0; i < d.pool.size(); i += 2)
+    absorb((uint64_t)d.pool[i] | (i + 1 < d.pool.size() ? (uint64_t)d.pool[i + 1] << 32 : 0));
+  return mix64(h);
+}
+
+bool same_dag(const Dag& a, const Dag& b) {
+  if (a.units.size() != b.units.size() || a.pool != b.pool) return false;
+  for (size_t i = 0; i < a.units.size(); ++i) {
+    const DagUnit &x = a.units[i], &y = b.units[i];
+    if (x.op != y.op || x.fn != y.fn || x.k != y.k || x.aux != y.aux || x.arg0 != y.arg0 ||
+        x.nargs != y.nargs || x.guarded != y.guarded)
+      return false;
+  }
+  return true;
+}
+
+bool same_sched(const SchedOptions& a, const SchedOptions& b) {
+  return a.n_warps == b.n_warps && a.smem_slots == b.smem_slots && a.window == b.window &&
+         a.bmax == b.bmax && a.xlat == b.xlat && a.bundle_base == b.bundle_base &&
+         a.spill_cost == b.spill_cost && a.pick_scan == b.pick_scan &&
+         a.active_warps == b.active_warps;
+}
+
 void finalize_stage(CompiledStage& st) {
   if (st.status != PQW_STAGE_OK || st.be->ready) return;
   st.be->prog = schedule_program(*st.dag, st.sched);

@@ -2,8 +2,11 @@
 #pragma once
 #include <stdint.h>
 
+#include <algorithm>
+#include <atomic>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/planeq_witness.h"
@@ -62,6 +65,26 @@ int confirm_stage(const int32_t* ir, size_t ir_len, const int64_t* consts, size_
 
 // Run the back end of a stage compiled with status OK (idempotent).
 void finalize_stage(CompiledStage& st);
+
+// Back-end sharing between stages whose value DAGs are equal.
+uint64_t dag_hash(const Dag& d);
+bool same_dag(const Dag& a, const Dag& b);
+bool same_sched(const SchedOptions& a, const SchedOptions& b);
+
+// f(i) for i in [0, n) on up to hardware_concurrency host threads
+template <class F>
+void host_parallel_for(size_t n, F&& f) {
+  const unsigned nt =
+      (unsigned)std::min<size_t>(n, std::max(1u, std::thread::hardware_concurrency()));
+  std::atomic<size_t> next{0};
+  auto work = [&] {
+    for (size_t i; (i = next.fetch_add(1)) < n;) f(i);
+  };
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < nt; ++t) pool.emplace_back(work);
+  work();
+  for (auto& t : pool) t.join();
+}
 
 // Variables (stage-relative indices) in the cone of obligation `obl`.
 std::vector<uint32_t> obligation_support(const CompiledStage& st, uint32_t obl);

@@ -6,6 +6,7 @@
 #include <sched.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -196,6 +197,39 @@ static int finalize_all(pqw_engine* e) {
       todo.push_back(&st);
   }
   if (todo.empty()) return PQW_OK;
+  // Programs whose texts differ but whose value DAGs are equal (the front end
+  // erases the difference: interface order, names) get one back end:
+  // schedule_program is a function of the DAG and the options only.
+  {
+    std::vector<uint64_t> h(todo.size());
+    pqw::host_parallel_for(todo.size(), [&](size_t i) { h[i] = pqw::dag_hash(*todo[i]->dag); });
+    std::unordered_map<uint64_t, std::vector<size_t>> reps;
+    std::unordered_map<const pqw::StageBackend*, std::shared_ptr<pqw::StageBackend>> same;
+    std::vector<pqw::CompiledStage*> kept;
+    for (size_t i = 0; i < todo.size(); ++i) {
+      auto& cand = reps[h[i]];
+      bool dup = false;
+      for (size_t r : cand) {
+        if (pqw::same_dag(*todo[r]->dag, *todo[i]->dag) &&
+            pqw::same_sched(todo[r]->sched, todo[i]->sched)) {
+          same.emplace(todo[i]->be.get(), todo[r]->be);
+          dup = true;
+          break;
+        }
+      }
+      if (!dup) {
+        cand.push_back(i);
+        kept.push_back(todo[i]);
+      }
+    }
+    if (!same.empty())
+      for (size_t i = 0; i < e->stages.size(); ++i) {
+        auto it = same.find(e->stages[i].be.get());
+        if (it != same.end()) e->stages[i].be = it->second;
+      }
+    todo.swap(kept);
+  }
+  static const bool timing = getenv("PQW_TIMING") != nullptr;
   // largest first, handed out through a shared counter
   std::sort(todo.begin(), todo.end(), [](const pqw::CompiledStage* a, const pqw::CompiledStage* b) {
     return a->dag->units.size() > b->dag->units.size();
@@ -216,7 +250,12 @@ static int finalize_all(pqw_engine* e) {
       const size_t i = next.fetch_add(1);
       if (i >= todo.size()) return;
       try {
+        const auto t0 = std::chrono::steady_clock::now();
         pqw::finalize_stage(*todo[i]);
+        if (timing)
+          fprintf(stderr, "PQW_TIMING back end %zu units %.1f ms\n", todo[i]->dag->units.size(),
+                  std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                      .count());
       } catch (const std::exception& ex) {
         std::lock_guard<std::mutex> g(err_mu);
         if (err.empty()) err = ex.what();
@@ -407,6 +446,12 @@ static int finalize_front(pqw_engine* e) {
   std::vector<size_t> todo;
   for (size_t i = 0; i < e->stages.size(); ++i)
     if (!e->front_done[i] && e->alias[i] < 0) todo.push_back(i);
+  // longest texts first (the pool's critical path is its largest program)
+  std::stable_sort(todo.begin(), todo.end(), [&](size_t a, size_t b) {
+    return e->cache_src.at(a).first.size() > e->cache_src.at(b).first.size();
+  });
+  static const bool timing = getenv("PQW_TIMING") != nullptr;
+  const auto t_front = std::chrono::steady_clock::now();
   unsigned nt = std::max(1u, std::thread::hardware_concurrency());
   {
     cpu_set_t cs;
@@ -438,6 +483,11 @@ static int finalize_front(pqw_engine* e) {
   for (unsigned t = 1; t < nt; ++t) pool.emplace_back(work);
   work();
   for (auto& t : pool) t.join();
+  if (timing)
+    fprintf(stderr, "PQW_TIMING front ends %zu programs %.1f ms (largest %zu words)\n", todo.size(),
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_front)
+                .count(),
+            todo.empty() ? (size_t)0 : e->cache_src.at(todo[0]).first.size());
   if (!err.empty()) return fail(PQW_EINVAL, err);
   for (size_t i = 0; i < e->stages.size(); ++i) {
     if (e->front_done[i]) continue;
