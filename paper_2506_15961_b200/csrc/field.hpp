@@ -30,11 +30,18 @@ PQW_HD uint32_t fred62(uint64_t t) {
   uint32_t r = (uint32_t)(t & P) + (uint32_t)(t >> 31);
   return r >= P ? r - P : r;
 }
+#if defined(__CUDA_ARCH__) && defined(PQW_WHATIF_CHEAP_ARITH)  // timing what-if only (wrong values)
+PQW_HD uint32_t fmul(uint32_t a, uint32_t b) { return a * b; }
+#else
 PQW_HD uint32_t fmul(uint32_t a, uint32_t b) { return fred62((uint64_t)a * b); }
+#endif
 
 // Full 64-bit accumulator to [0, P).
 PQW_HD uint64_t ffold64(uint64_t x) { return (x & P) + (x >> 31); }  // < 2^34
 PQW_HD uint32_t fred64(uint64_t x) {
+#if defined(__CUDA_ARCH__) && defined(PQW_WHATIF_CHEAP_ARITH)
+  return (uint32_t)x;
+#endif
   x = ffold64(x);                              // < 2^31 + 2^33
   uint32_t r = (uint32_t)(x & P) + (uint32_t)(x >> 31);  // < 2^31 + 8
   return r >= P ? r - P : r;

@@ -267,7 +267,11 @@ __device__ __forceinline__ uint32_t run_fill(CodeRing& cr, uint32_t pc, uint32_t
     const F8 D = cr.rd8(pc), G = cr.rd8(pc + 2);
     uint32_t a[8];
 #pragma unroll
+#ifdef PQW_WHATIF_FILL_SHARED  // timing what-if only (wrong values): fills as fast as LDS
+    for (int i = 0; i < 8; ++i) a[i] = lds(sb, G.v[i] & 0xFFFFu);
+#else
     for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const uint32_t*>(gl + G.v[i]);
+#endif
 #pragma unroll
     for (int i = 0; i < 8; ++i) sts(sb, D.v[i], a[i]);
   }
@@ -277,6 +281,9 @@ __device__ __forceinline__ uint32_t run_fill(CodeRing& cr, uint32_t pc, uint32_t
 // Wait (all lanes) until a warp's published progress reaches `target`.
 __device__ __forceinline__ void wait_progress(const Params& p, const uint32_t* flag,
                                               uint32_t target) {
+#ifdef PQW_WHATIF_NO_WAIT  // timing what-if only (races): no cross-warp waits
+  return;
+#endif
   if (ld_acquire(flag) < target) {
 #ifdef PQW_PROF
     const long long t0 = clock64();
@@ -546,7 +553,11 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
 }
 
 template <int NW, bool PROBE>
-__global__ void __launch_bounds__(32 * NW) eval_kernel(Params p) {
+// (32 * NW, 1): one CTA per SM, so up to 65536 / (32 * NW) registers; ptxas
+// then allocates 96 instead of 79 for NW = 16 (A/B s3e/s3f: 13.30 -> 12.83 ms on
+// 405B; forcing more with __maxnreg__ or software-pipelining DOT1 groups did
+// not help).
+__global__ void __launch_bounds__(32 * NW, 1) eval_kernel(Params p) {
   extern __shared__ __align__(16) uint8_t sfile[];
   __shared__ uint32_t s_item;
   __shared__ uint32_t s_invalid;     // lanes with a vanished denominator (bitmask)

@@ -623,6 +623,19 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
         for (int i = 0; i < I_NUM_OPS; ++i)
           if (by_op[i]) fprintf(stderr, " op%d=%.1f%%", i, 100.0 * by_op[i] / std::max<uint64_t>(tot, 1));
         fprintf(stderr, "\n");
+        uint64_t sv = 0, sv_loc = 0, fl = 0, fl_loc = 0;
+        for (uint32_t v : values) {
+          if (!spilled[v] || remat_ok(v)) continue;
+          const uint32_t q = bundles[bundle_of[v]].warp % 4;
+          bool l = true;
+          uint64_t nr = 0;
+          for (uint32_t i = rdb_off[v]; i < rdb_off[v + 1]; ++i, ++nr) l = l && bundles[rdb[i]].warp % 4 == q;
+          sv++; fl += nr;
+          if (l) { sv_loc++; fl_loc += nr; }
+        }
+        fprintf(stderr, "TMEMDBG spilled=%llu local=%llu fills=%llu local_fills=%llu gm_slots=%u\n",
+                (unsigned long long)sv, (unsigned long long)sv_loc, (unsigned long long)fl,
+                (unsigned long long)fl_loc, n_gm);
       }
 
       // ---- 3. synchronisation -------------------------------------------------
