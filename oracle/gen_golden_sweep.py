@@ -22,8 +22,14 @@ are the same function of (plan, stage) either way.
 Progress is appended to .work/sweep_<name>.jsonl so an interrupted sweep
 resumes where it stopped.
 
+With --budget-s T the sweep stops after T seconds of wall time and writes a
+partial record instead (tests/golden/verdicts_partial_<name>.json: the stages
+done so far with their indices, merged with an earlier partial record of the
+same plan digest); --shuffle SEED takes the remaining stages in a seeded
+random order, so a bounded run samples the whole plan instead of its prefix.
+
 Usage (build container only):
-  python -m oracle.gen_golden_sweep <workload> [jobs] [--mem-gb G]
+  python -m oracle.gen_golden_sweep <workload> [jobs] [--mem-gb G] [--shuffle SEED] [--budget-s T]
 """
 
 from __future__ import annotations
@@ -69,12 +75,15 @@ def _init(mem_gb: float):
 
 
 def main():
-    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    def opt(flag, cast, default):
+        return cast(sys.argv[sys.argv.index(flag) + 1]) if flag in sys.argv else default
+    mem_gb = opt("--mem-gb", float, 0.0)
+    shuffle = opt("--shuffle", int, None)
+    budget_s = opt("--budget-s", float, 0.0)
+    args = [a for k, a in enumerate(sys.argv[1:], 1)
+            if not a.startswith("--") and not sys.argv[k - 1].startswith("--")]
     name = args[0]
     jobs = int(args[1]) if len(args) > 1 else max(1, (os.cpu_count() or 2) - 2)
-    mem_gb = 0.0
-    if "--mem-gb" in sys.argv:
-        mem_gb = float(sys.argv[sys.argv.index("--mem-gb") + 1])
     sys.path.insert(0, ROOT)
     os.makedirs(WORK, exist_ok=True)
     t_start = time.time()
@@ -103,7 +112,17 @@ def main():
                 d = json.loads(line)
                 if d.get("digest") == digest:
                     done[d["i"]] = d
+    part_path = os.path.join(GOLDEN, f"verdicts_partial_{name}.json")
+    prior = json.load(open(part_path)) if os.path.exists(part_path) else None
+    if prior and prior.get("plan_sha256") == digest:
+        idx = prior.get("stage_index") or list(range(len(prior["stage_status"])))
+        for i, (tgt, st) in zip(idx, prior["stage_status"]):
+            done.setdefault(i, {"i": i, "target": tgt, "status": st,
+                                "reason": prior.get("stage_reason", {}).get(tgt), "wall_s": 0.0})
     todo = [i for i in range(len(stages)) if i not in done]
+    if shuffle is not None:
+        import random
+        random.Random(shuffle).shuffle(todo)
     _S.update(plan=rplan, stages=stages)
     gc.collect()
     gc.freeze()
@@ -116,6 +135,10 @@ def main():
             done[rec["i"]] = rec
             if k % 50 == 0:
                 print(f"  {len(done)}/{len(stages)} ({time.time() - t_start:.0f}s)", flush=True)
+            if budget_s and time.time() - t_start > budget_s:
+                _write_partial(part_path, name, digest, jobs, done, len(stages), t_build, prior)
+                pool.terminate()
+                return
     recs = [done[i] for i in range(len(stages))]
     statuses = {r["status"] for r in recs}
     verdict = ("refuted" if "refuted" in statuses else
@@ -136,6 +159,27 @@ def main():
     print(name, rec["verdict"], rec["ref_wall_s"], "s",
           {k: sum(1 for _, st in rec["stage_status"] if st == k)
            for k in ("proven", "refuted", "unknown", "error")}, flush=True)
+
+
+def _write_partial(path, name, digest, jobs, done, n_total, t_build, prior):
+    idx = sorted(done)
+    rec = {
+        "name": name, "plan_sha256": digest,
+        "generator": "oracle/gen_golden_sweep.py (bounded: --budget-s; remaining stages in seeded random order)",
+        "solver": "reference bundled engine", "jobs": jobs, "partial": True,
+        "stages_checked": len(idx), "stages_total": n_total,
+        "stage_index": idx,
+        "stage_status": [(done[i]["target"], done[i]["status"]) for i in idx],
+        "stage_reason": {done[i]["target"]: done[i]["reason"] for i in idx
+                         if done[i]["status"] != "proven" and done[i].get("reason")},
+        "ref_build_stages_s": round(t_build, 1),
+        "ref_stage_cpu_s": round(sum(done[i].get("wall_s", 0.0) for i in idx)
+                                 + (prior or {}).get("ref_stage_cpu_s", 0.0), 1),
+        "note": (prior or {}).get("note", ""),
+    }
+    with open(path, "w") as f:
+        json.dump(rec, f, indent=1)
+    print(name, "partial", len(idx), "/", n_total, flush=True)
 
 
 if __name__ == "__main__":

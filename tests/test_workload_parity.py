@@ -194,8 +194,9 @@ PARTIAL = _partial_records()
 @pytest.mark.parametrize("rec", PARTIAL, ids=[r["name"] for r in PARTIAL])
 def test_full_405b_stage_verdicts_match_reference_prefix(gpu, rec):
     """configs[3] itself, the full 126-layer Llama3-405B plan: the reference's
-    own verdicts on its first stages (the full reference sweep projects to ~23 h,
-    see the record's note) equal verify_plan's, through the native path."""
+    own verdicts on the stages it checked (its first stages, then a seeded random
+    sample of the rest; the full reference sweep projects to ~23 h, see the
+    record's note) equal verify_plan's, through the native path."""
     import hashlib
     from paper_2506_15961_b200.plan import dumps
     from paper_2506_15961_b200.verify import VerifyOptions, verify_plan
@@ -205,5 +206,6 @@ def test_full_405b_stage_verdicts_match_reference_prefix(gpu, rec):
     assert rep["engine"]["host_path"] == "native"
     got = [(s["target"], s["status"]) for s in rep["stages"]]
     want = [tuple(x) for x in rec["stage_status"]]
-    assert got[: len(want)] == want
+    idx = rec.get("stage_index") or list(range(len(want)))
+    assert [got[i] for i in idx] == want
     assert rep["verdict"] == "proven"
