@@ -278,6 +278,108 @@ __device__ __forceinline__ uint32_t run_fill(CodeRing& cr, uint32_t pc, uint32_t
   return pc;
 }
 
+// Handlers of the rarer bundle kinds (inversions, variables, constants,
+// checks, spills). Inlined: out of line (noinline, the ring state through
+// local memory) the 405B kernel went 12.76 -> 15.69 ms (A/B s3h).
+#define PQW_COLD __device__ __forceinline__
+
+PQW_COLD uint32_t h_inv(CodeRing& cr, const uint4* stream, uint32_t pc, uint32_t n, uint32_t sb) {
+  // Montgomery batch inversion over the bundle: prefix products go to the
+  // destination slots, one inversion, then a backward sweep (which reads
+  // the payload again from global memory). Every operand is a guarded
+  // denominator (a DEN of the same stage), so a witness where one
+  // vanishes is invalid and its garbage never counts.
+  const uint4* base = stream + pc;
+  const uint32_t ng = (n + 7u) / 8u;
+  uint32_t acc = 1;
+  for (uint32_t g = 0; g < n; g += 8, pc += 4) {
+    cr.ensure(pc, 4);
+    const F8 D = cr.rd8(pc), A = cr.rd8(pc + 2);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (g + i < n) {
+        acc = fmul(acc, lds(sb, A.v[i]));
+        sts(sb, D.v[i], acc);
+      }
+  }
+  uint32_t inv = finv(acc);
+  for (int32_t gi = (int32_t)ng - 1; gi >= 0; --gi) {
+    const uint32_t g = (uint32_t)gi * 8u;
+    const F8 D = ld8(base + 4 * gi), A = ld8(base + 4 * gi + 2);
+    const uint32_t dprev = gi > 0 ? __ldg(reinterpret_cast<const uint32_t*>(base + 4 * gi - 3) + 3)
+                                  : 0u;  // D.v[7] of the previous group
+#pragma unroll
+    for (int i = 7; i >= 0; --i)
+      if (g + i < n) {
+        if (g + i == 0) {
+          sts(sb, D.v[i], inv);
+        } else {
+          const uint32_t prev = lds(sb, i > 0 ? D.v[i > 0 ? i - 1 : 0] : dprev);
+          const uint32_t a = lds(sb, A.v[i]);
+          sts(sb, D.v[i], fmul(inv, prev));
+          inv = fmul(inv, a);
+        }
+      }
+  }
+  return pc;
+}
+
+template <bool PROBE>
+PQW_COLD uint32_t h_var(CodeRing& cr, uint32_t pc, uint32_t n, uint32_t sb, const uint64_t* vkeys,
+                        uint32_t w, uint32_t probe_w, uint32_t* probe_vars) {
+  for (uint32_t g = 0; g < n; g += 8, pc += 4) {
+    cr.ensure(pc, 4);
+    const F8 D = cr.rd8(pc), V = cr.rd8(pc + 2);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t v = witness_value(__ldg(vkeys + V.v[i]), w);
+      if (PROBE && w == probe_w) probe_vars[V.v[i]] = v;
+      sts(sb, D.v[i], v);
+    }
+  }
+  return pc;
+}
+
+PQW_COLD uint32_t h_const(CodeRing& cr, uint32_t pc, uint32_t n, uint32_t sb) {
+  for (uint32_t g = 0; g < n; g += 8, pc += 4) {
+    cr.ensure(pc, 4);
+    const F8 D = cr.rd8(pc), C = cr.rd8(pc + 2);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sts(sb, D.v[i], C.v[i]);
+  }
+  return pc;
+}
+
+template <bool PROBE>
+PQW_COLD uint32_t h_chk(CodeRing& cr, uint32_t pc, uint32_t n, uint32_t sb, uint32_t w, uint32_t probe_w,
+                        uint32_t probe_obl, uint32_t* probe_out, uint32_t& bad) {
+  for (uint32_t g = 0; g < n; g += 8, pc += 6) {
+    cr.ensure(pc, 6);
+    const F8 O = cr.rd8(pc), A = cr.rd8(pc + 2), B = cr.rd8(pc + 4);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t a = lds(sb, A.v[i]), b = lds(sb, B.v[i]);
+      if (PROBE && O.v[i] == probe_obl && w == probe_w) {
+        probe_out[0] = a;
+        probe_out[1] = b;
+      }
+      if (a != b) bad = min(bad, O.v[i]);
+    }
+  }
+  return pc;
+}
+
+PQW_COLD uint32_t h_spill(CodeRing& cr, uint32_t pc, uint32_t n, uint32_t sb, uint8_t* gl) {
+  for (uint32_t g = 0; g < n; g += 8, pc += 4) {
+    cr.ensure(pc, 4);
+    const F8 G = cr.rd8(pc), A = cr.rd8(pc + 2);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      *reinterpret_cast<uint32_t*>(gl + G.v[i]) = lds(sb, A.v[i]);
+  }
+  return pc;
+}
+
 // Wait (all lanes) until a warp's published progress reaches `target`.
 __device__ __forceinline__ void wait_progress(const Params& p, const uint32_t* flag,
                                               uint32_t target) {
@@ -425,80 +527,17 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
                                 [key](const uint32_t* x) { return uf_apply(key, x[0]); });
         break;
       }
-      case I_INV: {
-        // Montgomery batch inversion over the bundle: prefix products go to the
-        // destination slots, one inversion, then a backward sweep (which reads
-        // the payload again from global memory). Every operand is a guarded
-        // denominator (a DEN of the same stage), so a witness where one
-        // vanishes is invalid and its garbage never counts.
-        const uint4* base = stream + pc;
-        const uint32_t ng = (n + 7u) / 8u;
-        uint32_t acc = 1;
-        for (uint32_t g = 0; g < n; g += 8, pc += 4) {
-          cr.ensure(pc, 4);
-          const F8 D = cr.rd8(pc), A = cr.rd8(pc + 2);
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            if (g + i < n) {
-              acc = fmul(acc, lds(sb, A.v[i]));
-              sts(sb, D.v[i], acc);
-            }
-        }
-        uint32_t inv = finv(acc);
-        for (int32_t gi = (int32_t)ng - 1; gi >= 0; --gi) {
-          const uint32_t g = (uint32_t)gi * 8u;
-          const F8 D = ld8(base + 4 * gi), A = ld8(base + 4 * gi + 2);
-          const uint32_t dprev = gi > 0 ? __ldg(reinterpret_cast<const uint32_t*>(base + 4 * gi - 3) + 3)
-                                        : 0u;  // D.v[7] of the previous group
-#pragma unroll
-          for (int i = 7; i >= 0; --i)
-            if (g + i < n) {
-              if (g + i == 0) {
-                sts(sb, D.v[i], inv);
-              } else {
-                const uint32_t prev = lds(sb, i > 0 ? D.v[i > 0 ? i - 1 : 0] : dprev);
-                const uint32_t a = lds(sb, A.v[i]);
-                sts(sb, D.v[i], fmul(inv, prev));
-                inv = fmul(inv, a);
-              }
-            }
-        }
+      case I_INV:
+        pc = h_inv(cr, stream, pc, n, sb);
         break;
-      }
       case I_VAR:
-        for (uint32_t g = 0; g < n; g += 8, pc += 4) {
-          cr.ensure(pc, 4);
-          const F8 D = cr.rd8(pc), V = cr.rd8(pc + 2);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const uint32_t v = witness_value(__ldg(vkeys + V.v[i]), w);
-            if (PROBE && w == p.probe_w) p.probe_vars[V.v[i]] = v;
-            sts(sb, D.v[i], v);
-          }
-        }
+        pc = h_var<PROBE>(cr, pc, n, sb, vkeys, w, p.probe_w, p.probe_vars);
         break;
       case I_CONST:
-        for (uint32_t g = 0; g < n; g += 8, pc += 4) {
-          cr.ensure(pc, 4);
-          const F8 D = cr.rd8(pc), C = cr.rd8(pc + 2);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) sts(sb, D.v[i], C.v[i]);
-        }
+        pc = h_const(cr, pc, n, sb);
         break;
       case I_CHK:
-        for (uint32_t g = 0; g < n; g += 8, pc += 6) {
-          cr.ensure(pc, 6);
-          const F8 O = cr.rd8(pc), A = cr.rd8(pc + 2), B = cr.rd8(pc + 4);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const uint32_t a = lds(sb, A.v[i]), b = lds(sb, B.v[i]);
-            if (PROBE && O.v[i] == p.probe_obl && w == p.probe_w) {
-              p.probe_out[0] = a;
-              p.probe_out[1] = b;
-            }
-            if (a != b) bad = min(bad, O.v[i]);
-          }
-        }
+        pc = h_chk<PROBE>(cr, pc, n, sb, w, p.probe_w, p.probe_obl, p.probe_out, bad);
         break;
       case I_DEN:
         for (uint32_t g = 0; g < n; g += 8, pc += 2) {
@@ -514,13 +553,7 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
         pc = run_fill(cr, pc, n, sb, gl);
         break;
       case I_SPILL:
-        for (uint32_t g = 0; g < n; g += 8, pc += 4) {
-          cr.ensure(pc, 4);
-          const F8 G = cr.rd8(pc), A = cr.rd8(pc + 2);
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            *reinterpret_cast<uint32_t*>(gl + G.v[i]) = lds(sb, A.v[i]);
-        }
+        pc = h_spill(cr, pc, n, sb, gl);
         break;
       case I_WAIT:
         // header: z = producer warp, w = progress it must have published
