@@ -17,6 +17,7 @@
 #include <sys/mman.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cstdio>
 #include <atomic>
@@ -834,17 +835,32 @@ bool validate_graph(const GraphData& g, std::string& why) {
 // dangling input or a cycle.
 // `nodes` sorted ascending, all marked in `picked`; graph.py:96-150 order
 // (Kahn's algorithm, ready nodes by (device, seq, id))
+// Reusable per-thread buffers of topo_order (a stage's slice is a few hundred
+// nodes; allocating them per call cost more than the sort itself).
+struct TopoScratch {
+  std::vector<int32_t> loc;  // node -> position in `nodes` (valid where picked)
+  std::vector<int32_t> indeg, soff, src_of, dst_of, succ, fill, heap;
+  std::vector<int32_t> dev;
+  std::vector<int64_t> seq;
+};
+
 std::vector<int32_t> topo_order(const GraphData& g, const std::vector<int32_t>& nodes,
-                                const Marks& picked) {
+                                const Marks& picked, TopoScratch& S) {
   const size_t n = nodes.size();
-  auto local = [&](int32_t v) {  // position of a picked node in `nodes`
-    return (int32_t)(std::lower_bound(nodes.begin(), nodes.end(), v) - nodes.begin());
-  };
+  if (S.loc.size() < g.nn()) S.loc.resize(g.nn());
+  for (size_t i = 0; i < n; ++i) S.loc[(size_t)nodes[i]] = (int32_t)i;
+  // the (device, seq) part of the key, contiguous; ties fall back to the id
+  S.dev.resize(n);
+  S.seq.resize(n);
+  for (size_t i = 0; i < n; ++i) {
+    S.dev[i] = g.device[(size_t)nodes[i]];
+    S.seq[i] = g.seq[(size_t)nodes[i]];
+  }
   // in-edges within the slice as CSR of successors
-  std::vector<int32_t> indeg(n, 0), soff(n + 1, 0), src_of;
-  src_of.reserve(n * 2);
-  std::vector<int32_t> dst_of;
-  dst_of.reserve(n * 2);
+  S.indeg.assign(n, 0);
+  S.soff.assign(n + 1, 0);
+  S.src_of.clear();
+  S.dst_of.clear();
   for (size_t i = 0; i < n; ++i) {
     const int32_t v = nodes[i];
     for (int64_t j = g.in_off[v]; j < g.in_off[v + 1]; ++j) {
@@ -852,27 +868,32 @@ std::vector<int32_t> topo_order(const GraphData& g, const std::vector<int32_t>& 
       if (g.is_input[t]) continue;
       const int32_t src = g.producer[t];
       if (src >= 0 && picked.test((size_t)src)) {
-        indeg[i]++;
-        const int32_t k = local(src);
-        soff[(size_t)k + 1]++;
-        src_of.push_back(k);
-        dst_of.push_back((int32_t)i);
+        S.indeg[i]++;
+        const int32_t k = S.loc[(size_t)src];
+        S.soff[(size_t)k + 1]++;
+        S.src_of.push_back(k);
+        S.dst_of.push_back((int32_t)i);
       } else if (src < 0) {
         throw PlanError("dangling tensor");
       }
     }
   }
-  for (size_t i = 0; i < n; ++i) soff[i + 1] += soff[i];
-  std::vector<int32_t> succ(src_of.size());
-  {
-    std::vector<int32_t> fill(soff.begin(), soff.end() - 1);
-    for (size_t e = 0; e < src_of.size(); ++e) succ[(size_t)fill[(size_t)src_of[e]]++] = dst_of[e];
-  }
-  auto cmp = [&](int32_t a, int32_t b) { return g.before(nodes[b], nodes[a]); };  // min-heap
-  std::vector<int32_t> heap;
-  heap.reserve(n);
+  for (size_t i = 0; i < n; ++i) S.soff[i + 1] += S.soff[i];
+  S.succ.resize(S.src_of.size());
+  S.fill.assign(S.soff.begin(), S.soff.end() - 1);
+  for (size_t e = 0; e < S.src_of.size(); ++e)
+    S.succ[(size_t)S.fill[(size_t)S.src_of[e]]++] = S.dst_of[e];
+  // g.before on slice positions (graph.py:136 rank: device, seq, id)
+  auto before = [&](int32_t a, int32_t b) {
+    if (S.dev[a] != S.dev[b]) return S.dev[a] < S.dev[b];
+    if (S.seq[a] != S.seq[b]) return S.seq[a] < S.seq[b];
+    return g.nid[(size_t)nodes[a]] < g.nid[(size_t)nodes[b]];
+  };
+  auto cmp = [&](int32_t a, int32_t b) { return before(b, a); };  // min-heap
+  auto& heap = S.heap;
+  heap.clear();
   for (size_t i = 0; i < n; ++i)
-    if (!indeg[i]) heap.push_back((int32_t)i);
+    if (!S.indeg[i]) heap.push_back((int32_t)i);
   std::make_heap(heap.begin(), heap.end(), cmp);
   std::vector<int32_t> out;
   out.reserve(n);
@@ -881,9 +902,9 @@ std::vector<int32_t> topo_order(const GraphData& g, const std::vector<int32_t>& 
     const int32_t i = heap.back();
     heap.pop_back();
     out.push_back(nodes[i]);
-    for (int32_t e = soff[(size_t)i]; e < soff[(size_t)i + 1]; ++e) {
-      const int32_t s2 = succ[(size_t)e];
-      if (--indeg[(size_t)s2] == 0) {
+    for (int32_t e = S.soff[(size_t)i]; e < S.soff[(size_t)i + 1]; ++e) {
+      const int32_t s2 = S.succ[(size_t)e];
+      if (--S.indeg[(size_t)s2] == 0) {
         heap.push_back(s2);
         std::push_heap(heap.begin(), heap.end(), cmp);
       }
@@ -941,7 +962,8 @@ void build(pqw_plan* p) {
   Marks everything;
   everything.reset(L.nn());
   for (size_t i = 0; i < all.size(); ++i) everything.set(i);
-  const auto lorder = topo_order(L, all, everything);
+  TopoScratch ts0;
+  const auto lorder = topo_order(L, all, everything, ts0);
   std::vector<int64_t> pos(L.nn(), -1);
   for (size_t i = 0; i < lorder.size(); ++i) pos[lorder[i]] = (int64_t)i;
   const size_t ne = p->entries.size();
@@ -977,7 +999,16 @@ void build(pqw_plan* p) {
   std::string err;
   const unsigned nt = host_threads(produced.size());
   std::vector<Marks> seen_l(nt), picked_l(nt), seen_p(nt), picked_p(nt);
+  std::vector<TopoScratch> tscr(nt);
+  std::vector<std::array<double, 6>> acc(nt, std::array<double, 6>{});
   parallel_for(produced.size(), [&](size_t si, unsigned tid) {
+    auto tick = [&](int k, std::chrono::steady_clock::time_point& t) {
+      if (!timing) return;
+      const auto now = std::chrono::steady_clock::now();
+      acc[tid][k] += std::chrono::duration<double, std::milli>(now - t).count();
+      t = now;
+    };
+    auto tt = std::chrono::steady_clock::now();
     try {
       const int32_t r = produced[si];
       const Entry& e = p->entries[p->order[r]];
@@ -988,26 +1019,39 @@ void build(pqw_plan* p) {
       backward_slice(L, {e.logical},
                      [&](int32_t t) { return t != e.logical && p->entry_of_logical[t] >= 0; },
                      seen_l[tid], picked_l[tid], nodes, bound);
+      tick(0, tt);
       std::sort(nodes.begin(), nodes.end());
-      st.lnodes = topo_order(L, nodes, picked_l[tid]);
+      st.lnodes = topo_order(L, nodes, picked_l[tid], tscr[tid]);
+      tick(1, tt);
       for (int32_t b : bound)
         if (p->entry_of_logical[b] < 0) throw PlanError("logical input has no checkpoint entry");
       sort_by_name(L, bound);
       st.l_inputs = bound;
       backward_slice(P, e.shards, [&](int32_t t) { return first_rank[t] < r; }, seen_p[tid],
                      picked_p[tid], nodes, bound);
+      tick(2, tt);
+      if (timing) acc[tid][5] += (double)nodes.size();
       std::sort(nodes.begin(), nodes.end());
-      st.pnodes = topo_order(P, nodes, picked_p[tid]);
+      st.pnodes = topo_order(P, nodes, picked_p[tid], tscr[tid]);
+      tick(3, tt);
       for (int32_t b : bound)
         if (!(first_rank[b] < r)) throw PlanError("parallel input is not a checkpoint shard");
       sort_by_name(P, bound);
       st.p_inputs = bound;
+      tick(4, tt);
     } catch (const std::exception& ex) {
       std::lock_guard<std::mutex> l(err_mu);
       if (err.empty()) err = ex.what();
     }
   });
   if (!err.empty()) throw PlanError(err);
+  if (timing) {
+    std::array<double, 6> tot{};
+    for (auto& a : acc)
+      for (int k = 0; k < 6; ++k) tot[k] += a[k];
+    fprintf(stderr, "PQW_TIMING slices (thread-ms) lslice %.1f ltopo %.1f pslice %.1f ptopo %.1f rest %.1f; parallel slice nodes %.0f\n",
+            tot[0], tot[1], tot[2], tot[3], tot[4], tot[5]);
+  }
   lap("slices");
   // ownership in stage order: a node belongs to the first stage whose slice has it
   for (int side = 0; side < 2; ++side) {
