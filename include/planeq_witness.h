@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define PQW_ABI_VERSION 4
+#define PQW_ABI_VERSION 5
 #define PQW_PRIME 2147483647u /* 2^31 - 1 */
 
 /* error codes */
@@ -292,6 +292,9 @@ typedef struct pqw_graph_desc {
   const int64_t* node_seq;
   int64_t n_inputs;
   const char* input_names;     /* graph.inputs                                     */
+  /* byte length of each names buffer above (through its last NUL), or 0 when
+   * the caller does not know it (the library then scans for the n-th NUL) */
+  int64_t tensor_names_len, node_ids_len, node_inputs_len, node_outputs_len, input_names_len;
 } pqw_graph_desc;
 
 /* Lineage: checkpoint entries (dict order) and their shards. */

@@ -198,8 +198,9 @@ void cut_names(const char* s, size_t len, unsigned K, std::vector<size_t>& cut,
 }
 
 // copy the n NUL-separated names once, then view into the copy
-void split_names(const char* s, int64_t n, Col<char>& store, Col<std::string_view>& out) {
-  const size_t len = names_len(s, n);
+void split_names(const char* s, int64_t n, Col<char>& store, Col<std::string_view>& out,
+                 int64_t known_len = 0) {
+  const size_t len = known_len > 0 ? (size_t)known_len : names_len(s, n);
   par_copy(store, s, len);
   out.resize((size_t)n);
   const unsigned K = host_threads(std::max<size_t>(1, len / (1u << 20)));
@@ -314,10 +315,10 @@ struct GraphData {
   // into chunks at name boundaries, names counted per chunk, then resolved in
   // parallel (no copy of the names is kept)
   template <class V>
-  void resolve(const char* names, int64_t n, V& out) {
+  void resolve(const char* names, int64_t n, V& out, int64_t known_len = 0) {
     out.resize((size_t)n);
     if (n == 0) return;
-    const size_t len = names_len(names, n);
+    const size_t len = known_len > 0 ? (size_t)known_len : names_len(names, n);
     const unsigned K = host_threads(std::max<size_t>(1, len / (1u << 20)));
     std::vector<size_t> cut, first;
     cut_names(names, len, K, cut, first);
@@ -345,7 +346,7 @@ struct GraphData {
               std::chrono::duration<double, std::milli>(t - t0).count());
       t0 = t;
     };
-    split_names(d.tensor_names, d.n_tensors, tstore, tname);
+    split_names(d.tensor_names, d.n_tensors, tstore, tname, d.tensor_names_len);
     lap("tensor names");
     if (!index.build(tname)) {
       resolved = false;
@@ -358,7 +359,7 @@ struct GraphData {
     par_copy(dims, d.tensor_dims, (size_t)dim_off.back());
     par_copy(tflags, d.tensor_flags, (size_t)d.n_tensors);
     const size_t n = (size_t)d.n_nodes;
-    split_names(d.node_ids, d.n_nodes, nstore, nid);
+    split_names(d.node_ids, d.n_nodes, nstore, nid, d.node_ids_len);
     par_copy(kind, d.node_kind, n);
     par_copy(device, d.node_device, n);
     par_copy(seq, d.node_seq, n);
@@ -373,13 +374,13 @@ struct GraphData {
     }
     par_copy(attrs, d.node_attrs, (size_t)attr_off[n]);
     lap("node columns");
-    resolve(d.node_inputs, in_off[n], ins);
-    resolve(d.node_outputs, out_off[n], outs);
+    resolve(d.node_inputs, in_off[n], ins, d.node_inputs_len);
+    resolve(d.node_outputs, out_off[n], outs, d.node_outputs_len);
     lap("resolve io");
     {
       std::vector<int32_t> gin;
       const bool keep = resolved;
-      resolve(d.input_names, d.n_inputs, gin);
+      resolve(d.input_names, d.n_inputs, gin, d.input_names_len);
       resolved = keep;  // graph.inputs may name anything (it is only a set of ids)
       is_input.assign(nt(), 0);
       for (int32_t t : gin)

@@ -18,7 +18,7 @@ from .errors import EngineError, EngineUnavailable
 
 LIB_NAME = "libplaneq_witness.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 # PQW_STAGE_* codes
 STAGE_OK = 0

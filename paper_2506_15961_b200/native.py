@@ -58,7 +58,9 @@ class _GraphDesc(C.Structure):
                 ("node_nin", _I32P), ("node_nout", _I32P), ("node_inputs", C.c_char_p),
                 ("node_outputs", C.c_char_p), ("node_nattr", _I32P), ("node_attrs", _I64P),
                 ("node_device", _I32P), ("node_seq", _I64P), ("n_inputs", C.c_int64),
-                ("input_names", C.c_char_p)]
+                ("input_names", C.c_char_p), ("tensor_names_len", C.c_int64),
+                ("node_ids_len", C.c_int64), ("node_inputs_len", C.c_int64),
+                ("node_outputs_len", C.c_int64), ("input_names_len", C.c_int64)]
 
 
 class _LineageDesc(C.Structure):
@@ -260,7 +262,14 @@ def _pack_graph(g: Graph, consts: _Consts, keep: list) -> _GraphDesc:
                       p(arrs["flags"], _U8P), nn, strs["ids"], p(arrs["kind"], _I32P),
                       p(arrs["nin"], _I32P), p(arrs["nout"], _I32P), strs["ins"], strs["outs"],
                       p(arrs["nattr"], _I32P), p(arrs["attrs"], _I64P), p(arrs["device"], _I32P),
-                      p(arrs["seq"], _I64P), ng, strs["inputs"])
+                      p(arrs["seq"], _I64P), ng, strs["inputs"],
+                      *(_names_len(strs[k]) for k in ("tn", "ids", "ins", "outs", "inputs")))
+
+
+def _names_len(b) -> int:
+    """Byte length of a NUL-joined names buffer through its last NUL (the
+    library then need not scan for it), 0 when unknown."""
+    return len(b) if isinstance(b, (bytes, bytearray)) and (not b or b[-1] == 0) else 0
 
 
 def _lineage_columns(lineage) -> tuple:
