@@ -651,27 +651,45 @@ bool gather_parts(std::vector<Cols>& parts, PyObject* const_id, PyObject* out[NC
   });
   lap("gather");
   // const_id is a function of the exact value: memoise it per exact int /
-  // float value, and per object for anything else (Fraction, numpy scalars)
+  // float value, per (numerator, denominator) for a Fraction whose terms fit
+  // in 64 bits (every node carries its own Fraction object), and per object
+  // for anything else (numpy scalars, big fractions)
   struct Key {
-    uint64_t tag, bits;
-    bool operator==(const Key& o) const { return tag == o.tag && bits == o.bits; }
+    uint64_t tag, bits, bits2;
+    bool operator==(const Key& o) const { return tag == o.tag && bits == o.bits && bits2 == o.bits2; }
   };
   struct KeyHash {
-    size_t operator()(const Key& k) const { return std::hash<uint64_t>()(k.bits * 0x9E3779B97F4A7C15ull ^ k.tag); }
+    size_t operator()(const Key& k) const {
+      return std::hash<uint64_t>()((k.bits * 0x9E3779B97F4A7C15ull ^ k.bits2) * 0xBF58476D1CE4E5B9ull ^ k.tag);
+    }
   };
+  static PyObject* S_num = PyUnicode_InternFromString("_numerator");
+  static PyObject* S_den = PyUnicode_InternFromString("_denominator");
+  PyTypeObject* fraction_type = nullptr;  // the first type seen with both slots
   std::unordered_map<Key, int64_t, KeyHash> memo;
   for (size_t t = 0; t < nt; ++t) {
     const size_t word0 = off[t * NCOL + C_ATTRS] / sizeof(int64_t);
     for (auto& q : parts[t].consts) {
       PyObject* v = q.second;
-      Key key{3, reinterpret_cast<uintptr_t>(v)};
+      Key key{3, reinterpret_cast<uintptr_t>(v), 0};
       long long x;
       if (PyFloat_CheckExact(v)) {
         const double d = PyFloat_AS_DOUBLE(v);
-        key = {1, 0};
+        key = {1, 0, 0};
         std::memcpy(&key.bits, &d, sizeof(d));
       } else if (fast_int(v, x)) {
-        key = {2, static_cast<uint64_t>(x)};
+        key = {2, static_cast<uint64_t>(x), 0};
+      } else if (!PyLong_Check(v) && (fraction_type == nullptr || Py_TYPE(v) == fraction_type)) {
+        PyObject* nu = PyObject_GetAttr(v, S_num);
+        PyObject* de = nu ? PyObject_GetAttr(v, S_den) : nullptr;
+        long long a, b;
+        if (nu && de && fast_int(nu, a) && fast_int(de, b) && b > 0) {
+          fraction_type = Py_TYPE(v);
+          key = {4, static_cast<uint64_t>(a), static_cast<uint64_t>(b)};
+        }
+        Py_XDECREF(nu);
+        Py_XDECREF(de);
+        PyErr_Clear();
       }
       auto it = memo.find(key);
       int64_t id;

@@ -135,6 +135,9 @@ def peak_fieldops(device: int = 0) -> dict:
     return {"mul": out[0], "add": out[1], "hash": out[2], "inv": out[3]}
 
 
+_I64_MIN = -(1 << 63)
+
+
 def _ptr(a: np.ndarray, ct):
     return a.ctypes.data_as(C.POINTER(ct))
 
@@ -236,17 +239,15 @@ class Engine:
         return _LazyStage(self, idx)
 
     def stage_status(self, idx: int) -> StageCompile:
-        st = np.zeros(16, dtype=np.int64)
-        self._check(self.lib.pqw_stage_status(self._h, idx, _ptr(st, C.c_int64)))
-        imin = np.iinfo(np.int64).min
-        return StageCompile(index=idx, status=int(st[0]), info=int(st[1]),
-                            obligations=int(st[2]), fast=int(st[3]), residual=int(st[4]),
-                            code_len=int(st[5]), slots=int(st[6]), degree=int(st[7]),
-                            const_lhs=int(st[8]), const_rhs=int(st[9]),
-                            exact_lhs=None if st[10] == imin else int(st[10]),
-                            exact_rhs=None if st[11] == imin else int(st[11]),
-                            field_ops=int(st[12]), n_vars=int(st[13]),
-                            spill_slots=int(st[14]), bundles=int(st[15]))
+        st = (C.c_int64 * 16)()  # a ctypes buffer: no numpy round trip per stage
+        self._check(self.lib.pqw_stage_status(self._h, idx, st))
+        s = st[:]
+        return StageCompile(index=idx, status=s[0], info=s[1], obligations=s[2], fast=s[3],
+                            residual=s[4], code_len=s[5], slots=s[6], degree=s[7],
+                            const_lhs=s[8], const_rhs=s[9],
+                            exact_lhs=None if s[10] == _I64_MIN else s[10],
+                            exact_rhs=None if s[11] == _I64_MIN else s[11],
+                            field_ops=s[12], n_vars=s[13], spill_slots=s[14], bundles=s[15])
 
     def select(self, active) -> None:
         """Schedule and upload only the stages whose flag is set."""
