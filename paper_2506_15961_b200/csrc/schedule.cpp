@@ -24,6 +24,7 @@
 #include "schedule.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <deque>
@@ -227,7 +228,16 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
   // o.bmax; false if the value file cannot hold even its temporaries.
   static const uint32_t leaf_window =
       getenv("PQW_LEAF_WINDOW") ? (uint32_t)atoi(getenv("PQW_LEAF_WINDOW")) : 0;
+  static const bool timing = getenv("PQW_TIMING") != nullptr && getenv("PQW_TIMING_BACKEND") != nullptr;
   auto try_once = [&](const SchedOptions& o, Program& prog) -> bool {
+    auto tb0 = std::chrono::steady_clock::now();
+    auto blap = [&](const char* what) {
+      if (!timing || N < 10000) return;
+      const auto t = std::chrono::steady_clock::now();
+      fprintf(stderr, "PQW_TIMING back end %u units: %s %.1f ms\n", N, what,
+              std::chrono::duration<double, std::milli>(t - tb0).count());
+      tb0 = t;
+    };
     // ---- 1. list scheduling -------------------------------------------------
     std::vector<uint64_t> fin(N, 0), F1(N, 0), F2(N, 0);
     std::vector<int32_t> wof(N, -1), W1(N, -1);
@@ -365,6 +375,7 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
       return vdef[a] != vdef[b] ? vdef[a] < vdef[b] : a < b;
     });
 
+    blap("list scheduling");
     // ---- 2. allocation: choose spills, then colour exactly -------------------
     const uint32_t K = o.smem_slots;
     // the distinct bundles reading each value (CSR)
@@ -396,33 +407,56 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
     };
     // slots the exact colouring below will need for a spill choice: the most
     // shared-memory intervals alive at once (a slot frees strictly after its
-    // interval's end), without building the intervals themselves
-    std::vector<uint64_t> events;
+    // interval's end), without building the intervals themselves. Every
+    // interval endpoint is 4 Z + r, r in {0, 1}, with Z a bundle's start
+    // (start * NW + warp) or finish (finish * NW) key; numbering the distinct
+    // Z keeps the order, so a difference array over 2 * |Z| points replaces
+    // sorting the endpoints (same count: an interval [a, b] covers a..b).
+    std::vector<uint64_t> zkey;
+    zkey.reserve(2 * NB);
+    for (uint32_t b = 0; b < NB; ++b) {
+      zkey.push_back(bundles[b].start * NW + bundles[b].warp);
+      zkey.push_back(bundles[b].finish * NW);
+    }
+    std::sort(zkey.begin(), zkey.end());
+    zkey.erase(std::unique(zkey.begin(), zkey.end()), zkey.end());
+    auto zrank = [&](uint64_t z) {
+      return (uint32_t)(std::lower_bound(zkey.begin(), zkey.end(), z) - zkey.begin());
+    };
+    std::vector<uint32_t> p_start(NB), p_fin(NB);  // point index of bts(b) - 1 and of rend(b)
+    for (uint32_t b = 0; b < NB; ++b) {
+      p_start[b] = 2 * zrank(bundles[b].start * NW + bundles[b].warp);
+      p_fin[b] = 2 * zrank(bundles[b].finish * NW);
+    }
+    std::vector<uint32_t> p_vend(N, 0);  // point of vend: the latest reader's rend
+    for (uint32_t v : values) {
+      uint32_t best = p_fin[bundle_of[v]];
+      for (uint32_t i = cons_off[v]; i < cons_off[v + 1]; ++i) best = std::max(best, p_fin[bundle_of[cons[i]]]);
+      p_vend[v] = best;
+    }
+    std::vector<int32_t> cover(2 * zkey.size() + 2);
     auto slots_needed = [&](const std::vector<uint8_t>& spilled) -> uint32_t {
-      events.clear();
-      auto add = [&](uint64_t a, uint64_t b) {  // [a, b]; a start sorts before an end at the same time
-        events.push_back(a << 1);
-        events.push_back((b << 1) | 1);
+      std::fill(cover.begin(), cover.end(), 0);
+      auto add = [&](uint32_t a, uint32_t b) {  // points a..b
+        cover[a]++;
+        cover[b + 1]--;
       };
       for (uint32_t v : values) {
         const uint32_t bdef = bundle_of[v];
         if (!spilled[v]) {
-          add(vdef[v], vend[v]);
+          add(p_start[bdef] + 1, p_vend[v]);  // [vdef, vend]
         } else {
-          if (!remat_ok(v)) add(vdef[v], rend(bdef) + 1);
-          for (uint32_t i = rdb_off[v]; i < rdb_off[v + 1]; ++i) add(bts[rdb[i]] - 1, rend(rdb[i]));
+          if (!remat_ok(v)) add(p_start[bdef] + 1, p_fin[bdef] + 1);  // [vdef, rend(bdef) + 1]
+          for (uint32_t i = rdb_off[v]; i < rdb_off[v + 1]; ++i)
+            add(p_start[rdb[i]], p_fin[rdb[i]]);  // [bts - 1, rend]
         }
       }
-      std::sort(events.begin(), events.end());
-      uint32_t live = 0, most = 0;
-      for (uint64_t e : events) {
-        if (e & 1) {
-          --live;
-        } else {
-          most = std::max(most, ++live);
-        }
+      int32_t live = 0, most = 0;
+      for (int32_t c : cover) {
+        live += c;
+        most = std::max(most, live);
       }
-      return most;
+      return (uint32_t)most;
     };
     // spill choice for `keff` resident values: sweep in definition order
     // keeping at most keff values resident; when full, the resident value (or
@@ -638,6 +672,7 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
                 (unsigned long long)fl_loc, n_gm);
       }
 
+      blap("allocation");
       // ---- 3. synchronisation -------------------------------------------------
       const uint32_t NE = (uint32_t)ex.size();
       std::vector<std::vector<uint32_t>> stream(NW);
@@ -705,6 +740,7 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
         }
       }
 
+      blap("synchronisation");
       // ---- 4. emission ------------------------------------------------------------
       prog = Program{};
       auto& code = prog.code;
@@ -860,6 +896,7 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
         }
         code.push_back(pqw_ins{I_END, 0, 0, 0});
       }
+      blap("emission");
       prog.n_slots = n_sm;
       prog.n_spill = n_gm;
       prog.n_bundles = NB;
