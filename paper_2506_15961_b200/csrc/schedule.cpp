@@ -28,6 +28,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <deque>
+#include <memory>
 #include <queue>
 #include <set>
 #include <stdexcept>
@@ -91,10 +92,55 @@ struct Exec {             // one instruction bundle of a warp stream
   uint32_t seq = 0;       // position in the warp's stream
 };
 
+// Reader list of an interval: almost every interval has one to three readers
+// (a fill temporary exactly one), so they live inline; longer lists spill to
+// the heap. Tens of thousands of intervals per large program made the
+// per-interval std::vector allocations a visible part of the back end.
+struct Readers {
+  static constexpr uint32_t INL = 3;
+  uint32_t n = 0, cap = INL;
+  uint32_t inl[INL];
+  std::unique_ptr<uint32_t[]> heap;
+  Readers() = default;
+  Readers(std::initializer_list<uint32_t> l) {
+    for (uint32_t x : l) push_back(x);
+  }
+  Readers(Readers&& o) noexcept : n(o.n), cap(o.cap), heap(std::move(o.heap)) {
+    std::copy(o.inl, o.inl + INL, inl);
+    o.n = 0;
+    o.cap = INL;
+  }
+  Readers& operator=(Readers&& o) noexcept {
+    n = o.n;
+    cap = o.cap;
+    heap = std::move(o.heap);
+    std::copy(o.inl, o.inl + INL, inl);
+    o.n = 0;
+    o.cap = INL;
+    return *this;
+  }
+  uint32_t* data() { return heap ? heap.get() : inl; }
+  const uint32_t* data() const { return heap ? heap.get() : inl; }
+  void push_back(uint32_t x) {
+    if (n == cap) {
+      std::unique_ptr<uint32_t[]> h(new uint32_t[2 * cap]);
+      std::copy(data(), data() + n, h.get());
+      heap = std::move(h);
+      cap *= 2;
+    }
+    data()[n++] = x;
+  }
+  bool empty() const { return n == 0; }
+  uint32_t size() const { return n; }
+  uint32_t operator[](uint32_t i) const { return data()[i]; }
+  const uint32_t* begin() const { return data(); }
+  const uint32_t* end() const { return data() + n; }
+};
+
 struct Interval {
   uint64_t start, end;
   uint32_t writer;        // exec id
-  std::vector<uint32_t> readers;  // exec ids
+  Readers readers;        // exec ids
   uint32_t slot = 0;
 };
 
@@ -549,6 +595,8 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
           }
         }
       }
+      if (timing && N >= 10000) fprintf(stderr, "PQW_TIMING back end %u units: reserve search %u tries\n", N, tries + 1);
+      blap("reserve search");
       // exec bundles: [FILL] main [SPILL] per main bundle
       std::vector<Exec> ex;
       std::vector<int32_t> fill_of(NB, -1), spill_of(NB, -1), main_exec(NB, -1);
@@ -630,6 +678,7 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
       if (n_sm > K) fail("internal: colouring needs more slots than the interval count");
       owners(gm, g_own, g_wr);
       const uint32_t n_gm = colour(gm, gprev, g_own, g_wr, NW);
+      blap("intervals + colouring");
       if (getenv("PQW_DEBUG_QUAD")) {
         // slot-time of shared intervals whose writer and readers share a quadrant
         uint64_t tot = 0, loc = 0, nloc = 0, same_warp = 0;
