@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libplaneq_witness.so")
 SOURCES = ["compiler.cpp", "schedule.cpp", "plan.cpp", "witness_kernel.cu"]
-HEADERS = ["compiler.hpp", "field.hpp", "isa.hpp", "schedule.hpp", "interp.cuh"]
+HEADERS = ["compiler.hpp", "field.hpp", "isa.hpp", "pool.hpp", "schedule.hpp", "interp.cuh"]
 
 
 def _stale() -> bool:

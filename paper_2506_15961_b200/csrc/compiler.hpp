@@ -1,5 +1,6 @@
 // compiler.hpp -- host-side stage compiler: tensor-op program -> v4 F_p program.
 #pragma once
+#include "pool.hpp"
 #include <stdint.h>
 
 #include <algorithm>
@@ -77,13 +78,9 @@ void host_parallel_for(size_t n, F&& f) {
   const unsigned nt =
       (unsigned)std::min<size_t>(n, std::max(1u, std::thread::hardware_concurrency()));
   std::atomic<size_t> next{0};
-  auto work = [&] {
+  run_on_threads(nt, [&](unsigned) {
     for (size_t i; (i = next.fetch_add(1)) < n;) f(i);
-  };
-  std::vector<std::thread> pool;
-  for (unsigned t = 1; t < nt; ++t) pool.emplace_back(work);
-  work();
-  for (auto& t : pool) t.join();
+  });
 }
 
 // Variables (stage-relative indices) in the cone of obligation `obl`.

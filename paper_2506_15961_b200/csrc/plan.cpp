@@ -37,6 +37,7 @@
 
 #include "../../include/planeq_witness.h"
 #include "field.hpp"
+#include "pool.hpp"
 
 namespace pqw {
 int set_last_error(int code, const std::string& msg);  // witness_kernel.cu (pqw_last_error)
@@ -129,17 +130,13 @@ template <class F>
 void parallel_for(size_t n, F&& f) {
   const unsigned nt = host_threads(n);
   std::atomic<size_t> next{0};
-  auto work = [&](unsigned tid) {
+  run_on_threads(nt, [&](unsigned tid) {
     for (;;) {
       const size_t i = next.fetch_add(1);
       if (i >= n) return;
       f(i, tid);
     }
-  };
-  std::vector<std::thread> pool;
-  for (unsigned t = 1; t < nt; ++t) pool.emplace_back(work, t);
-  work(0);
-  for (auto& t : pool) t.join();
+  });
 }
 
 template <class T, class A>

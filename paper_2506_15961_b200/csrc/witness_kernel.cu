@@ -262,10 +262,7 @@ static int finalize_all(pqw_engine* e) {
       }
     }
   };
-  std::vector<std::thread> pool;
-  for (unsigned t = 1; t < nt; ++t) pool.emplace_back(work);
-  work();
-  for (auto& t : pool) t.join();
+  pqw::run_on_threads(nt, [&](unsigned) { work(); });
   if (!err.empty()) return fail(PQW_EINVAL, std::string("stage compile: ") + err);
   return PQW_OK;
 }
@@ -479,10 +476,7 @@ static int finalize_front(pqw_engine* e) {
       }
     }
   };
-  std::vector<std::thread> pool;
-  for (unsigned t = 1; t < nt; ++t) pool.emplace_back(work);
-  work();
-  for (auto& t : pool) t.join();
+  pqw::run_on_threads(nt, [&](unsigned) { work(); });
   if (timing)
     fprintf(stderr, "PQW_TIMING front ends %zu programs %.1f ms (largest %zu words)\n", todo.size(),
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_front)
