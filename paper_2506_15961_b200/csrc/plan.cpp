@@ -742,6 +742,35 @@ bool validate_graph(const GraphData& g, std::string& why) {
   }
   // dangling inputs (graph.py topo_sort) and cycles
   const size_t n = g.nn();
+  // Fast path: when every producer precedes its consumer in node order (a
+  // graph built front to back), there is no cycle; only dangling inputs need
+  // looking for. One parallel pass instead of the serial Kahn sweep below.
+  {
+    std::atomic<int> state{0};  // 0 forward, 1 dangling, 2 a backward edge
+    const size_t chunk = 16384;
+    parallel_for((n + chunk - 1) / chunk, [&](size_t c, unsigned) {
+      for (size_t v = c * chunk; v < std::min(n, (c + 1) * chunk); ++v)
+        for (int64_t j = g.in_off[v]; j < g.in_off[v + 1]; ++j) {
+          const int32_t t = g.ins[j];
+          if (g.is_input[t]) continue;
+          const int32_t src = g.producer[t];
+          if (src < 0) {
+            state.store(1);
+            return;
+          }
+          if ((size_t)src >= v) {
+            int expect = 0;
+            state.compare_exchange_strong(expect, 2);
+          }
+        }
+    });
+    if (state.load() == 1) {
+      why = "dangling tensor";
+      return false;
+    }
+    if (state.load() == 0) goto shapes;
+  }
+  {
   // successor lists in CSR form (no per-node allocation)
   std::vector<int32_t> indeg(n, 0), soff(n + 1, 0);
   for (size_t v = 0; v < n; ++v)
@@ -781,6 +810,8 @@ bool validate_graph(const GraphData& g, std::string& why) {
       return false;
     }
   }
+  }
+shapes:
   auto same_shape = [&](int32_t a, int32_t b) {
     const int64_t la = g.dim_off[a + 1] - g.dim_off[a], lb = g.dim_off[b + 1] - g.dim_off[b];
     return la == lb && std::equal(g.dims.begin() + g.dim_off[a], g.dims.begin() + g.dim_off[a + 1],
