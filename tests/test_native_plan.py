@@ -50,7 +50,22 @@ def _python_ok(fn, *a):
 
 @pytest.mark.parametrize("name,rel", PLANS, ids=[n for n, _ in PLANS])
 def test_native_stages_and_programs_match_host(lib, name, rel):
+    _check_against_host(load_plan(rel), name)
+
+
+@pytest.mark.parametrize("name,rel", PLANS[:6], ids=[n for n, _ in PLANS[:6]])
+def test_native_core_on_back_to_front_node_order(lib, name, rel):
+    """Both graphs' node lists reversed (still acyclic, but producers now follow
+    their consumers): the validation and slice-order fast paths for
+    front-to-back graphs do not apply, and the stages and programs still equal
+    the host's."""
     plan = load_plan(rel)
+    plan.logical.nodes.reverse()
+    plan.parallel.nodes.reverse()
+    _check_against_host(plan, name)
+
+
+def _check_against_host(plan, name):
     nat = NativePlan(plan)
     ok_py = all(_python_ok(validate_concrete, g)[0] for g in (plan.logical, plan.parallel))
     assert nat.validate() == ok_py, name
