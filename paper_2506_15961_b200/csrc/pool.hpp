@@ -9,8 +9,12 @@
 // host thread) gets `false` back and starts its own threads as before.
 #pragma once
 
+#include <unistd.h>
+
+#include <atomic>
 #include <condition_variable>
 #include <cstdint>
+#include <cstdlib>
 #include <functional>
 #include <mutex>
 #include <thread>
@@ -70,9 +74,19 @@ class HostPool {
 };
 
 // The process-wide pool (never destroyed: its detached workers stay parked
-// until the process exits).
+// until the process exits). A forked child has none of the parent's workers
+// (and may have inherited a held lock), so a process whose pid differs from
+// the pool's creator gets a pool of its own.
 inline HostPool& host_pool() {
-  static HostPool* p = new HostPool();
+  static std::atomic<HostPool*> pool{nullptr};
+  static std::atomic<pid_t> owner{0};
+  const pid_t me = getpid();
+  HostPool* p = pool.load(std::memory_order_acquire);
+  if (p == nullptr || owner.load(std::memory_order_acquire) != me) {
+    p = new HostPool();  // a replaced pool is left alone (its users may still hold it)
+    pool.store(p, std::memory_order_release);
+    owner.store(me, std::memory_order_release);
+  }
   return *p;
 }
 
@@ -82,7 +96,8 @@ inline void run_on_threads(unsigned nt, const std::function<void(unsigned)>& bod
     body(0);
     return;
   }
-  if (host_pool().run(nt, body)) return;
+  static const bool no_pool = std::getenv("PQW_NO_POOL") != nullptr;  // A/B switch
+  if (!no_pool && host_pool().run(nt, body)) return;
   std::vector<std::thread> extra;
   for (unsigned t = 1; t < nt; ++t) extra.emplace_back(body, t);
   body(0);

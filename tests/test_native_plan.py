@@ -321,3 +321,40 @@ def test_batched_queue_dedups_like_per_stage_add(lib):
     for e in (one, batch, split):
         e.close()
     nat.close()
+
+
+def test_native_core_in_a_forked_child(lib, monkeypatch):
+    """The library's host thread pool does not survive fork(); a child process
+    (e.g. a fork-based worker pool around verify_plan) gets a pool of its own
+    instead of waiting on the parent's workers forever."""
+    import signal
+    import time
+    monkeypatch.setenv("PQW_THREADS", "4")
+    plan = _base()
+
+    def run():
+        nat = NativePlan(plan)
+        ok = nat.validate() and nat.build_stages()
+        n = nat.n_stages
+        nat.close()
+        return ok, n
+
+    want = run()  # the parent's pool now has parked workers
+    pid = os.fork()
+    if pid == 0:  # child: must finish, with the same stages
+        signal.alarm(60)
+        try:
+            os._exit(0 if run() == want else 1)
+        except BaseException:  # noqa: BLE001
+            os._exit(2)
+    deadline = time.time() + 90
+    while True:
+        done, status = os.waitpid(pid, os.WNOHANG)
+        if done:
+            break
+        if time.time() > deadline:
+            os.kill(pid, signal.SIGKILL)
+            os.waitpid(pid, 0)
+            raise AssertionError("native core hung in a forked child")
+        time.sleep(0.05)
+    assert os.WIFEXITED(status) and os.WEXITSTATUS(status) == 0, status
