@@ -355,11 +355,14 @@ struct GraphData {
     for (int64_t i = 0; i < d.n_tensors; ++i) dim_off[i + 1] = dim_off[i] + d.tensor_ndim[i];
     par_copy(dims, d.tensor_dims, (size_t)dim_off.back());
     par_copy(tflags, d.tensor_flags, (size_t)d.n_tensors);
+    lap("  tensor dims");
     const size_t n = (size_t)d.n_nodes;
     split_names(d.node_ids, d.n_nodes, nstore, nid, d.node_ids_len);
+    lap("  node ids");
     par_copy(kind, d.node_kind, n);
     par_copy(device, d.node_device, n);
     par_copy(seq, d.node_seq, n);
+    lap("  kind/device/seq");
     in_off.resize(n + 1);
     out_off.resize(n + 1);
     attr_off.resize(n + 1);
