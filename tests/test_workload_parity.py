@@ -207,5 +207,10 @@ def test_full_405b_stage_verdicts_match_reference_prefix(gpu, rec):
     got = [(s["target"], s["status"]) for s in rep["stages"]]
     want = [tuple(x) for x in rec["stage_status"]]
     idx = rec.get("stage_index") or list(range(len(want)))
-    assert [got[i] for i in idx] == want
+    assert [got[i][0] for i in idx] == [t for t, _ in want]
+    for i, (target, status) in zip(idx, want):
+        if status in ("proven", "refuted"):
+            assert got[i][1] == status, target
+        else:  # the reference itself did not decide (timeout / error): ours must
+            assert got[i][1] in ("proven", "refuted"), target
     assert rep["verdict"] == "proven"
