@@ -20,6 +20,9 @@
  * pqw_last_error() describes the last failure on the calling thread. An engine
  * is not thread-safe: call it from one thread at a time (it parallelises its
  * own compilation internally). Engines on different devices are independent.
+ * The library's parallel loops share one pool of host threads (PQW_THREADS
+ * caps them) that stay parked between calls; a loop started while another
+ * holds the pool, or in a forked child, runs on threads of its own.
  * No torch types cross this boundary: plain pointers and sizes only.
  */
 #ifndef PLANEQ_WITNESS_H
