@@ -15,6 +15,7 @@
 #include <condition_variable>
 #include <cstdint>
 #include <cstdlib>
+#include <exception>
 #include <functional>
 #include <mutex>
 #include <thread>
@@ -41,10 +42,18 @@ class HostPool {
       ++gen_;
     }
     cv_.notify_all();
-    body(0);
-    std::unique_lock<std::mutex> g(mu_);
-    done_.wait(g, [&] { return pending_ == 0; });
-    body_ = nullptr;
+    std::exception_ptr err;
+    try {
+      body(0);
+    } catch (...) {  // the workers still use the caller's frame: wait for them first
+      err = std::current_exception();
+    }
+    {
+      std::unique_lock<std::mutex> g(mu_);
+      done_.wait(g, [&] { return pending_ == 0; });
+      body_ = nullptr;
+    }
+    if (err) std::rethrow_exception(err);
     return true;
   }
 
