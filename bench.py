@@ -385,6 +385,11 @@ def main():
                          "peak": round(peak / 1e9, 3), "unit": "Gfieldop/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic_bytes(args, desc),
                          "traffic_source": "profiles/traffic.json (ncu --set full, same workload)",
+                         "traffic_model": int(stats.get("h2d_bytes", 0)),
+                         "traffic_model_source": "this run's device image (code, variable keys, "
+                                                 "stage table) that one launch reads: each byte "
+                                                 "from DRAM once, then L2-resident; the L2 flush "
+                                                 "between steps makes every launch re-read it",
                          "peak_source": "measured register-resident F_p mul/add/hash/inv kernels "
                                         "(pqw_peak_fieldops) weighted by this image's op mix",
                          "field_ops_per_witness": {k: int(v) for k, v in fo.items()},
