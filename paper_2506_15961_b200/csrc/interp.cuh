@@ -435,7 +435,8 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
     // through the jump table
     const uint32_t kx = h.x >> 16;
     if (op == I_WAIT) {
-      wait_progress(p, prog + h.z, h.w);
+      wait_progress(p, prog + (h.z >> 24) - 1, h.z & 0xFFFFFFu);
+      if (h.w) wait_progress(p, prog + (h.w >> 24) - 1, h.w & 0xFFFFFFu);
     } else if (op == I_DOT && kx == 1) {
       pc = run_elementwise<2>(cr, pc, n, sb, [](const uint32_t* x) { return fmul(x[0], x[1]); });
     } else if (op == I_FILL) {
@@ -556,8 +557,9 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
         pc = h_spill(cr, pc, n, sb, gl);
         break;
       case I_WAIT:
-        // header: z = producer warp, w = progress it must have published
-        wait_progress(p, prog + h.z, h.w);
+        // up to two waits, (producer warp + 1) << 24 | progress in z and w
+        wait_progress(p, prog + (h.z >> 24) - 1, h.z & 0xFFFFFFu);
+        if (h.w) wait_progress(p, prog + (h.w >> 24) - 1, h.w & 0xFFFFFFu);
         break;
       default:
         __builtin_unreachable();

@@ -34,7 +34,7 @@ def fields(op: str, k: int) -> int:
 def decode(code: np.ndarray, n_warps: int) -> list[list[tuple]]:
     """Per warp: list of (op, fn, k, aux, signal, cols) where cols[f] is the u32
     array of field f over the bundle's n ops and signal the progress published
-    after the bundle (header.w; for WAIT: the progress waited for)."""
+    after the bundle (header.w; for WAIT: a second wait, 0 for none)."""
     flat = code.reshape(-1)
     out = []
     for w in range(n_warps):
@@ -93,8 +93,9 @@ def run(code: np.ndarray, n_slots: int, var_keys: np.ndarray, var_base: int, see
         op, fn, k, aux, sig, cols = streams[w][pc[w]]
         if op == "END":
             return False
-        if op == "WAIT":
-            return prog[aux] >= sig
+        if op == "WAIT":  # up to two waits: (warp + 1) << 24 | progress
+            ok = prog[(aux >> 24) - 1] >= (aux & 0xFFFFFF)
+            return ok and (not sig or prog[(sig >> 24) - 1] >= (sig & 0xFFFFFF))
         if aux:  # a wait folded into the bundle header
             return prog[(aux >> 24) - 1] >= (aux & 0xFFFFFF)
         return True
