@@ -557,9 +557,10 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
         pc = h_spill(cr, pc, n, sb, gl);
         break;
       case I_WAIT:
-        // up to two waits, (producer warp + 1) << 24 | progress in z and w
+        // up to three waits, (producer warp + 1) << 24 | progress in z, w, y
         wait_progress(p, prog + (h.z >> 24) - 1, h.z & 0xFFFFFFu);
         if (h.w) wait_progress(p, prog + (h.w >> 24) - 1, h.w & 0xFFFFFFu);
+        if (h.y) wait_progress(p, prog + (h.y >> 24) - 1, h.y & 0xFFFFFFu);
         break;
       default:
         __builtin_unreachable();
@@ -577,7 +578,7 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
       if (lane == 0) {
         unsigned long long* c = p.prof + 8 + 4 * cls;
         atomicAdd(c + 0, (unsigned long long)(t_now - t_start));   // bundle cycles
-        atomicAdd(c + 1, (unsigned long long)((n + 7) / 8));        // groups
+        atomicAdd(c + 1, (unsigned long long)(op == I_WAIT ? 0 : (n + 7) / 8));  // groups
         atomicAdd(c + 2, 1ull);                                     // bundles
         atomicAdd(c + 3, (unsigned long long)(t_start - t_end));    // dispatch cycles
       }

@@ -11,8 +11,8 @@
 //   header.x = op | fn << 8 | k << 16,  header.y = n (ops in the bundle),
 //   header.z = a wait folded into the bundle ((warp + 1) << 24 | progress; 0:
 //   none), header.w = progress this warp publishes after the bundle (0: none)
-//   -- a WAIT instruction carries up to two waits in that encoding, z and w
-//   ((producer warp + 1) << 24 | progress; w = 0: only one).
+//   -- a WAIT instruction carries up to three waits in that encoding, in z, w
+//   and y ((producer warp + 1) << 24 | progress; 0 in w or y: none there).
 // A bundle holds n independent ops of one kind. Its payload is ceil(n / 8)
 // groups; a group lists, field by field, 8 u32 values (two records) for the 8
 // ops of the group (unused entries of the last group are 0):

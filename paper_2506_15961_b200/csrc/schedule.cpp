@@ -821,16 +821,17 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
         reinterpret_cast<uint32_t*>(code.data())[w] = (uint32_t)code.size();
         for (uint32_t e : stream[w]) {
           const Exec& E = ex[e];
-          // all but the last wait become WAIT instructions, two per instruction;
+          // all but the last wait become WAIT instructions, three per instruction;
           // the last one rides in the bundle header: each (warp + 1) << 24 | count
           const size_t nwait = waits[e].size();
           auto enc = [](const std::pair<uint32_t, uint32_t>& wt) -> uint32_t {
             if (wt.second >= (1u << 24)) fail("stream too long for a folded wait");
             return ((wt.first + 1) << 24) | wt.second;
           };
-          for (size_t i = 0; i + 1 < nwait; i += 2) {
+          for (size_t i = 0; i + 1 < nwait; i += 3) {
             const uint32_t second = i + 2 < nwait ? enc(waits[e][i + 1]) : 0u;
-            code.push_back(pqw_ins{isa_header(I_WAIT, 0, 0), 0, enc(waits[e][i]), second});
+            const uint32_t third = i + 3 < nwait ? enc(waits[e][i + 2]) : 0u;
+            code.push_back(pqw_ins{isa_header(I_WAIT, 0, 0), third, enc(waits[e][i]), second});
             prog.op_hist[I_WAIT]++;
           }
           prog.n_waits += (uint32_t)nwait;

@@ -34,7 +34,8 @@ def fields(op: str, k: int) -> int:
 def decode(code: np.ndarray, n_warps: int) -> list[list[tuple]]:
     """Per warp: list of (op, fn, k, aux, signal, cols) where cols[f] is the u32
     array of field f over the bundle's n ops and signal the progress published
-    after the bundle (header.w; for WAIT: a second wait, 0 for none)."""
+    after the bundle (header.w; for WAIT: a second wait, 0 for none; a WAIT's
+    third wait, header.y, is returned as k)."""
     flat = code.reshape(-1)
     out = []
     for w in range(n_warps):
@@ -49,6 +50,8 @@ def decode(code: np.ndarray, n_warps: int) -> list[list[tuple]]:
             n = int(h[1])
             aux = int(h[2])
             sig = int(h[3])
+            if op == "WAIT":  # header.y of a WAIT is its third wait, not an op count
+                k, n = n, 0
             nf = fields(op, k)
             ng = (n + GROUP - 1) // GROUP
             cols = [np.zeros(ng * GROUP, dtype=np.int64) for _ in range(nf)]
@@ -93,9 +96,8 @@ def run(code: np.ndarray, n_slots: int, var_keys: np.ndarray, var_base: int, see
         op, fn, k, aux, sig, cols = streams[w][pc[w]]
         if op == "END":
             return False
-        if op == "WAIT":  # up to two waits: (warp + 1) << 24 | progress
-            ok = prog[(aux >> 24) - 1] >= (aux & 0xFFFFFF)
-            return ok and (not sig or prog[(sig >> 24) - 1] >= (sig & 0xFFFFFF))
+        if op == "WAIT":  # up to three waits (aux, sig, k): (warp + 1) << 24 | progress
+            return all(not x or prog[(x >> 24) - 1] >= (x & 0xFFFFFF) for x in (aux, sig, k))
         if aux:  # a wait folded into the bundle header
             return prog[(aux >> 24) - 1] >= (aux & 0xFFFFFF)
         return True
