@@ -420,9 +420,11 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
     const uint4 h = cr.rec(pc);
     ++pc;
     const uint32_t op = h.x & 0xFFu;
-    const uint32_t n = h.y;
-    if (op != I_WAIT && h.z)  // a wait folded into the bundle header
+    const uint32_t n = h.y & 0x1FFFu;
+    if (op != I_WAIT && h.z) {  // one or two waits folded into the bundle header
       wait_progress(p, prog + (h.z >> 24) - 1, h.z & 0xFFFFFFu);
+      if (h.y >> 13) wait_progress(p, prog + (h.y >> 26) - 1, (h.y >> 13) & 0x1FFFu);
+    }
 #ifdef PQW_PROF
     const long long t_start = clock64();
     const uint32_t kk = h.x >> 16;

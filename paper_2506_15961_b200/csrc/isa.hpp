@@ -8,7 +8,8 @@
 // out of one shared value file.
 //
 // Instruction = one header record + payload records.
-//   header.x = op | fn << 8 | k << 16,  header.y = n (ops in the bundle),
+//   header.x = op | fn << 8 | k << 16,  header.y = n (ops in the bundle, low
+//   13 bits) | a second folded wait << 13 ((warp + 1) << 13 | progress < 2^13),
 //   header.z = a wait folded into the bundle ((warp + 1) << 24 | progress; 0:
 //   none), header.w = progress this warp publishes after the bundle (0: none)
 //   -- a WAIT instruction carries up to three waits in that encoding, in z, w

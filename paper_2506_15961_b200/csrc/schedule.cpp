@@ -828,9 +828,13 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
             if (wt.second >= (1u << 24)) fail("stream too long for a folded wait");
             return ((wt.first + 1) << 24) | wt.second;
           };
-          for (size_t i = 0; i + 1 < nwait; i += 3) {
-            const uint32_t second = i + 2 < nwait ? enc(waits[e][i + 1]) : 0u;
-            const uint32_t third = i + 3 < nwait ? enc(waits[e][i + 2]) : 0u;
+          // the second-to-last wait also rides in the header (y >> 13) when its
+          // count fits 13 bits (and the bundle's n fits the low 13)
+          const bool fold2 = nwait >= 2 && waits[e][nwait - 2].second < (1u << 13);
+          const size_t n_instr_waits = nwait - (nwait ? 1 : 0) - (fold2 ? 1 : 0);
+          for (size_t i = 0; i < n_instr_waits; i += 3) {
+            const uint32_t second = i + 1 < n_instr_waits ? enc(waits[e][i + 1]) : 0u;
+            const uint32_t third = i + 2 < n_instr_waits ? enc(waits[e][i + 2]) : 0u;
             code.push_back(pqw_ins{isa_header(I_WAIT, 0, 0), third, enc(waits[e][i]), second});
             prog.op_hist[I_WAIT]++;
           }
@@ -942,6 +946,17 @@ Program schedule_program(const Dag& dag, const SchedOptions& opt) {
             const auto& pr = waits[e][nwait - 1];
             if (pr.second >= (1u << 24)) fail("stream too long for a folded wait");
             code[hdr].a = ((pr.first + 1) << 24) | pr.second;
+          }
+          if (fold2) {
+            const auto& pr = waits[e][nwait - 2];
+            if (code[hdr].dst < (1u << 13)) {
+              code[hdr].dst |= (((pr.first + 1) << 13) | pr.second) << 13;
+            } else {  // n too large to share the word: a WAIT instruction after all
+              code.insert(code.begin() + (ptrdiff_t)hdr,
+                          pqw_ins{isa_header(I_WAIT, 0, 0), 0, enc(pr), 0});
+              prog.op_hist[I_WAIT]++;
+              ++last_hdr;
+            }
           }
           if (signal_after[e]) {
             code[last_hdr].b = E.seq + 1;  // header.w: publish progress after this exec

@@ -52,6 +52,10 @@ def decode(code: np.ndarray, n_warps: int) -> list[list[tuple]]:
             sig = int(h[3])
             if op == "WAIT":  # header.y of a WAIT is its third wait, not an op count
                 k, n = n, 0
+            elif n >> 13:  # a second folded wait in header.y >> 13: (warp + 1) << 13 | count
+                w2 = n >> 13
+                aux = [aux, ((w2 >> 13) << 24) | (w2 & 0x1FFF)]
+                n &= 0x1FFF
             nf = fields(op, k)
             ng = (n + GROUP - 1) // GROUP
             cols = [np.zeros(ng * GROUP, dtype=np.int64) for _ in range(nf)]
@@ -98,8 +102,9 @@ def run(code: np.ndarray, n_slots: int, var_keys: np.ndarray, var_base: int, see
             return False
         if op == "WAIT":  # up to three waits (aux, sig, k): (warp + 1) << 24 | progress
             return all(not x or prog[(x >> 24) - 1] >= (x & 0xFFFFFF) for x in (aux, sig, k))
-        if aux:  # a wait folded into the bundle header
-            return prog[(aux >> 24) - 1] >= (aux & 0xFFFFFF)
+        if aux:  # one or two waits folded into the bundle header
+            return all(prog[(a >> 24) - 1] >= (a & 0xFFFFFF)
+                       for a in (aux if isinstance(aux, list) else [aux]))
         return True
 
     def step(w):
