@@ -1273,19 +1273,36 @@ CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* con
   // ---- back end: DAG of scheduling units in depth-first priority order -------
   auto dag = std::make_shared<Dag>();
   {
-    const size_t G = E.groups.size();
+    const size_t G0 = E.groups.size();
+    // A guarded inversion's batch product is zero exactly when one of its
+    // operands is (F_p has no zero divisors), so its bundle checks those
+    // denominators itself (fn = 1): the DEN units of values that a guarded
+    // inversion in this DAG takes are dropped (one dispatch fewer each).
+    std::vector<uint8_t> inv_checked(B.vals.size(), 0);
+    for (size_t g = 0; g < G0; ++g) {
+      const auto& gr = E.groups[g];
+      if (gr.kind != 0) continue;
+      const Val& v = B.vals[gr.v];
+      if (v.kind != K_CONST && v.kind != K_VAR && v.op == O_INV && (B.vals[v.a].flags & F_DEN))
+        inv_checked[v.a] = 1;
+    }
+    std::vector<uint32_t> keep;
+    keep.reserve(G0);
+    for (size_t g = 0; g < G0; ++g)
+      if (!(E.groups[g].kind == 2 && inv_checked[E.groups[g].v])) keep.push_back((uint32_t)g);
+    const size_t G = keep.size();
     std::vector<int32_t> unit_of(B.vals.size(), -1);
-    for (size_t g = 0; g < G; ++g)
-      if (E.groups[g].kind == 0) unit_of[E.groups[g].v] = (int32_t)g;
+    for (size_t u = 0; u < G; ++u)
+      if (E.groups[keep[u]].kind == 0) unit_of[E.groups[keep[u]].v] = (int32_t)u;
     auto uof = [&](uint32_t v) -> uint32_t {
       if (unit_of[v] < 0) bad("internal: operand without a defining unit");
       return (uint32_t)unit_of[v];
     };
     std::vector<uint32_t> opnds;
     dag->units.resize(G);
-    for (size_t g = 0; g < G; ++g) {
-      const auto& gr = E.groups[g];
-      DagUnit& d = dag->units[g];
+    for (size_t u = 0; u < G; ++u) {
+      const auto& gr = E.groups[keep[u]];
+      DagUnit& d = dag->units[u];
       d.arg0 = (uint32_t)dag->pool.size();
       if (gr.kind == 1) {
         d.op = I_CHK;
@@ -1317,6 +1334,7 @@ CompiledStage compile_stage(const int32_t* ir, size_t ir_len, const int64_t* con
             case O_INV:
               d.op = I_INV;
               d.guarded = (B.vals[v.a].flags & F_DEN) != 0;  // batch only checked denominators
+              d.fn = d.guarded ? 1u : 0u;  // fn 1: the bundle is the operands' DEN check
               break;
             default: bad("internal: bad value op");
           }

@@ -283,7 +283,8 @@ __device__ __forceinline__ uint32_t run_fill(CodeRing& cr, uint32_t pc, uint32_t
 // local memory) the 405B kernel went 12.76 -> 15.69 ms (A/B s3h).
 #define PQW_COLD __device__ __forceinline__
 
-PQW_COLD uint32_t h_inv(CodeRing& cr, const uint4* stream, uint32_t pc, uint32_t n, uint32_t sb) {
+PQW_COLD uint32_t h_inv(CodeRing& cr, const uint4* stream, uint32_t pc, uint32_t n, uint32_t sb,
+                        bool checks, bool& valid) {
   // Montgomery batch inversion over the bundle: prefix products go to the
   // destination slots, one inversion, then a backward sweep (which reads
   // the payload again from global memory). Every operand is a guarded
@@ -302,6 +303,9 @@ PQW_COLD uint32_t h_inv(CodeRing& cr, const uint4* stream, uint32_t pc, uint32_t
         sts(sb, D.v[i], acc);
       }
   }
+  // fn 1: these operands are guarded denominators whose DEN ops the compiler
+  // dropped -- the product vanishes exactly when one of them does
+  if (checks && acc == 0) valid = false;
   uint32_t inv = finv(acc);
   for (int32_t gi = (int32_t)ng - 1; gi >= 0; --gi) {
     const uint32_t g = (uint32_t)gi * 8u;
@@ -531,7 +535,7 @@ __device__ __forceinline__ void run_stream(const Params& p, const StageDesc& sd,
         break;
       }
       case I_INV:
-        pc = h_inv(cr, stream, pc, n, sb);
+        pc = h_inv(cr, stream, pc, n, sb, ((h.x >> 8) & 0xFFu) != 0, valid);
         break;
       case I_VAR:
         pc = h_var<PROBE>(cr, pc, n, sb, vkeys, w, p.probe_w, p.probe_vars);

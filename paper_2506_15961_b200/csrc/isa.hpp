@@ -20,7 +20,9 @@
 //   DOT k   D, A0, B0, ..., A(k-1), B(k-1)    d = sum_j a_j * b_j  (k = 1: multiply)
 //   SUM k   D, A0, ..., A(k-1)                d = sum_j a_j        (k = 2: add)
 //   SUB     D, A, B        NEG  D, A          HASH fn   D, A       (d = f_fn(a))
-//   INV     D, A           batched: every d_i = a_i^-1 via one inversion
+//   INV     D, A           batched: every d_i = a_i^-1 via one inversion (fn 1: the
+//                          operands are guarded denominators; a zero product
+//                          invalidates the witness, standing in for their DENs)
 //   VAR     D, V (stage-relative var index)   CONST     D, C (residue)
 //   CHK     O (obligation id), A, B           DEN       A
 //   FILL    D, G (global spill slot -> shared)  SPILL   G, A (shared -> global)

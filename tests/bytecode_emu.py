@@ -139,6 +139,8 @@ def run(code: np.ndarray, n_slots: int, var_keys: np.ndarray, var_base: int, see
             for i in range(n):
                 acc = acc * sm[s(cols[1][i])] % P
                 sm[s(cols[0][i])] = acc
+            if fn:  # the guarded operands' DEN check (their DEN ops were dropped)
+                valid &= acc != 0
             inv = m31.inv(acc)
             for i in range(n - 1, 0, -1):
                 prev = sm[s(cols[0][i - 1])].copy()
